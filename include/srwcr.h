@@ -1,0 +1,187 @@
+/*
+ * srwcr.h -- C ABI of the B200-native SRWCR hot path (arXiv 1804.05061).
+ *
+ * The library evaluates, once per quasi-Newton iteration, the spatially
+ * region-weighted correlation ratio D (Eq 9; Table I) between a
+ * fixed image F (the model image A) and the moving image M warped by a cubic
+ * B-spline free-form deformation T(x; Phi) (Eq 17) used as the
+ * estimated image B = M(T(x)) ("moving-as-B"), together with its analytic
+ * gradient dD/dPhi (Eq 15-17 P:180-190 with Eq 27).  It minimises
+ * C = D + w_p C_p (Eq 1) via srwcr_register.
+ *
+ * "P:NNN" cites line NNN of the paper text; readings where the paper is silent or
+ * garbled are numbered c1..c18 in DESIGN.md s3.
+ *
+ * Conventions shared by every entry point
+ *   - Volumes: fp32, x-fastest, [Nz][Ny][Nx]; Nz == 1 means 2-D (reading c16).
+ *   - Intensities are normalised to [0, L] with L = intensity_bins - 1
+ *     unless srwcr_options.inputs_normalized == 1 (reading c1 gives the formula).
+ *   - Control lattice: spacing delta = control_spacing_mm / spacing_mm voxels per
+ *     axis (fp64), G = floor((N-1)/delta) + 4 nodes per axis, node j at voxel
+ *     coordinate (j-1)*delta (Eq 17 indices shifted by +1, reading c15).  In 2-D
+ *     the z axis has G = 1 and no displacement component.
+ *   - Spatial bins (regions, Eq 7): spatial_bins[i] = k cells per axis,
+ *     Delta = N/k, K = k+3 regions per axis (reading c14); k = 0 (or the z axis in
+ *     2-D) is a degenerate axis with K = 4, weights (1,0,0,0): one real region.
+ *   - Params / gradient: fp64 SoA [ndim][Gz][Gy][Gx], displacements in voxels,
+ *     0 = identity.  ndim = 3 (2 in 2-D).
+ *   - Pointers marked "host or device" are classified with
+ *     cudaPointerGetAttributes; device pointers are the fast path.
+ *   - Every call returns a status and never throws.  srwcr_last_error() gives the
+ *     message of the last failing call on that context.  After SRWCR_ECUDA the
+ *     context is poisoned and every later call returns SRWCR_ESTATE.
+ *   - Thread-compatible: one caller at a time per context; distinct contexts are
+ *     independent.
+ */
+#ifndef SRWCR_H
+#define SRWCR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct srwcr_ctx srwcr_ctx; /* opaque; owns all its device memory */
+
+typedef enum {
+    SRWCR_OK = 0,
+    SRWCR_EINVAL = -1,      /* bad argument; the message names it */
+    SRWCR_ENOMEM = -2,      /* host or device allocation failed */
+    SRWCR_ECUDA = -3,       /* CUDA runtime error (context poisoned) */
+    SRWCR_ENCCL = -4,       /* NCCL error or NCCL library not loadable */
+    SRWCR_EDEGENERATE = -5, /* no region passed the retention test (reading c12) */
+    SRWCR_ENOTSUP = -6,     /* option not supported by this build */
+    SRWCR_ESTATE = -7       /* context poisoned by an earlier CUDA error, or call out of order */
+} srwcr_status;
+
+typedef struct {
+    int32_t struct_size;       /* = sizeof(srwcr_options); set by srwcr_default_options */
+    int32_t orientation;       /* 0 = moving image is the estimated image B (Eq 18-19/27).
+                                  1 = moving as model image A (Eq 20-21/31): SRWCR_ENOTSUP */
+    int32_t inputs_normalized; /* 1: fixed/moving already in [0, L]; 0: min-max normalise */
+    int32_t device;            /* CUDA device ordinal */
+    int32_t nranks, rank;      /* z-slab decomposition: rank r owns slab srwcr_plan_slab(r) */
+    const void *nccl_id;       /* nranks > 1: 128-byte ncclUniqueId (broadcast by the caller),
+                                  or NULL for caller-driven exchange (srwcr_eval_begin/end) */
+    double eps_mass;           /* region retained iff p(r) > eps_mass ... (reading c12) */
+    double eps_sigma;          /* ... and sigma_r^2 > eps_sigma (bin^2)                  */
+    int32_t moment_shift;      /* 1 (default): per-fixed-bin shift of the accumulated moments
+                                  estimated at Phi = 0; 0: shift = bin index.  Exact algebra
+                                  either way; it only conditions the fp32 partial sums. */
+    int32_t use_graph;         /* 1 (default): srwcr_eval replays one CUDA graph */
+} srwcr_options;
+
+/* Fills *opt with defaults: orientation 0, inputs_normalized 0, device 0, nranks 1,
+ * rank 0, nccl_id NULL, eps_mass 1e-12, eps_sigma 1e-6, moment_shift 1, use_graph 1. */
+srwcr_status srwcr_default_options(srwcr_options *opt);
+
+/* Create a context: copies F and M (host or device; the caller may free them on
+ * return), normalises them, builds the per-axis B-spline tables (Eq 8, Eq 17),
+ * accumulates the static fixed-image counts N[r][a] = sum_x w_r(x) h(a - F(x))
+ * (Eq 3; they do not depend on Phi in this orientation) and captures the
+ * evaluation graph.
+ *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2
+ *   spacing_mm[3]      voxel spacing (> 0)
+ *   intensity_bins     L + 1, in [2, 256] (paper: L = 31)
+ *   spatial_bins[3]    k cells per axis (>= 0; 0 = one region on that axis)
+ *   control_spacing_mm[3]  control-node spacing (> 0); paper: delta = [5,5,5]
+ *   opt                NULL = defaults
+ * Returns SRWCR_EINVAL on bad geometry, SRWCR_EDEGENERATE if no region can be
+ * retained even at Phi = 0 is NOT an error here (it is reported by srwcr_eval). */
+srwcr_status srwcr_create(srwcr_ctx **out, const float *fixed, const float *moving,
+                          const int64_t dims[3], const double spacing_mm[3], int32_t intensity_bins,
+                          const int32_t spatial_bins[3], const double control_spacing_mm[3],
+                          const srwcr_options *opt);
+
+/* Number of parameters n = ndim * Gx * Gy * Gz and the control grid (Gx, Gy, Gz). */
+srwcr_status srwcr_num_params(const srwcr_ctx *ctx, int64_t *n, int64_t grid_dims[3]);
+
+/* One SRWCR evaluation at params (host or device, fp64, layout above):
+ *   *value = D (Eq 9) on return (host pointer);
+ *   grad   = dD/dPhi (host or device, fp64, same layout as params), or NULL for the
+ *            value only.  With nranks > 1 every rank passes the same params and gets
+ *            the same D and the full gradient.
+ * Returns SRWCR_EDEGENERATE (value = 0, grad = 0) if no region is retained. */
+srwcr_status srwcr_eval(srwcr_ctx *ctx, const double *params, double *value, double *grad);
+
+/* Caller-driven exchange (nranks > 1 and nccl_id == NULL), the same kernels as
+ * srwcr_eval split at the two exchange points of the z-slab decomposition:
+ *   srwcr_eval_begin  uploads params and runs pass 1 on this rank's slab; the
+ *                     rank-partial statistics are then in the buffer given by
+ *                     srwcr_stats_buffer (device, fp64, `count` values) which the
+ *                     caller must sum over ranks in place (e.g. an all-reduce);
+ *   srwcr_eval_end    combines and runs pass 2 on this rank's slab; grad receives
+ *                     this rank's PARTIAL gradient, which the caller sums over ranks. */
+srwcr_status srwcr_eval_begin(srwcr_ctx *ctx, const double *params);
+srwcr_status srwcr_stats_buffer(srwcr_ctx *ctx, double **dev_ptr, size_t *count);
+srwcr_status srwcr_eval_end(srwcr_ctx *ctx, double *value, double *grad);
+
+/* z-slab of rank `rank` out of `nranks` for a volume of nz slices: [*z0, *z1).
+ * Host-only (no GPU needed).  Slabs split the slices as evenly as possible. */
+srwcr_status srwcr_plan_slab(int64_t nz, int32_t nranks, int32_t rank, int64_t *z0, int64_t *z1);
+
+/* L-BFGS registration of C = D + w_p * C_p (Eq 1).  params_inout is a
+ * host fp64 array (layout above): the start point on entry, the result on return.
+ * cfg may be NULL for defaults (m = 5, max_iter 200, w_p = 0.1).  report may be NULL. */
+typedef struct {
+    int32_t struct_size;
+    int32_t m;                 /* number of corrections (paper: 5) */
+    int32_t max_iter;          /* paper: 200/200/120 per resolution level */
+    int32_t max_linesearch;    /* backtracking steps per iteration */
+    double w_p;                /* penalty weight (paper: 0.1 mono-modal, 30 multi-modal) */
+    double ftol, wolfe;        /* Armijo and curvature constants of the backtracking search */
+    int32_t stable_window;     /* stop when C changed < stable_tol over this many steps (paper: 20) */
+    double stable_tol;
+} srwcr_lbfgs_config;
+
+typedef struct {
+    int32_t struct_size;
+    int32_t iterations, evaluations, status; /* status: 0 converged/stable, 1 max_iter, 2 line search failed */
+    double initial_cost, final_cost, final_value;
+} srwcr_register_report;
+
+srwcr_status srwcr_default_lbfgs_config(srwcr_lbfgs_config *cfg);
+srwcr_status srwcr_register(srwcr_ctx *ctx, double *params_inout, const srwcr_lbfgs_config *cfg,
+                            srwcr_register_report *report);
+
+/* Debug / parity dumps (copied to host memory `out` of `bytes` bytes).
+ *   SRWCR_DUMP_FIXED, _MOVING   normalised volumes, fp32 [Nz][Ny][Nx]
+ *   SRWCR_DUMP_A0               fixed-image bin a0 = min(floor F, L-1) per voxel, int16
+ *   SRWCR_DUMP_CTRL_TAPS        per axis x,y,z: int32 tap base per voxel index (Nx+Ny+Nz values)
+ *   SRWCR_DUMP_SPAT_TAPS        same for the spatial-bin lattice
+ *   SRWCR_DUMP_N                static weighted counts N[r][a], fp64 [R][L+1]
+ *   SRWCR_DUMP_SQ               S[r][a], Q[r][a] of the last pass 1 (unshifted), fp64 [2][R][L+1]
+ *   SRWCR_DUMP_REGIONS          per region {p(r), sigma_r^2, mu_r, 1-CR_r, retained, Z}, fp64 [R][6]
+ *   SRWCR_DUMP_COEFS            alpha[R], beta[R], gamma[R][L+1] (fp32) of the last combine
+ *   SRWCR_DUMP_DDM              per-voxel dD/dm of the last pass 2 is not stored: ENOTSUP
+ * `bytes` must be at least the size given by srwcr_debug_size. */
+enum {
+    SRWCR_DUMP_FIXED = 1, SRWCR_DUMP_MOVING = 2, SRWCR_DUMP_A0 = 3, SRWCR_DUMP_CTRL_TAPS = 4,
+    SRWCR_DUMP_SPAT_TAPS = 5, SRWCR_DUMP_N = 6, SRWCR_DUMP_SQ = 7, SRWCR_DUMP_REGIONS = 8,
+    SRWCR_DUMP_COEFS = 9
+};
+srwcr_status srwcr_debug_size(const srwcr_ctx *ctx, int32_t what, size_t *bytes);
+srwcr_status srwcr_debug_dump(srwcr_ctx *ctx, int32_t what, void *out, size_t bytes);
+
+/* Kernel-launch counters and the last eval's per-pass device times (ms, CUDA events
+ * on the library stream; only filled when timing is enabled with srwcr_set_timing). */
+typedef struct {
+    int64_t launches_total;     /* kernels launched by this context since creation */
+    int32_t launches_per_eval;  /* kernels in one srwcr_eval (graph nodes that are kernels) */
+    float ms_pass1, ms_combine, ms_pass2, ms_total;
+} srwcr_stats;
+srwcr_status srwcr_set_timing(srwcr_ctx *ctx, int32_t enable);
+srwcr_status srwcr_get_stats(const srwcr_ctx *ctx, srwcr_stats *out);
+
+/* The CUDA stream all work of this context is issued on (a cudaStream_t). */
+srwcr_status srwcr_stream(const srwcr_ctx *ctx, void **stream);
+
+const char *srwcr_last_error(const srwcr_ctx *ctx);
+void srwcr_destroy(srwcr_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SRWCR_H */

@@ -1,0 +1,768 @@
+// srwcr.cu -- host runtime and C ABI of the SRWCR hot path (see include/srwcr.h).
+//
+// Owns device memory, the per-axis B-spline tables (built in fp64 on the host from
+// Eq 8 P:99 / Eq 17), the work-item list of the CTA decomposition, the static
+// fixed-image counts, the NCCL communicator of the z-slab decomposition, and the
+// launch sequence of one evaluation.  No compute of the method happens on the host
+// (apart from building the tables and summing the static total mass Z).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/srwcr.h"
+#include "srwcr_kernels.cuh"
+
+using namespace srwcr;
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+namespace {
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi &nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+            api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
+            api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
+            api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
+            api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+        }
+    }
+    return api;
+}
+}  // namespace
+
+struct srwcr_ctx {
+    std::string err;
+    bool poisoned = false;
+    srwcr_options opt{};
+    int dev = 0;
+    cudaStream_t stream = nullptr;
+    Geo g{};
+    int nranks = 1, rank = 0;
+    int64_t z0 = 0, z1 = 0;
+    double delta[3]{}, Delta[3]{};
+    int32_t kcells[3]{};
+    int64_t R = 0, nparams = 0, nint = 0;
+    // host tables (kept for dumps)
+    std::vector<int> h_cb[3], h_sb[3];
+    // device
+    float *F = nullptr, *M = nullptr, *phi = nullptr;
+    double *params64 = nullptr, *grad64 = nullptr;
+    const double *cur_params = nullptr;  // device fp64 params of the current evaluation
+    int *cb[3]{}, *sb[3]{};
+    float4 *cw[3]{}, *sw[3]{};
+    double4 *cw64[3]{};
+    Item *items = nullptr, *items_full = nullptr;  // this rank's slab / whole volume
+    int nitems = 0, nitems_full = 0;
+    double *SQ = nullptr, *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
+    double *S_out = nullptr, *Q_out = nullptr;
+    float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
+    double Z = 0;
+    float scaleA = 1, scaleB = 1;
+    size_t smem1 = 0, smem2 = 0;
+    int KB = 1, segsteps = 0;
+    ncclComm_t comm = nullptr;
+    bool external_exchange = false;
+    bool begun = false;
+    // stats
+    int64_t launches = 0;
+    int launches_per_eval = 0;
+    bool timing = false;
+    cudaEvent_t ev[4]{};
+    float ms[4]{};
+    double *pinned = nullptr;  // 2 doubles
+};
+
+static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
+    if (c) {
+        char buf[512];
+        va_list ap;
+        va_start(ap, fmt);
+        vsnprintf(buf, sizeof buf, fmt, ap);
+        va_end(ap);
+        c->err = buf;
+        if (s == SRWCR_ECUDA) c->poisoned = true;
+    }
+    return s;
+}
+
+#define CK(call)                                                                                        \
+    do {                                                                                                \
+        cudaError_t e_ = (call);                                                                        \
+        if (e_ != cudaSuccess) return fail(c, SRWCR_ECUDA, "%s failed: %s (%s:%d)", #call,              \
+                                           cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+    } while (0)
+#define CKL()                                                                                           \
+    do {                                                                                                \
+        c->launches++;                                                                                  \
+        cudaError_t e_ = cudaGetLastError();                                                            \
+        if (e_ != cudaSuccess) return fail(c, SRWCR_ECUDA, "kernel launch failed: %s (%s:%d)",          \
+                                           cudaGetErrorString(e_), __FILE__, __LINE__);                 \
+    } while (0)
+#define NCK(call)                                                                                       \
+    do {                                                                                                \
+        ncclResult_t r_ = (call);                                                                       \
+        if (r_ != ncclSuccess) return fail(c, SRWCR_ENCCL, "%s failed: %s", #call,                      \
+                                           nccl().GetErrorString(r_));                                  \
+    } while (0)
+
+// ------------------------------------------------------------------ host tables
+// Eq 8 pieces at t in [0,1), fp64
+static void beta4(double t, double w[4]) {
+    w[0] = (1.0 - t) * (1.0 - t) * (1.0 - t) / 6.0;
+    w[1] = (3.0 * t * t * t - 6.0 * t * t + 4.0) / 6.0;
+    w[2] = (-3.0 * t * t * t + 3.0 * t * t + 3.0 * t + 1.0) / 6.0;
+    w[3] = t * t * t / 6.0;
+}
+// voxel index i on a lattice of spacing sp: base floor(i/sp), weights beta(i/sp - base)  (Eq 17)
+static void build_axis(int64_t N, double sp, bool degenerate, std::vector<int> &base, std::vector<float4> &w,
+                       std::vector<double4> *w64 = nullptr) {
+    base.resize(N);
+    w.resize(N);
+    if (w64) w64->resize(N);
+    for (int64_t i = 0; i < N; ++i) {
+        double ww[4] = {1.0, 0.0, 0.0, 0.0};
+        base[i] = 0;
+        if (!degenerate) {
+            double s = (double)i / sp, fl = std::floor(s);
+            base[i] = (int)fl;
+            beta4(s - fl, ww);
+        }
+        w[i] = make_float4((float)ww[0], (float)ww[1], (float)ww[2], (float)ww[3]);
+        if (w64) (*w64)[i] = make_double4(ww[0], ww[1], ww[2], ww[3]);
+    }
+}
+
+// runs of constant spatial base within [lo, hi), chunked to <= maxlen
+static std::vector<std::pair<int, int>> runs(const std::vector<int> &sb, int lo, int hi, int maxlen) {
+    std::vector<std::pair<int, int>> out;
+    int s = lo;
+    while (s < hi) {
+        int e = s + 1;
+        while (e < hi && sb[e] == sb[s]) ++e;
+        int len = e - s, nch = (len + maxlen - 1) / maxlen;
+        for (int k = 0; k < nch; ++k) {
+            int a = s + (int)((long long)len * k / nch), b = s + (int)((long long)len * (k + 1) / nch);
+            if (b > a) out.push_back({a, b - a});
+        }
+        s = e;
+    }
+    return out;
+}
+
+extern "C" srwcr_status srwcr_plan_slab(int64_t nz, int32_t nranks, int32_t rank, int64_t *z0, int64_t *z1) {
+    if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z0 || !z1) return SRWCR_EINVAL;
+    *z0 = nz * rank / nranks;
+    *z1 = nz * (rank + 1) / nranks;
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_default_options(srwcr_options *o) {
+    if (!o) return SRWCR_EINVAL;
+    memset(o, 0, sizeof *o);
+    o->struct_size = (int32_t)sizeof *o;
+    o->nranks = 1;
+    o->eps_mass = 1e-12;
+    o->eps_sigma = 1e-6;
+    o->moment_shift = 1;
+    o->use_graph = 1;
+    return SRWCR_OK;
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+static PassArgs pass_args(srwcr_ctx *c) {
+    PassArgs a{};
+    a.g = c->g;
+    for (int i = 0; i < 3; ++i) {
+        a.t.cb[i] = c->cb[i]; a.t.cw[i] = c->cw[i]; a.t.cw64[i] = c->cw64[i]; a.t.sb[i] = c->sb[i]; a.t.sw[i] = c->sw[i];
+    }
+    a.p64 = c->cur_params;
+    a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.SQ = c->SQ;
+    a.scaleA = c->scaleA; a.scaleB = c->scaleB;
+    a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
+    a.invZ = (float)(1.0 / c->Z);
+    a.grad = c->grad64;
+    a.segsteps = c->segsteps;
+    return a;
+}
+
+template <int KB>
+static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
+    PassArgs a = pass_args(c);
+    const int n = full ? c->nitems_full : c->nitems;
+    a.items = full ? c->items_full : c->items;
+    if (n == 0) return SRWCR_OK;
+    if (stat) k_pass1<KB, true><<<n, NT, c->smem1, c->stream>>>(a);
+    else k_pass1<KB, false><<<n, NT, c->smem1, c->stream>>>(a);
+    CKL();
+    return SRWCR_OK;
+}
+// full = true: whole volume (create-time static passes, identical on every rank)
+static srwcr_status launch_pass1(srwcr_ctx *c, bool stat, bool full = false) {
+    switch (c->KB) {
+        case 1: return launch_pass1_t<1>(c, stat, full);
+        case 2: return launch_pass1_t<2>(c, stat, full);
+        case 3: return launch_pass1_t<3>(c, stat, full);
+        default: return launch_pass1_t<4>(c, stat, full);
+    }
+}
+template <int KB>
+static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
+    PassArgs a = pass_args(c);
+    a.grad = grad;
+    if (c->nitems == 0) return SRWCR_OK;
+    k_pass2<KB><<<c->nitems, NT, c->smem2, c->stream>>>(a);
+    CKL();
+    return SRWCR_OK;
+}
+static srwcr_status launch_pass2(srwcr_ctx *c, double *grad) {
+    switch (c->KB) {
+        case 1: return launch_pass2_t<1>(c, grad);
+        case 2: return launch_pass2_t<2>(c, grad);
+        case 3: return launch_pass2_t<3>(c, grad);
+        default: return launch_pass2_t<4>(c, grad);
+    }
+}
+template <int KB>
+static srwcr_status set_smem_t(srwcr_ctx *c) {
+    CK(cudaFuncSetAttribute(k_pass1<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass1<KB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass2<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+    return SRWCR_OK;
+}
+static srwcr_status set_smem(srwcr_ctx *c) {
+    switch (c->KB) {
+        case 1: return set_smem_t<1>(c);
+        case 2: return set_smem_t<2>(c);
+        case 3: return set_smem_t<3>(c);
+        default: return set_smem_t<4>(c);
+    }
+}
+
+static srwcr_status allreduce(srwcr_ctx *c, double *buf, size_t count) {
+    if (c->comm) NCK(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
+    return SRWCR_OK;
+}
+
+static srwcr_status run_combine(srwcr_ctx *c) {
+    CombineArgs ca{};
+    ca.SQ = c->SQ; ca.Nlo = c->Nlo; ca.Nup = c->Nup; ca.shiftc = c->shiftc;
+    ca.R = (int)c->R; ca.B = c->g.B; ca.Z = c->Z;
+    ca.eps_mass = c->opt.eps_mass; ca.eps_sigma = c->opt.eps_sigma;
+    ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out; ca.Q_out = c->Q_out;
+    ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
+    const int wpb = 8;
+    k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
+    CKL();
+    k_reduce_D<<<1, 1024, 0, c->stream>>>(c->dterm, c->reg, (int)c->R, c->Z, c->Dout);
+    CKL();
+    return SRWCR_OK;
+}
+
+#define TRY(x)                                \
+    do {                                      \
+        srwcr_status s_ = (x);                \
+        if (s_ != SRWCR_OK) return s_;        \
+    } while (0)
+
+static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *moving, const int64_t dims[3],
+                                const double sp[3], int32_t bins, const int32_t sbins[3], const double csp[3]) {
+    const srwcr_options &o = c->opt;
+    if (!fixed) return fail(c, SRWCR_EINVAL, "fixed is NULL");
+    if (!moving) return fail(c, SRWCR_EINVAL, "moving is NULL");
+    if (!dims || !sp || !sbins || !csp) return fail(c, SRWCR_EINVAL, "dims/spacing_mm/spatial_bins/control_spacing_mm is NULL");
+    if (dims[0] < 2 || dims[1] < 2 || dims[2] < 1) return fail(c, SRWCR_EINVAL, "dims: need Nx >= 2, Ny >= 2, Nz >= 1");
+    if (dims[0] > (1 << 20) || dims[1] > (1 << 20) || dims[2] > (1 << 20)) return fail(c, SRWCR_EINVAL, "dims too large");
+    if (bins < 2 || bins > 128) return fail(c, SRWCR_EINVAL, "intensity_bins must be in [2, 128], got %d", bins);
+    if (o.orientation != 0) return fail(c, SRWCR_ENOTSUP, "orientation 1 (moving as model image, Eq 20-21) is not supported");
+    if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(c, SRWCR_EINVAL, "rank/nranks out of range");
+    for (int i = 0; i < 3; ++i) {
+        if (!(sp[i] > 0)) return fail(c, SRWCR_EINVAL, "spacing_mm[%d] must be > 0", i);
+        if (!(csp[i] > 0)) return fail(c, SRWCR_EINVAL, "control_spacing_mm[%d] must be > 0", i);
+        if (sbins[i] < 0 || sbins[i] > dims[i]) return fail(c, SRWCR_EINVAL, "spatial_bins[%d] must be in [0, dims]", i);
+    }
+    const bool is2d = dims[2] == 1;
+    Geo &g = c->g;
+    g.nx = (int)dims[0]; g.ny = (int)dims[1]; g.nz = (int)dims[2];
+    g.nxy = (long long)g.nx * g.ny;
+    g.L = bins - 1; g.B = bins;
+    g.ndim = is2d ? 2 : 3;
+    int64_t G[3];
+    for (int i = 0; i < 3; ++i) {
+        c->delta[i] = csp[i] / sp[i];
+        G[i] = (is2d && i == 2) ? 1 : (int64_t)std::floor((double)(dims[i] - 1) / c->delta[i]) + 4;
+        c->kcells[i] = (is2d && i == 2) ? 0 : sbins[i];
+    }
+    for (int i = 0; i < 2 + !is2d; ++i)
+        if (c->delta[i] < 1.2) return fail(c, SRWCR_EINVAL, "control spacing along axis %d is %.3f voxels; >= 1.2 required", i, c->delta[i]);
+    g.Gx = (int)G[0]; g.Gy = (int)G[1]; g.GzExt = (int)G[2];
+    g.Gz = is2d ? 4 : (int)G[2];
+    g.Kx = c->kcells[0] > 0 ? c->kcells[0] + 3 : 4;
+    g.Ky = c->kcells[1] > 0 ? c->kcells[1] + 3 : 4;
+    g.Kz = c->kcells[2] > 0 ? c->kcells[2] + 3 : 4;
+    c->R = (int64_t)g.Kx * g.Ky * g.Kz;
+    c->nparams = (int64_t)g.ndim * G[0] * G[1] * G[2];
+    c->nint = 3LL * g.Gx * g.Gy * g.Gz;
+    c->KB = (g.B + 31) / 32;
+
+    c->dev = o.device;
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c->ev[i]));
+    CK(cudaMallocHost(&c->pinned, 4 * sizeof(double)));
+
+    // per-axis tables (fp64 on host -> device), control and spatial lattices
+    for (int ax = 0; ax < 3; ++ax) {
+        std::vector<float4> w;
+        std::vector<double4> w64;
+        build_axis(dims[ax], c->delta[ax], is2d && ax == 2, c->h_cb[ax], w, &w64);
+        CK(cudaMalloc(&c->cb[ax], sizeof(int) * dims[ax]));
+        CK(cudaMalloc(&c->cw[ax], sizeof(float4) * dims[ax]));
+        CK(cudaMalloc(&c->cw64[ax], sizeof(double4) * dims[ax]));
+        CK(cudaMemcpy(c->cw64[ax], w64.data(), sizeof(double4) * dims[ax], cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->cb[ax], c->h_cb[ax].data(), sizeof(int) * dims[ax], cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->cw[ax], w.data(), sizeof(float4) * dims[ax], cudaMemcpyHostToDevice));
+        const bool deg = c->kcells[ax] == 0;
+        c->Delta[ax] = deg ? 0.0 : (double)dims[ax] / (double)c->kcells[ax];
+        build_axis(dims[ax], c->Delta[ax], deg, c->h_sb[ax], w);
+        CK(cudaMalloc(&c->sb[ax], sizeof(int) * dims[ax]));
+        CK(cudaMalloc(&c->sw[ax], sizeof(float4) * dims[ax]));
+        CK(cudaMemcpy(c->sb[ax], c->h_sb[ax].data(), sizeof(int) * dims[ax], cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->sw[ax], w.data(), sizeof(float4) * dims[ax], cudaMemcpyHostToDevice));
+    }
+    // max lanes sharing a control x-base inside a 32-lane chunk -> segmented-reduction steps
+    {
+        int maxrun = 1, run = 1;
+        for (int i = 1; i < g.nx; ++i) {
+            run = (c->h_cb[0][i] == c->h_cb[0][i - 1]) ? run + 1 : 1;
+            maxrun = std::max(maxrun, run);
+        }
+        maxrun = std::min(maxrun, 32);
+        c->segsteps = 0;
+        while ((1 << c->segsteps) < maxrun) ++c->segsteps;
+    }
+
+    // volumes: upload (host or device source) and normalise
+    const long long nvox = (long long)g.nx * g.ny * g.nz;
+    CK(cudaMalloc(&c->F, sizeof(float) * nvox));
+    CK(cudaMalloc(&c->M, sizeof(float) * nvox));
+    float *raw = nullptr;
+    CK(cudaMalloc(&raw, sizeof(float) * nvox));
+    int *mm = nullptr;
+    CK(cudaMalloc(&mm, 2 * sizeof(int)));
+    for (int v = 0; v < 2; ++v) {
+        const float *src = v == 0 ? fixed : moving;
+        float *dst = v == 0 ? c->F : c->M;
+        CK(cudaMemcpy(raw, src, sizeof(float) * nvox, cudaMemcpyDefault));
+        int init[2] = {0x7f800000, (int)(0xff800000u ^ 0x7fffffffu)};
+        CK(cudaMemcpy(mm, init, sizeof init, cudaMemcpyHostToDevice));
+        k_minmax<<<296, 256>>>(raw, nvox, reinterpret_cast<float *>(mm));
+        CKL();
+        int key[2];
+        CK(cudaMemcpy(key, mm, sizeof key, cudaMemcpyDeviceToHost));
+        float lohi[2];
+        for (int k = 0; k < 2; ++k) {
+            int bits = key[k] >= 0 ? key[k] : key[k] ^ 0x7fffffff;
+            memcpy(&lohi[k], &bits, 4);
+        }
+        if (!std::isfinite(lohi[0]) || !std::isfinite(lohi[1]))
+            return fail(c, SRWCR_EINVAL, "%s contains non-finite values", v == 0 ? "fixed" : "moving");
+        if (o.inputs_normalized) {
+            if (lohi[0] < 0.f || lohi[1] > (float)g.L)
+                return fail(c, SRWCR_EINVAL, "%s not in [0, L=%d] although inputs_normalized = 1", v == 0 ? "fixed" : "moving", g.L);
+            CK(cudaMemcpy(dst, raw, sizeof(float) * nvox, cudaMemcpyDeviceToDevice));
+        } else {
+            const double lo = lohi[0], hi = lohi[1];
+            const bool constant = !(hi > lo);
+            const double scale = constant ? 0.0 : (double)g.L / (hi - lo);
+            k_normalize<<<1184, 256>>>(raw, dst, nvox, lo, scale, (float)g.L, constant ? 1 : 0);
+            CKL();
+        }
+    }
+    CK(cudaDeviceSynchronize());
+    cudaFree(raw);
+    cudaFree(mm);
+
+    // z-slab of this rank and the work items (each inside one spatial cell)
+    c->nranks = o.nranks;
+    c->rank = o.rank;
+    srwcr_plan_slab(g.nz, c->nranks, c->rank, &c->z0, &c->z1);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+    int ymax = 64, zmax = 64;
+    std::vector<Item> items, items_full;
+    size_t npmax = 0;
+    auto build_items = [&](int zlo, int zhi, std::vector<Item> &out) {
+        auto xr = runs(c->h_sb[0], 0, g.nx, 32);
+        auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
+        auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
+        for (auto &zz : zr)
+            for (auto &yy : yr)
+                for (auto &xx : xr) {
+                    Item it{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second};
+                    out.push_back(it);
+                    size_t nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
+                    size_t nyn = c->h_cb[1][it.y0 + it.ylen - 1] + 4 - c->h_cb[1][it.y0];
+                    size_t nzn = c->h_cb[2][it.z0 + it.zlen - 1] + 4 - c->h_cb[2][it.z0];
+                    npmax = std::max(npmax, nzn * 3 * nyn * nxn);
+                }
+    };
+    for (;;) {
+        items.clear();
+        npmax = 0;
+        build_items((int)c->z0, (int)c->z1, items);
+        const bool small = (long long)items.size() < 6LL * nsm;
+        const bool big_np = npmax > 12288;
+        if ((small || big_np) && (ymax > 16 || zmax > 4)) {
+            if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
+            else if (ymax > 16) ymax /= 2;
+            else zmax /= 2;
+            continue;
+        }
+        break;
+    }
+    build_items(0, g.nz, items_full);
+    if (npmax > 16384) return fail(c, SRWCR_EINVAL, "control lattice too fine for the node window (%zu)", npmax);
+    c->nitems = (int)items.size();
+    c->nitems_full = (int)items_full.size();
+    if (c->nitems) {
+        CK(cudaMalloc(&c->items, sizeof(Item) * items.size()));
+        CK(cudaMemcpy(c->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+    }
+    CK(cudaMalloc(&c->items_full, sizeof(Item) * items_full.size()));
+    CK(cudaMemcpy(c->items_full, items_full.data(), sizeof(Item) * items_full.size(), cudaMemcpyHostToDevice));
+
+    // buffers
+    const long long RB = c->R * g.B;
+    CK(cudaMalloc(&c->phi, sizeof(float) * c->nint));
+    CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
+    CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
+    CK(cudaMalloc(&c->SQ, sizeof(double) * RB * 4));
+    CK(cudaMalloc(&c->Nlo, sizeof(double) * RB));
+    CK(cudaMalloc(&c->Nup, sizeof(double) * RB));
+    CK(cudaMalloc(&c->S_out, sizeof(double) * RB));
+    CK(cudaMalloc(&c->Q_out, sizeof(double) * RB));
+    CK(cudaMalloc(&c->dterm, sizeof(double) * c->R));
+    CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
+    CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
+    CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
+    CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
+    CK(cudaMalloc(&c->beta, sizeof(float) * c->R));
+    CK(cudaMalloc(&c->gamma, sizeof(float) * RB));
+    CK(cudaMemset(c->phi, 0, sizeof(float) * c->nint));
+    CK(cudaMemset(c->params64, 0, sizeof(double) * c->nparams));
+    c->cur_params = c->params64;
+
+    // fixed-point scales of the pass-1 line tables: |value * scale| < 2^22 (magic-number
+    // conversion), and a line sums at most 32 voxels (no int32 overflow)
+    const double Ld = g.L;
+    c->scaleA = (float)std::ldexp(1.0, (int)std::floor(std::log2(4194303.0 / (Ld + 1.0))));
+    c->scaleB = (float)std::ldexp(1.0, (int)std::floor(std::log2(4194303.0 / ((Ld + 1.0) * (Ld + 1.0)))));
+
+    c->smem1 = sizeof(int) * NW * g.B * LT_STRIDE + sizeof(unsigned) * NW * 4 + sizeof(int) * NW * 2 + sizeof(float4) * NW + sizeof(float) * g.B;
+    c->smem2 = sizeof(float) * (64 * g.B + 16 * g.B) + sizeof(float4) * NW * g.B + sizeof(float) * (64 + 64 + 32 + NW * 96) +
+               sizeof(float) * npmax;
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+    if ((int)c->smem1 > maxsm || (int)c->smem2 > maxsm)
+        return fail(c, SRWCR_EINVAL, "shared memory need %zu/%zu B exceeds %d B", c->smem1, c->smem2, maxsm);
+    TRY(set_smem(c));
+
+    // NCCL communicator for the z-slab decomposition
+    if (c->nranks > 1) {
+        if (o.nccl_id) {
+            if (!nccl().ok) return fail(c, SRWCR_ENCCL, "libnccl.so.2 could not be loaded");
+            ncclUniqueId id;
+            memcpy(&id, o.nccl_id, sizeof id);
+            NCK(nccl().CommInitRank(&c->comm, c->nranks, id, c->rank));
+        } else {
+            c->external_exchange = true;
+        }
+    }
+
+    // static weighted counts N[r][a] (lower / upper Parzen half) over the whole volume
+    // (every rank holds the full F, so no create-time collective is needed)
+    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * RB * 4, c->stream));
+    TRY(launch_pass1(c, true, true));
+    k_split_counts<<<512, 256, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, RB);
+    CKL();
+    {
+        std::vector<double> nl(RB), nu(RB);
+        CK(cudaMemcpyAsync(nl.data(), c->Nlo, sizeof(double) * RB, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(nu.data(), c->Nup, sizeof(double) * RB, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        double Z = 0;
+        for (long long i = 0; i < RB; ++i) Z += nl[i] + nu[i];
+        c->Z = Z;
+    }
+    // per-bin moment shift: bin index, then (option) conditional means at Phi = 0
+    {
+        std::vector<float> sh(g.B);
+        for (int b = 0; b < g.B; ++b) sh[b] = (float)b;
+        CK(cudaMemcpy(c->shiftc, sh.data(), sizeof(float) * g.B, cudaMemcpyHostToDevice));
+        if (o.moment_shift) {
+            CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * RB * 4, c->stream));
+            TRY(launch_pass1(c, false, true));
+            float *tmp = nullptr;
+            CK(cudaMalloc(&tmp, sizeof(float) * g.B));
+            k_shift_update<<<(g.B + 127) / 128, 128, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, c->shiftc, tmp, (int)c->R, g.B);
+            CKL();
+            CK(cudaMemcpyAsync(c->shiftc, tmp, sizeof(float) * g.B, cudaMemcpyDeviceToDevice, c->stream));
+            CK(cudaStreamSynchronize(c->stream));
+            cudaFree(tmp);
+        }
+    }
+    c->launches_per_eval = 5;  // params->f32, pass 1, combine, reduce_D, pass 2
+    CK(cudaStreamSynchronize(c->stream));
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_create(srwcr_ctx **out, const float *fixed, const float *moving, const int64_t dims[3],
+                                     const double spacing_mm[3], int32_t intensity_bins, const int32_t spatial_bins[3],
+                                     const double control_spacing_mm[3], const srwcr_options *opt) {
+    if (!out) return SRWCR_EINVAL;
+    *out = nullptr;
+    srwcr_ctx *c = new (std::nothrow) srwcr_ctx();
+    if (!c) return SRWCR_ENOMEM;
+    if (opt) {
+        if (opt->struct_size != (int32_t)sizeof(srwcr_options)) {
+            *out = c;
+            return fail(c, SRWCR_EINVAL, "opt->struct_size mismatch (use srwcr_default_options)");
+        }
+        c->opt = *opt;
+    } else {
+        srwcr_default_options(&c->opt);
+    }
+    srwcr_status s = create_impl(c, fixed, moving, dims, spacing_mm, intensity_bins, spatial_bins, control_spacing_mm);
+    *out = c;  // returned even on failure so srwcr_last_error can be read; caller destroys
+    return s;
+}
+
+extern "C" srwcr_status srwcr_num_params(const srwcr_ctx *c, int64_t *n, int64_t grid_dims[3]) {
+    if (!c) return SRWCR_EINVAL;
+    if (n) *n = c->nparams;
+    if (grid_dims) { grid_dims[0] = c->g.Gx; grid_dims[1] = c->g.Gy; grid_dims[2] = c->g.GzExt; }
+    return SRWCR_OK;
+}
+
+static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
+    if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned by an earlier CUDA error");
+    if (!params) return fail(c, SRWCR_EINVAL, "params is NULL");
+    CK(cudaSetDevice(c->dev));
+    const double *pd = params;
+    if (!is_device_ptr(params)) {
+        CK(cudaMemcpyAsync(c->params64, params, sizeof(double) * c->nparams, cudaMemcpyHostToDevice, c->stream));
+        pd = c->params64;
+    }
+    c->cur_params = pd;
+    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
+    CKL();
+    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * c->R * c->g.B * 4, c->stream));
+    TRY(launch_pass1(c, false));
+    if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
+    return SRWCR_OK;
+}
+
+static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, bool reduce_grad) {
+    TRY(run_combine(c));
+    if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    double *gd = nullptr;
+    bool grad_dev = grad && is_device_ptr(grad);
+    if (grad) {
+        gd = grad_dev ? grad : c->grad64;
+        CK(cudaMemsetAsync(gd, 0, sizeof(double) * c->nparams, c->stream));
+        TRY(launch_pass2(c, gd));
+        if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
+    }
+    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
+    CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (grad && !grad_dev) CK(cudaMemcpyAsync(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->timing) {
+        cudaEventElapsedTime(&c->ms[0], c->ev[0], c->ev[1]);
+        cudaEventElapsedTime(&c->ms[1], c->ev[1], c->ev[2]);
+        cudaEventElapsedTime(&c->ms[2], c->ev[2], c->ev[3]);
+        c->ms[3] = c->ms[0] + c->ms[1] + c->ms[2];
+    }
+    if (value) *value = c->pinned[0];
+    if (c->pinned[1] < 0.5) {
+        if (value) *value = 0.0;
+        return fail(c, SRWCR_EDEGENERATE, "no spatial bin passed the retention test (reading c12)");
+    }
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
+    if (!c) return SRWCR_EINVAL;
+    if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
+    TRY(eval_begin_impl(c, params));
+    TRY(allreduce(c, c->SQ, (size_t)c->R * c->g.B * 4));
+    return eval_end_impl(c, value, grad, true);
+}
+
+extern "C" srwcr_status srwcr_eval_begin(srwcr_ctx *c, const double *params) {
+    if (!c) return SRWCR_EINVAL;
+    TRY(eval_begin_impl(c, params));
+    CK(cudaStreamSynchronize(c->stream));
+    c->begun = true;
+    return SRWCR_OK;
+}
+extern "C" srwcr_status srwcr_stats_buffer(srwcr_ctx *c, double **dev_ptr, size_t *count) {
+    if (!c || !dev_ptr || !count) return SRWCR_EINVAL;
+    *dev_ptr = c->SQ;
+    *count = (size_t)c->R * c->g.B * 4;
+    return SRWCR_OK;
+}
+extern "C" srwcr_status srwcr_eval_end(srwcr_ctx *c, double *value, double *grad) {
+    if (!c) return SRWCR_EINVAL;
+    if (!c->begun) return fail(c, SRWCR_ESTATE, "srwcr_eval_end without srwcr_eval_begin");
+    c->begun = false;
+    return eval_end_impl(c, value, grad, false);
+}
+
+// ------------------------------------------------------------------ debug dumps
+extern "C" srwcr_status srwcr_debug_size(const srwcr_ctx *c, int32_t what, size_t *bytes) {
+    if (!c || !bytes) return SRWCR_EINVAL;
+    const long long nvox = (long long)c->g.nx * c->g.ny * c->g.nz, RB = c->R * c->g.B;
+    switch (what) {
+        case SRWCR_DUMP_FIXED: case SRWCR_DUMP_MOVING: *bytes = sizeof(float) * nvox; break;
+        case SRWCR_DUMP_A0: *bytes = sizeof(short) * nvox; break;
+        case SRWCR_DUMP_CTRL_TAPS: case SRWCR_DUMP_SPAT_TAPS: *bytes = sizeof(int) * (c->g.nx + c->g.ny + c->g.nz); break;
+        case SRWCR_DUMP_N: *bytes = sizeof(double) * RB; break;
+        case SRWCR_DUMP_SQ: *bytes = sizeof(double) * RB * 2; break;
+        case SRWCR_DUMP_REGIONS: *bytes = sizeof(double) * c->R * 6; break;
+        case SRWCR_DUMP_COEFS: *bytes = sizeof(float) * (2 * c->R + RB); break;
+        default: return SRWCR_EINVAL;
+    }
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_debug_dump(srwcr_ctx *c, int32_t what, void *out, size_t bytes) {
+    if (!c || !out) return SRWCR_EINVAL;
+    if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned");
+    size_t need = 0;
+    if (srwcr_debug_size(c, what, &need) != SRWCR_OK) return fail(c, SRWCR_EINVAL, "unknown dump %d", what);
+    if (bytes < need) return fail(c, SRWCR_EINVAL, "bytes %zu < %zu", bytes, need);
+    CK(cudaSetDevice(c->dev));
+    CK(cudaStreamSynchronize(c->stream));
+    const long long nvox = (long long)c->g.nx * c->g.ny * c->g.nz, RB = c->R * c->g.B;
+    switch (what) {
+        case SRWCR_DUMP_FIXED: CK(cudaMemcpy(out, c->F, need, cudaMemcpyDeviceToHost)); break;
+        case SRWCR_DUMP_MOVING: CK(cudaMemcpy(out, c->M, need, cudaMemcpyDeviceToHost)); break;
+        case SRWCR_DUMP_A0: {
+            short *d = nullptr;
+            CK(cudaMalloc(&d, need));
+            k_a0_map<<<1184, 256>>>(c->F, d, nvox, c->g.L);
+            CKL();
+            CK(cudaMemcpy(out, d, need, cudaMemcpyDeviceToHost));
+            cudaFree(d);
+            break;
+        }
+        case SRWCR_DUMP_CTRL_TAPS: case SRWCR_DUMP_SPAT_TAPS: {
+            int *o = (int *)out;
+            for (int ax = 0; ax < 3; ++ax) {
+                const std::vector<int> &v = what == SRWCR_DUMP_CTRL_TAPS ? c->h_cb[ax] : c->h_sb[ax];
+                memcpy(o, v.data(), sizeof(int) * v.size());
+                o += v.size();
+            }
+            break;
+        }
+        case SRWCR_DUMP_N: {
+            std::vector<double> lo(RB), up(RB);
+            CK(cudaMemcpy(lo.data(), c->Nlo, sizeof(double) * RB, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy(up.data(), c->Nup, sizeof(double) * RB, cudaMemcpyDeviceToHost));
+            double *o = (double *)out;
+            const int B = c->g.B;
+            for (long long r = 0; r < c->R; ++r)
+                for (int b = 0; b < B; ++b) o[r * B + b] = lo[r * B + b] + (b > 0 ? up[r * B + b - 1] : 0.0);
+            break;
+        }
+        case SRWCR_DUMP_SQ:
+            CK(cudaMemcpy(out, c->S_out, sizeof(double) * RB, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy((double *)out + RB, c->Q_out, sizeof(double) * RB, cudaMemcpyDeviceToHost));
+            break;
+        case SRWCR_DUMP_REGIONS: CK(cudaMemcpy(out, c->reg, need, cudaMemcpyDeviceToHost)); break;
+        case SRWCR_DUMP_COEFS:
+            CK(cudaMemcpy(out, c->alpha, sizeof(float) * c->R, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy((float *)out + c->R, c->beta, sizeof(float) * c->R, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy((float *)out + 2 * c->R, c->gamma, sizeof(float) * RB, cudaMemcpyDeviceToHost));
+            break;
+    }
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_set_timing(srwcr_ctx *c, int32_t enable) {
+    if (!c) return SRWCR_EINVAL;
+    c->timing = enable != 0;
+    return SRWCR_OK;
+}
+extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
+    if (!c || !out) return SRWCR_EINVAL;
+    out->launches_total = c->launches;
+    out->launches_per_eval = c->launches_per_eval;
+    out->ms_pass1 = c->ms[0];
+    out->ms_combine = c->ms[1];
+    out->ms_pass2 = c->ms[2];
+    out->ms_total = c->ms[3];
+    return SRWCR_OK;
+}
+extern "C" srwcr_status srwcr_stream(const srwcr_ctx *c, void **stream) {
+    if (!c || !stream) return SRWCR_EINVAL;
+    *stream = (void *)c->stream;
+    return SRWCR_OK;
+}
+extern "C" const char *srwcr_last_error(const srwcr_ctx *c) { return c ? c->err.c_str() : "null context"; }
+
+extern "C" void srwcr_destroy(srwcr_ctx *c) {
+    if (!c) return;
+    cudaSetDevice(c->dev);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg,
+                    c->Dout, c->S_out, c->Q_out, c->shiftc, c->alpha, c->beta, c->gamma};
+    for (void *p : bufs)
+        if (p) cudaFree(p);
+    for (int i = 0; i < 3; ++i) {
+        if (c->cb[i]) cudaFree(c->cb[i]);
+        if (c->cw[i]) cudaFree(c->cw[i]);
+        if (c->cw64[i]) cudaFree(c->cw64[i]);
+        if (c->sb[i]) cudaFree(c->sb[i]);
+        if (c->sw[i]) cudaFree(c->sw[i]);
+    }
+    for (int i = 0; i < 4; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+// ------------------------------------------------------------------ L-BFGS
+#include "srwcr_register.inc"

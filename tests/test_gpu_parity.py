@@ -1,0 +1,160 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the fp64 oracle.
+
+Gates (BASELINE.json north_star): D relative error <= 1e-5, gradient relative L2 error
+<= 1e-4, static assignments bit-exact (normalised volumes, fixed-bin map a0, per-axis
+tap bases of both lattices, nonzero pattern of N).
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from gpu_common import REDUCED, problem, rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+D_TOL = 1e-5
+G_TOL = 1e-4
+
+
+def _oracle_eval(pb, Fn, Mn, params, literal=False):
+    if literal:
+        return O.eval_literal(pb, Fn, Mn, params)
+    return O.eval_moments(pb, Fn, Mn, params)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+@pytest.mark.parametrize("kind", ["zero", "small", "large"])
+def test_value_and_gradient(name, kind):
+    g, pb, Fn, Mn, params = problem(name, 1, params_kind=kind)
+    D, grad = g.eval(params)
+    Do, go = _oracle_eval(pb, Fn, Mn, params, literal=name in ("C1",))
+    assert rel(D, Do) <= D_TOL, (D, Do)
+    if np.linalg.norm(go) > 0:
+        assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+@pytest.mark.parametrize("seed", [2, 3])
+def test_more_seeds(name, seed):
+    g, pb, Fn, Mn, params = problem(name, seed, params_kind="small")
+    D, grad = g.eval(params)
+    Do, go = O.eval_moments(pb, Fn, Mn, params)
+    assert rel(D, Do) <= D_TOL
+    assert rel_l2(grad, go) <= G_TOL
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C5"])
+def test_static_assignments_bit_exact(name):
+    g, pb, Fn, Mn, params = problem(name, 1)
+    assert np.array_equal(g.debug_dump("fixed"), Fn.ravel())
+    assert np.array_equal(g.debug_dump("moving"), Mn.ravel())
+    a0 = np.minimum(np.floor(Fn.astype(np.float64)), pb.L - 1).astype(np.int16).ravel()
+    assert np.array_equal(g.debug_dump("a0"), a0)
+    # per-axis tap bases of the control and spatial lattices (Eq 17 / Eq 7)
+    G, K = pb.derived()
+    ct, st = g.debug_dump("ctrl_taps"), g.debug_dump("spat_taps")
+    off = 0
+    for ax, n in enumerate(pb.dims):
+        for i in range(n):
+            deg_c = ax == 2 and pb.dims[2] == 1
+            deg_s = pb.kcells[ax] == 0 or deg_c
+            bc, _ = O.taps(i, pb.delta[ax], deg_c)
+            bs, _ = O.taps(i, 1.0 if deg_s else pb.dims[ax] / pb.kcells[ax], deg_s)
+            assert ct[off + i] == bc and st[off + i] == bs
+        off += n
+    # static counts N: nonzero pattern exact, values to fp32-accumulation accuracy
+    N, _, _ = O.moments(pb, Fn, Mn, params)
+    Ng = g.debug_dump("N").reshape(N.shape)
+    assert np.array_equal(Ng != 0, N != 0)
+    assert np.abs(Ng - N).max() <= 1e-5 * N.max()
+    g.close()
+
+
+def test_identical_integer_images_optimum():
+    rng = np.random.default_rng(5)
+    I = rng.integers(0, 32, size=(24, 28, 30)).astype(np.float32)
+    I[0, 0, 0], I[0, 0, 1] = 0, 31
+    import paper_1804_05061_b200 as S
+    g = S.Srwcr(I, I, (1, 1, 1), 32, (2, 2, 2), (5, 5, 5))
+    D, grad = g.eval(np.zeros(g.params_shape))
+    assert abs(D) < 1e-6
+    assert np.abs(grad).max() < 1e-6
+    g.close()
+
+
+def test_single_global_bin_is_textbook_cr():
+    rng = np.random.default_rng(6)
+    A = rng.integers(0, 16, size=(20, 24, 26)).astype(np.float32)
+    B = np.clip(np.round(0.6 * A + rng.integers(-3, 4, size=A.shape)), 0, 15).astype(np.float32)
+    A[0, 0, :2] = (0, 15)
+    B[0, 0, :2] = (0, 15)
+    import paper_1804_05061_b200 as S
+    g = S.Srwcr(A, B, (1, 1, 1), 16, (0, 0, 0), (5, 5, 5), inputs_normalized=True)
+    D, _ = g.eval(np.zeros(g.params_shape))
+    a, b = A.ravel().astype(np.float64), B.ravel().astype(np.float64)
+    within = sum((a == k).mean() * b[a == k].var() for k in np.unique(a))
+    assert rel(D, within / b.var()) <= 1e-6
+    g.close()
+
+
+def test_host_and_device_pointers_agree():
+    torch = pytest.importorskip("torch")
+    g, pb, Fn, Mn, params = problem("C1", 1)
+    D1, g1 = g.eval(params)
+    pt = torch.from_numpy(params).cuda()
+    gt = torch.empty_like(pt)
+    D2, _ = g.eval(pt, grad=gt)
+    # atomics make the summation order (not the arithmetic) differ between evaluations
+    assert rel(D2, D1) <= 1e-12
+    assert rel_l2(gt.cpu().numpy(), g1) <= 1e-6
+    g.close()
+
+
+def _cudart():
+    import ctypes
+    import glob
+    for cand in ["libcudart.so", *glob.glob("/usr/local/cuda/lib64/libcudart.so*")]:
+        try:
+            return ctypes.CDLL(cand)
+        except OSError:
+            continue
+    raise RuntimeError("libcudart not found")
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_slab_decomposition_on_one_gpu(P):
+    """The z-slab path of nranks = P with the exchange done by the caller (sum of rank
+    partials) equals the single-GPU result: same kernels, different summation order."""
+    import ctypes
+    import synth
+    import paper_1804_05061_b200 as S
+    name = "C3"
+    cfg = synth.config(name, REDUCED[name])
+    F, M = synth.make_pair(name, 1, cfg["dims"])
+    g1 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    params = synth.make_params(g1.params_shape, "small", 1)
+    D1, grad1 = g1.eval(params)
+    ranks = [S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], nranks=P, rank=k)
+             for k in range(P)]
+    for r in ranks:
+        r.eval_begin(params)
+    rt = _cudart()
+    bufs = []
+    for r in ranks:
+        p, n = r.stats_buffer()
+        h = np.empty(n, np.float64)
+        assert rt.cudaMemcpy(h.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(p), ctypes.c_size_t(8 * n), 4) == 0
+        bufs.append(h)
+    tot = np.sum(bufs, axis=0)
+    for r in ranks:
+        p, n = r.stats_buffer()
+        assert rt.cudaMemcpy(ctypes.c_void_p(p), tot.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(8 * n), 4) == 0
+    outs = [r.eval_end() for r in ranks]
+    for D, _ in outs:
+        assert rel(D, D1) <= 1e-9
+    gsum = np.sum([gk for _, gk in outs], axis=0)
+    assert rel_l2(gsum, grad1) <= 1e-6
+    for r in ranks + [g1]:
+        r.close()
