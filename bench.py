@@ -307,6 +307,7 @@ def main():
             "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": int(params_np.nbytes),
                     "d2h_bytes_per_step": int(params_np.nbytes) + 8},
             "gpu_launches": int(launches),
+            "decomposition": {k: g.stats()[k] for k in ("warps_per_cta", "slot_capacity", "voxels_per_lane", "items")},
             "clocks": clk.summary(),
             "D": D,
         }

@@ -64,6 +64,7 @@ struct srwcr_ctx {
     int64_t R = 0, nparams = 0, nint = 0;
     // host tables (kept for dumps)
     std::vector<int> h_cb[3], h_sb[3];
+    std::vector<float4> h_sw[3];
     // device
     float *F = nullptr, *M = nullptr, *phi = nullptr;
     double *params64 = nullptr, *grad64 = nullptr;
@@ -72,14 +73,17 @@ struct srwcr_ctx {
     float4 *cw[3]{}, *sw[3]{};
     double4 *cw64[3]{};
     Item *items = nullptr, *items_full = nullptr;  // this rank's slab / whole volume
+    ItemW *itemw = nullptr, *itemw_full = nullptr;
+    int *slotbins = nullptr;                         // slot lists of both item lists
     int nitems = 0, nitems_full = 0;
-    double *SQ = nullptr, *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
-    double *S_out = nullptr, *Q_out = nullptr;
+    int W = 16, W2 = 16, XV = 1, S = 1;               // warps per CTA (pass 1, pass 2), voxels per lane, slots
+    double *SQ = nullptr, *Qt = nullptr;             // stats: [R][B][2] binned, then [R] binless
+    double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
+    double *S_out = nullptr;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
     double Z = 0;
-    float scaleA = 1, scaleB = 1;
     size_t smem1 = 0, smem2 = 0;
-    int KB = 1, segsteps = 0;
+    int segsteps = 0;
     ncclComm_t comm = nullptr;
     bool external_exchange = false;
     bool begun = false;
@@ -204,8 +208,8 @@ static PassArgs pass_args(srwcr_ctx *c) {
         a.t.cb[i] = c->cb[i]; a.t.cw[i] = c->cw[i]; a.t.cw64[i] = c->cw64[i]; a.t.sb[i] = c->sb[i]; a.t.sw[i] = c->sw[i];
     }
     a.p64 = c->cur_params;
-    a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.SQ = c->SQ;
-    a.scaleA = c->scaleA; a.scaleB = c->scaleB;
+    a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
+    a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
     a.grad = c->grad64;
@@ -213,58 +217,45 @@ static PassArgs pass_args(srwcr_ctx *c) {
     return a;
 }
 
-template <int KB>
+template <int XV>
 static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     PassArgs a = pass_args(c);
     const int n = full ? c->nitems_full : c->nitems;
     a.items = full ? c->items_full : c->items;
+    a.itemw = full ? c->itemw_full : c->itemw;
     if (n == 0) return SRWCR_OK;
-    if (stat) k_pass1<KB, true><<<n, NT, c->smem1, c->stream>>>(a);
-    else k_pass1<KB, false><<<n, NT, c->smem1, c->stream>>>(a);
+    if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
 // full = true: whole volume (create-time static passes, identical on every rank)
 static srwcr_status launch_pass1(srwcr_ctx *c, bool stat, bool full = false) {
-    switch (c->KB) {
-        case 1: return launch_pass1_t<1>(c, stat, full);
-        case 2: return launch_pass1_t<2>(c, stat, full);
-        case 3: return launch_pass1_t<3>(c, stat, full);
-        default: return launch_pass1_t<4>(c, stat, full);
-    }
+    return c->XV == 2 ? launch_pass1_t<2>(c, stat, full) : launch_pass1_t<1>(c, stat, full);
 }
-template <int KB>
+template <int XV>
 static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     PassArgs a = pass_args(c);
     a.grad = grad;
     if (c->nitems == 0) return SRWCR_OK;
-    k_pass2<KB><<<c->nitems, NT, c->smem2, c->stream>>>(a);
+    a.W = c->W2;
+    k_pass2<XV><<<c->nitems, 32 * c->W2, c->smem2, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
 static srwcr_status launch_pass2(srwcr_ctx *c, double *grad) {
-    switch (c->KB) {
-        case 1: return launch_pass2_t<1>(c, grad);
-        case 2: return launch_pass2_t<2>(c, grad);
-        case 3: return launch_pass2_t<3>(c, grad);
-        default: return launch_pass2_t<4>(c, grad);
-    }
+    return c->XV == 2 ? launch_pass2_t<2>(c, grad) : launch_pass2_t<1>(c, grad);
 }
-template <int KB>
+template <int XV>
 static srwcr_status set_smem_t(srwcr_ctx *c) {
-    CK(cudaFuncSetAttribute(k_pass1<KB, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass1<KB, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass2<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+    CK(cudaFuncSetAttribute(k_pass1<XV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass1<XV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
     return SRWCR_OK;
 }
-static srwcr_status set_smem(srwcr_ctx *c) {
-    switch (c->KB) {
-        case 1: return set_smem_t<1>(c);
-        case 2: return set_smem_t<2>(c);
-        case 3: return set_smem_t<3>(c);
-        default: return set_smem_t<4>(c);
-    }
-}
+static srwcr_status set_smem(srwcr_ctx *c) { return c->XV == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c); }
+
+static size_t stats_count(const srwcr_ctx *c) { return (size_t)c->R * c->g.B * 2 + (size_t)c->R; }
 
 static srwcr_status allreduce(srwcr_ctx *c, double *buf, size_t count) {
     if (c->comm) NCK(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
@@ -273,10 +264,10 @@ static srwcr_status allreduce(srwcr_ctx *c, double *buf, size_t count) {
 
 static srwcr_status run_combine(srwcr_ctx *c) {
     CombineArgs ca{};
-    ca.SQ = c->SQ; ca.Nlo = c->Nlo; ca.Nup = c->Nup; ca.shiftc = c->shiftc;
+    ca.SQ = c->SQ; ca.Qt = c->Qt; ca.Nlo = c->Nlo; ca.Nup = c->Nup; ca.shiftc = c->shiftc;
     ca.R = (int)c->R; ca.B = c->g.B; ca.Z = c->Z;
     ca.eps_mass = c->opt.eps_mass; ca.eps_sigma = c->opt.eps_sigma;
-    ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out; ca.Q_out = c->Q_out;
+    ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out;
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
     const int wpb = 8;
     k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
@@ -330,7 +321,6 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->R = (int64_t)g.Kx * g.Ky * g.Kz;
     c->nparams = (int64_t)g.ndim * G[0] * G[1] * G[2];
     c->nint = 3LL * g.Gx * g.Gy * g.Gz;
-    c->KB = (g.B + 31) / 32;
 
     c->dev = o.device;
     CK(cudaSetDevice(c->dev));
@@ -352,6 +342,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         const bool deg = c->kcells[ax] == 0;
         c->Delta[ax] = deg ? 0.0 : (double)dims[ax] / (double)c->kcells[ax];
         build_axis(dims[ax], c->Delta[ax], deg, c->h_sb[ax], w);
+        c->h_sw[ax] = w;
         CK(cudaMalloc(&c->sb[ax], sizeof(int) * dims[ax]));
         CK(cudaMalloc(&c->sw[ax], sizeof(float4) * dims[ax]));
         CK(cudaMemcpy(c->sb[ax], c->h_sb[ax].data(), sizeof(int) * dims[ax], cudaMemcpyHostToDevice));
@@ -416,22 +407,31 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     srwcr_plan_slab(g.nz, c->nranks, c->rank, &c->z0, &c->z1);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
+    // voxels per lane: 2 when every spatial x-cell is at least 48 voxels wide
+    {
+        int minw = g.nx;
+        auto xr = runs(c->h_sb[0], 0, g.nx, 1 << 30);
+        for (auto &r : xr) minw = std::min(minw, r.second);
+        c->XV = minw >= 48 ? 2 : 1;
+    }
+    const int xmax = 32 * c->XV;
     int ymax = 64, zmax = 64;
     std::vector<Item> items, items_full;
     size_t npmax = 0;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out) {
-        auto xr = runs(c->h_sb[0], 0, g.nx, 32);
+        auto xr = runs(c->h_sb[0], 0, g.nx, xmax);
         auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
         auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
         for (auto &zz : zr)
             for (auto &yy : yr)
                 for (auto &xx : xr) {
-                    Item it{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second};
+                    Item it{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second, 0, 0, 0.f, 0};
                     out.push_back(it);
                     size_t nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
                     size_t nyn = c->h_cb[1][it.y0 + it.ylen - 1] + 4 - c->h_cb[1][it.y0];
                     size_t nzn = c->h_cb[2][it.z0 + it.zlen - 1] + 4 - c->h_cb[2][it.z0];
                     npmax = std::max(npmax, nzn * 3 * nyn * nxn);
+                    if (nxn > 32) npmax = SIZE_MAX;   // ffd_layer contracts y for <= 32 x-nodes
                 }
     };
     for (;;) {
@@ -452,6 +452,58 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (npmax > 16384) return fail(c, SRWCR_EINVAL, "control lattice too fine for the node window (%zu)", npmax);
     c->nitems = (int)items.size();
     c->nitems_full = (int)items_full.size();
+
+    // per item: fixed bins present (slot lists), binless shift cI, spatial weight sums
+    std::vector<int> slotbins;
+    int smax = 1;
+    auto scan_items = [&](std::vector<Item> &its, ItemW **dw) -> srwcr_status {
+        const size_t n = its.size();
+        if (n == 0) return SRWCR_OK;
+        Item *d_it = nullptr;
+        unsigned *d_mask = nullptr;
+        double *d_sum = nullptr;
+        CK(cudaMalloc(&d_it, sizeof(Item) * n));
+        CK(cudaMalloc(&d_mask, sizeof(unsigned) * 4 * n));
+        CK(cudaMalloc(&d_sum, sizeof(double) * n));
+        CK(cudaMemcpy(d_it, its.data(), sizeof(Item) * n, cudaMemcpyHostToDevice));
+        k_item_scan<<<(unsigned)n, 256>>>(c->F, c->M, d_it, g, d_mask, d_sum);
+        CKL();
+        std::vector<unsigned> mask(4 * n);
+        std::vector<double> sum(n);
+        CK(cudaMemcpy(mask.data(), d_mask, sizeof(unsigned) * 4 * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(sum.data(), d_sum, sizeof(double) * n, cudaMemcpyDeviceToHost));
+        cudaFree(d_it);
+        cudaFree(d_mask);
+        cudaFree(d_sum);
+        std::vector<ItemW> w(n);
+        for (size_t i = 0; i < n; ++i) {
+            Item &it = its[i];
+            it.slot_off = (int)slotbins.size();
+            int ns = 0;
+            for (int b = 0; b < g.B; ++b)
+                if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
+            it.nslots = ns;
+            smax = std::max(smax, ns);
+            it.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
+            ItemW &iw = w[i];
+            for (int l = 0; l < 4; ++l) iw.sx[l] = iw.sy[l] = iw.sz[l] = 0.0;
+            const int lo[3] = {it.x0, it.y0, it.z0}, len[3] = {it.xlen, it.ylen, it.zlen};
+            double *dst[3] = {iw.sx, iw.sy, iw.sz};
+            for (int ax = 0; ax < 3; ++ax)
+                for (int k = lo[ax]; k < lo[ax] + len[ax]; ++k) {
+                    const float4 q = c->h_sw[ax][k];
+                    dst[ax][0] += q.x; dst[ax][1] += q.y; dst[ax][2] += q.z; dst[ax][3] += q.w;
+                }
+        }
+        CK(cudaMalloc(dw, sizeof(ItemW) * n));
+        CK(cudaMemcpy(*dw, w.data(), sizeof(ItemW) * n, cudaMemcpyHostToDevice));
+        return SRWCR_OK;
+    };
+    TRY(scan_items(items, &c->itemw));
+    TRY(scan_items(items_full, &c->itemw_full));
+    c->S = smax;
+    CK(cudaMalloc(&c->slotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
+    CK(cudaMemcpy(c->slotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
     if (c->nitems) {
         CK(cudaMalloc(&c->items, sizeof(Item) * items.size()));
         CK(cudaMemcpy(c->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
@@ -464,11 +516,11 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->phi, sizeof(float) * c->nint));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
-    CK(cudaMalloc(&c->SQ, sizeof(double) * RB * 4));
+    CK(cudaMalloc(&c->SQ, sizeof(double) * stats_count(c)));
+    c->Qt = c->SQ + RB * 2;
     CK(cudaMalloc(&c->Nlo, sizeof(double) * RB));
     CK(cudaMalloc(&c->Nup, sizeof(double) * RB));
     CK(cudaMalloc(&c->S_out, sizeof(double) * RB));
-    CK(cudaMalloc(&c->Q_out, sizeof(double) * RB));
     CK(cudaMalloc(&c->dterm, sizeof(double) * c->R));
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
     CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
@@ -480,19 +532,20 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMemset(c->params64, 0, sizeof(double) * c->nparams));
     c->cur_params = c->params64;
 
-    // fixed-point scales of the pass-1 line tables: |value * scale| < 2^22 (magic-number
-    // conversion), and a line sums at most 32 voxels (no int32 overflow)
-    const double Ld = g.L;
-    c->scaleA = (float)std::ldexp(1.0, (int)std::floor(std::log2(4194303.0 / (Ld + 1.0))));
-    c->scaleB = (float)std::ldexp(1.0, (int)std::floor(std::log2(4194303.0 / ((Ld + 1.0) * (Ld + 1.0)))));
-
-    c->smem1 = sizeof(int) * NW * g.B * LT_STRIDE + sizeof(unsigned) * NW * 4 + sizeof(int) * NW * 2 + sizeof(float4) * NW + sizeof(float) * g.B;
-    c->smem2 = sizeof(float) * (64 * g.B + 16 * g.B) + sizeof(float4) * NW * g.B + sizeof(float) * (64 + 64 + 32 + NW * 96) +
-               sizeof(float) * npmax;
+    // shared memory and warps per CTA of each pass: the largest W in {16, 12, 8, 6, 4} that fits
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-    if ((int)c->smem1 > maxsm || (int)c->smem2 > maxsm)
-        return fail(c, SRWCR_EINVAL, "shared memory need %zu/%zu B exceeds %d B", c->smem1, c->smem2, maxsm);
+    const int Wc[5] = {16, 12, 8, 6, 4};
+    c->W = c->W2 = 0;
+    for (int W : Wc) {
+        const size_t s1 = sizeof(int) * (((size_t)W * c->S * LTS + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * 32 +
+                          sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16;
+        if (!c->W && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
+        const size_t s2 = sizeof(float4) * (size_t)W * g.B * (GYS + 1) +
+                          sizeof(float) * (64 * (size_t)g.B + (g.B + 1) + 128 + W * 192) + sizeof(float) * npmax;
+        if (!c->W2 && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
+    }
+    if (c->W == 0 || c->W2 == 0) return fail(c, SRWCR_EINVAL, "shared memory too small for %d bins / %d slots", g.B, c->S);
     TRY(set_smem(c));
 
     // NCCL communicator for the z-slab decomposition
@@ -509,7 +562,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
 
     // static weighted counts N[r][a] (lower / upper Parzen half) over the whole volume
     // (every rank holds the full F, so no create-time collective is needed)
-    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * RB * 4, c->stream));
+    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
     TRY(launch_pass1(c, true, true));
     k_split_counts<<<512, 256, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, RB);
     CKL();
@@ -528,7 +581,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         for (int b = 0; b < g.B; ++b) sh[b] = (float)b;
         CK(cudaMemcpy(c->shiftc, sh.data(), sizeof(float) * g.B, cudaMemcpyHostToDevice));
         if (o.moment_shift) {
-            CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * RB * 4, c->stream));
+            CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
             TRY(launch_pass1(c, false, true));
             float *tmp = nullptr;
             CK(cudaMalloc(&tmp, sizeof(float) * g.B));
@@ -585,7 +638,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
     CKL();
-    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * c->R * c->g.B * 4, c->stream));
+    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
     TRY(launch_pass1(c, false));
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
     return SRWCR_OK;
@@ -624,7 +677,7 @@ extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *v
     if (!c) return SRWCR_EINVAL;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
     TRY(eval_begin_impl(c, params));
-    TRY(allreduce(c, c->SQ, (size_t)c->R * c->g.B * 4));
+    TRY(allreduce(c, c->SQ, stats_count(c)));
     return eval_end_impl(c, value, grad, true);
 }
 
@@ -638,7 +691,7 @@ extern "C" srwcr_status srwcr_eval_begin(srwcr_ctx *c, const double *params) {
 extern "C" srwcr_status srwcr_stats_buffer(srwcr_ctx *c, double **dev_ptr, size_t *count) {
     if (!c || !dev_ptr || !count) return SRWCR_EINVAL;
     *dev_ptr = c->SQ;
-    *count = (size_t)c->R * c->g.B * 4;
+    *count = stats_count(c);
     return SRWCR_OK;
 }
 extern "C" srwcr_status srwcr_eval_end(srwcr_ctx *c, double *value, double *grad) {
@@ -657,7 +710,7 @@ extern "C" srwcr_status srwcr_debug_size(const srwcr_ctx *c, int32_t what, size_
         case SRWCR_DUMP_A0: *bytes = sizeof(short) * nvox; break;
         case SRWCR_DUMP_CTRL_TAPS: case SRWCR_DUMP_SPAT_TAPS: *bytes = sizeof(int) * (c->g.nx + c->g.ny + c->g.nz); break;
         case SRWCR_DUMP_N: *bytes = sizeof(double) * RB; break;
-        case SRWCR_DUMP_SQ: *bytes = sizeof(double) * RB * 2; break;
+        case SRWCR_DUMP_SQ: *bytes = sizeof(double) * (RB + c->R); break;
         case SRWCR_DUMP_REGIONS: *bytes = sizeof(double) * c->R * 6; break;
         case SRWCR_DUMP_COEFS: *bytes = sizeof(float) * (2 * c->R + RB); break;
         default: return SRWCR_EINVAL;
@@ -707,7 +760,7 @@ extern "C" srwcr_status srwcr_debug_dump(srwcr_ctx *c, int32_t what, void *out, 
         }
         case SRWCR_DUMP_SQ:
             CK(cudaMemcpy(out, c->S_out, sizeof(double) * RB, cudaMemcpyDeviceToHost));
-            CK(cudaMemcpy((double *)out + RB, c->Q_out, sizeof(double) * RB, cudaMemcpyDeviceToHost));
+            CK(cudaMemcpy((double *)out + RB, c->Qt, sizeof(double) * c->R, cudaMemcpyDeviceToHost));
             break;
         case SRWCR_DUMP_REGIONS: CK(cudaMemcpy(out, c->reg, need, cudaMemcpyDeviceToHost)); break;
         case SRWCR_DUMP_COEFS:
@@ -732,6 +785,10 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->ms_combine = c->ms[1];
     out->ms_pass2 = c->ms[2];
     out->ms_total = c->ms[3];
+    out->warps_per_cta = c->W;
+    out->slot_capacity = c->S;
+    out->voxels_per_lane = c->XV;
+    out->items = c->nitems;
     return SRWCR_OK;
 }
 extern "C" srwcr_status srwcr_stream(const srwcr_ctx *c, void **stream) {
@@ -746,8 +803,9 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg,
-                    c->Dout, c->S_out, c->Q_out, c->shiftc, c->alpha, c->beta, c->gamma};
+    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->itemw, c->itemw_full,
+                    c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
+                    c->beta, c->gamma};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

@@ -8,20 +8,21 @@
 // kernels 1-4 materialise them).  DESIGN.md s5-s6 describe the data flow,
 // the roofline of each kernel and what differs from the paper's GPU design.
 //
-// Work decomposition: a CTA of 16 warps owns one "item" = a box of voxels inside
-// ONE spatial cell (so all its voxels share the same 4x4x4 = 64 regions of Eq 7).
-// Lane = x (<= 32 voxels), warp = one row y of a 16-row chunk, and the CTA marches
-// z through the item one slice at a time.
+// Work decomposition (v2): a CTA owns one "item" = a box of voxels inside ONE spatial
+// cell (all its voxels share the same 4x4x4 = 64 regions of Eq 7).  Each warp owns
+// whole rows of the item: lane = x (XV voxels per lane: x0+lane, x0+lane+32), and the
+// warp marches z through the item independently of the other warps (no CTA barrier
+// inside the march).  CTA-level tables are touched only at row and item ends.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 namespace srwcr {
 
-constexpr int NW = 16;          // warps per CTA
-constexpr int NT = NW * 32;     // threads per CTA
 constexpr unsigned FULL = 0xffffffffu;
-constexpr int LT_STRIDE = 17;   // line-table row stride (16 entries + 1 pad: conflict-free rows)
+constexpr int LTS = 9;          // line-table slot stride: 8 entries (4 x-taps x {lo, hi}) + 1 pad
+constexpr int GYS = 5;          // pass-2 per-warp gamma table: float4 per (bin, x-tap), 4 + 1 pad per bin
+constexpr int MAXW = 16;        // max warps per CTA
 
 struct Tables {                 // per-axis B-spline taps, index = voxel coordinate on that axis
     const int *cb[3];           // control lattice: tap base floor(i/delta)          (Eq 17)
@@ -40,7 +41,13 @@ struct Geo {
     int ndim, GzExt;            // external components (2 or 3) and external Gz
 };
 
-struct Item { int x0, xlen, y0, ylen, z0, zlen; };
+struct Item {
+    int x0, xlen, y0, ylen, z0, zlen;
+    int slot_off, nslots;       // the item's fixed bins a0 (static slot list in slotbins)
+    float cI;                   // binless moment shift of the item (mean of M over the box)
+    int pad;
+};
+struct ItemW { double sx[4], sy[4], sz[4]; };  // per-item sums of the fp32 spatial weights
 
 struct PassArgs {
     Geo g;
@@ -48,10 +55,13 @@ struct PassArgs {
     const float *F;             // normalised fixed image  (model image A)
     const float *M;             // normalised moving image (estimated image B after warping)
     const float *phi;           // fp32 displacements [3][Gz][Gy][Gx]
-    const float *shiftc;        // per-fixed-bin moment shift c_a (pass 1)
+    const float *shiftc;        // per-fixed-bin shift c_a of the binned first moment
     const Item *items;
-    double *SQ;                 // pass 1 out: [R][B][4] shifted partial moments (fp64)
-    float scaleA, scaleB;       // pass 1 fixed-point scales of the line tables
+    const ItemW *itemw;
+    const int *slotbins;        // concatenated per-item slot -> bin lists
+    double *SQ;                 // pass 1 out: [R][B][2] shifted binned first moments (lo, hi)
+    double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
+    int W, S;                   // warps per CTA, slot capacity of the smem tables
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
@@ -62,15 +72,21 @@ struct PassArgs {
 __device__ __forceinline__ float f4(const float4 &v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
+__device__ __forceinline__ float dot4(const float4 &a, const float4 &b) {
+    return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
+}
+// 2^k as a float, k in [-126, 127]
+__device__ __forceinline__ float exp2i(int k) { return __int_as_float((k + 127) << 23); }
 
 // ---------------------------------------------------------------- FFD
-// Contribution of control layer gz to this lane's displacement, contracted over the
-// 4x4 (x, y) taps: U[c] = sum_{l,m} cwx_l cwy_m phi[c][gz][cby+m][cbx+l].  The warp
-// shares one row y, so lanes j < nxn first contract y for x-node xn0+j (coalesced
-// loads), then every lane gathers its 4 x-taps by shuffle.
-__device__ __forceinline__ void ffd_layer(const float *__restrict__ phi, const Geo &g, int gz, int cby,
-                                          float4 cwy, int xn0, int nxn, int relx, float4 cwx, int lane,
-                                          float U[3]) {
+// Contribution of control layer gz to the displacements of this lane's XV voxels,
+// contracted over the 4x4 (x, y) taps: U[v][c] = sum_{l,m} cwx_l cwy_m phi[c][gz][cby+m][cbx_v+l].
+// The warp shares one row y, so lanes j < nxn first contract y for x-node xn0+j
+// (coalesced loads), then every lane gathers its 4 x-taps per voxel by shuffle.
+template <int XV>
+__device__ __forceinline__ void ffd_layer(const float *__restrict__ phi, const Geo &g, int gz, int cby, float4 cwy,
+                                          int xn0, int nxn, const int (&relx)[XV], const float4 (&cwx)[XV],
+                                          int lane, float (&U)[XV][3]) {
     float p0 = 0.f, p1 = 0.f, p2 = 0.f;
     if (lane < nxn) {
         const long long plane = (long long)g.Gx * g.Gy;
@@ -78,20 +94,23 @@ __device__ __forceinline__ void ffd_layer(const float *__restrict__ phi, const G
         const float *p = phi + (long long)gz * plane + (long long)cby * g.Gx + xn0 + lane;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
-            float w = f4(cwy, m);
+            const float w = f4(cwy, m);
             p0 = fmaf(w, __ldg(p + m * g.Gx), p0);
             p1 = fmaf(w, __ldg(p + cs + m * g.Gx), p1);
             p2 = fmaf(w, __ldg(p + 2 * cs + m * g.Gx), p2);
         }
     }
-    U[0] = U[1] = U[2] = 0.f;
 #pragma unroll
-    for (int l = 0; l < 4; ++l) {
-        int src = relx + l;
-        float w = f4(cwx, l);
-        U[0] = fmaf(w, __shfl_sync(FULL, p0, src), U[0]);
-        U[1] = fmaf(w, __shfl_sync(FULL, p1, src), U[1]);
-        U[2] = fmaf(w, __shfl_sync(FULL, p2, src), U[2]);
+    for (int v = 0; v < XV; ++v) {
+        U[v][0] = U[v][1] = U[v][2] = 0.f;
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int src = relx[v] + l;
+            const float w = f4(cwx[v], l);
+            U[v][0] = fmaf(w, __shfl_sync(FULL, p0, src), U[v][0]);
+            U[v][1] = fmaf(w, __shfl_sync(FULL, p1, src), U[v][1]);
+            U[v][2] = fmaf(w, __shfl_sync(FULL, p2, src), U[v][2]);
+        }
     }
 }
 
@@ -102,9 +121,9 @@ __device__ __forceinline__ void ffd_layer(const float *__restrict__ phi, const G
 // report `clamped` (their derivative is 0, reading c2); cell = min(floor y, N-2).
 __device__ __forceinline__ void axis_cell(int i, float u, int N, int &c0, float &t, bool &cl) {
     if (N == 1) { c0 = 0; t = 0.f; cl = true; return; }
-    float fu = floorf(u);
-    int c = i + (int)fu;
-    float tt = u - fu;
+    const float fu = floorf(u);
+    const int c = i + (int)fu;
+    const float tt = u - fu;
     if (c < 0) { c0 = 0; t = 0.f; cl = true; }
     else if (c >= N - 1) { c0 = N - 2; t = 1.f; cl = !(c == N - 1 && tt == 0.f); }
     else { c0 = c; t = tt; cl = false; }
@@ -124,15 +143,15 @@ __device__ __forceinline__ float sample_m(const float *__restrict__ M, const Geo
     axis_cell(z, uz, g.nz, cz, tz, clz);
     const long long dyo = g.nx, dzo = g.nz > 1 ? g.nxy : 0;
     const float *b = M + (long long)cz * g.nxy + (long long)cy * g.nx + cx;
-    float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + dyo), c110 = __ldg(b + dyo + 1);
-    float c001 = __ldg(b + dzo), c101 = __ldg(b + dzo + 1), c011 = __ldg(b + dzo + dyo),
-          c111 = __ldg(b + dzo + dyo + 1);
-    float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
-    float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
-    float f0 = lerpf(e00, e10, ty), f1 = lerpf(e01, e11, ty);
+    const float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + dyo), c110 = __ldg(b + dyo + 1);
+    const float c001 = __ldg(b + dzo), c101 = __ldg(b + dzo + 1), c011 = __ldg(b + dzo + dyo),
+                c111 = __ldg(b + dzo + dyo + 1);
+    const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
+    const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
+    const float f0 = lerpf(e00, e10, ty), f1 = lerpf(e01, e11, ty);
     if (GRAD) {
-        float dx0 = lerpf(c100 - c000, c110 - c010, ty), dx1 = lerpf(c101 - c001, c111 - c011, ty);
-        float dy0 = lerpf(c010 - c000, c110 - c100, tx), dy1 = lerpf(c011 - c001, c111 - c101, tx);
+        const float dx0 = lerpf(c100 - c000, c110 - c010, ty), dx1 = lerpf(c101 - c001, c111 - c011, ty);
+        const float dy0 = lerpf(c010 - c000, c110 - c100, tx), dy1 = lerpf(c011 - c001, c111 - c101, tx);
         gx = clx ? 0.f : lerpf(dx0, dx1, tz);
         gy = cly ? 0.f : lerpf(dy0, dy1, tz);
         gz = clz ? 0.f : (f1 - f0);
@@ -145,283 +164,403 @@ __device__ __forceinline__ float sample_m(const float *__restrict__ M, const Geo
 // h(f) and h(1-f), written so that f = 0 and f = 1 give exact zeros (reading c5).
 __device__ __forceinline__ void parzen_pair(float f, float &hlo, float &hhi) {
     if (f < 0.5f) {
-        float w = f * fmaf(1.8f, f, 0.1f);
+        const float w = f * fmaf(1.8f, f, 0.1f);
         hhi = w;
         hlo = 1.0f - w;
     } else {
-        float s = 1.0f - f;
-        float w = s * fmaf(1.8f, s, 0.1f);
+        const float s = 1.0f - f;
+        const float w = s * fmaf(1.8f, s, 0.1f);
         hlo = w;
         hhi = 1.0f - w;
     }
 }
 
+// recursive-halving warp reduction of 8 per-lane values: afterwards every lane holds
+// the warp total of value (lane >> 2)   (9 shuffles)
+__device__ __forceinline__ float halving8(const float (&v)[8], int lane) {
+    float r4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float send = (lane & 16) ? v[i] : v[i + 4], keep = (lane & 16) ? v[i + 4] : v[i];
+        r4[i] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+    float r2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const float send = (lane & 8) ? r4[i] : r4[i + 2], keep = (lane & 8) ? r4[i + 2] : r4[i];
+        r2[i] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    const float send = (lane & 4) ? r2[0] : r2[1], keep = (lane & 4) ? r2[1] : r2[0];
+    float r = keep + __shfl_xor_sync(FULL, send, 4);
+    r += __shfl_xor_sync(FULL, r, 2);
+    r += __shfl_xor_sync(FULL, r, 1);
+    return r;
+}
+
+// position of the r-th (0-based) set bit of w (branch-free 5-step select)
+__device__ __forceinline__ int select_bit(unsigned w, int r) {
+    int pos = 0;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const unsigned lo = w & ((1u << s) - 1u);
+        const int c = __popc(lo);
+        const bool up = r >= c;
+        r = up ? r - c : r;
+        w = up ? (w >> s) : lo;
+        pos += up ? s : 0;
+    }
+    return pos;
+}
+// the j-th set bit of a (<= 128-bit) mask, or -1
+__device__ __forceinline__ int mask_select(const unsigned (&bits)[4], int nw, int j) {
+    int pos = -1, base = 0;
+    for (int k = 0; k < nw; ++k) {
+        const int c = __popc(bits[k]);
+        if (pos < 0 && j >= base && j < base + c) pos = 32 * k + select_bit(bits[k], j - base);
+        base += c;
+    }
+    return pos;
+}
+
+// sample cell along one axis (pass 1: no clamp flag): one unsigned compare on the fast path
+__device__ __forceinline__ int axis_fast(int i, float u, int nm2, float &t) {
+    const float fu = floorf(u);
+    int c = i + (int)fu;
+    t = u - fu;
+    if ((unsigned)c > (unsigned)nm2) {
+        if (c < 0) { c = 0; t = 0.f; }
+        else { c = nm2; t = 1.f; }
+    }
+    return c;
+}
+// same with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
+// flag telling that the fp32 position lies within tol of an integer, i.e. of a cell or
+// clamp boundary where the derivative of the interpolant jumps
+__device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, float &t, bool &cl, bool &near) {
+    const float fu = floorf(u);
+    int c = i + (int)fu;
+    t = u - fu;
+    cl = false;
+    near = t < tol || t > 1.0f - tol;
+    if ((unsigned)c > (unsigned)nm2) {
+        if (c < 0) { near = c == -1 && t > 1.0f - tol; c = 0; t = 0.f; cl = true; }
+        else { near = c == nm2 + 1 && t < tol; cl = !(c == nm2 + 1 && t == 0.f); c = nm2; t = 1.f; }
+    }
+    return c;
+}
+
 // ---------------------------------------------------------------- pass 1
-// Accumulates, per region r and fixed bin a0 (the lower of the two Parzen bins of F),
-// the four shifted moments  T0 = sum w_r h_lo (g1 - c), T1 = sum w_r h_hi (g1 - c),
-// T2 = sum w_r h_lo q', T3 = sum w_r h_hi q'  with g1 = sum_b b h(b - m) and
-// q' = sum_b (b - c)^2 h(b - m) = (g1 - c)^2 + w1 (1 - w1)  (Eq 3 P:73 rewritten as
-// moments; c = c_{a0}).  STATIC mode accumulates the weighted counts
-// (T0 = sum w_r h_lo, T1 = sum w_r h_hi) instead, in fp32 so that the zero pattern of
-// N is exact.
+// Moving-as-B orientation: the fixed-image bins and the spatial weights are static, so
+// the combine needs, per region r,
+//   binned (per fixed bin a):  S_ra = sum_x w_r h_a(F) g1(m),  g1 = sum_b b h(b - m)
+//   binless:                   Q_r  = sum_x w_r g2(m),          g2 = sum_b b^2 h(b - m)
+// (Eq 3 P:73 rewritten as moments; V_r = Q_r - sum_a S_ra^2/N_ra needs
+// Q only per region).  Per voxel the binned part is keyed by a0 (the lower Parzen bin of
+// F) with two channels  lo = h_lo (g1 - c_a0),  hi = h_hi (g1 - c_a0)  (c_a: per-bin
+// shift), times the 4 spatial x-taps -> 8 values.  The binless part is q' = (g1 - cI)^2
+// + w1 (1 - w1) and g1 - cI (cI: per-item shift), times the 4 x-taps.
 //
-// Privatisation: per voxel, 16 values (4 spatial x-taps x 4 channels)
-// go into the warp's line table LT[warp][a0][16] (int32 fixed point, native ATOMS;
-// a warp whose 32 lanes share a0 reduces in registers first).  After each slice the
-// CTA folds the 16 line tables into register accumulators owned by half-warps (half-
-// warp h owns bins h, h+32, ...; lane e owns entry e = 4*xtap + channel), applying
-// the row's y-weights; at the end of the slice the z-weights; at the end of the item
-// the owners flush 64 regions x owned bins x 16 entries to SQ with fp64 atomics.
-template <int KB, bool STATIC>
-__global__ void __launch_bounds__(NT, 1) k_pass1(PassArgs a) {
+// Privatisation, all per warp, no CTA barrier inside the march:
+//   line  : LT[warp][slot][8]  int32 fixed point (native ATOMS; warp-uniform bins reduce
+//           in registers), one 32/64-voxel line = one (row, z)
+//   column: K[warp][slot][8][4 z-taps]  fp32, after every line; 4 slots per instruction
+//   cell  : CT[slot][4 y-taps][32]  fp32 (CTA), after every row: K x wy, float atomics
+//   global: SQ[r][bin][2] fp64 atomics, once per item
+// STATIC mode accumulates the weighted counts (lo = h_lo, hi = h_hi) in fp32 (float
+// line tables) so that the zero pattern of N is exact.
+// Lanes past the item's x-extent sample the item's last column with zero weights, so
+// the voxel loop has no divergent branches.
+template <int XV, bool STATIC>
+__global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
-    const int B = g.B;
-    int *LT = reinterpret_cast<int *>(smem);                       // [NW][B][LT_STRIDE]
-    unsigned *mask = reinterpret_cast<unsigned *>(LT + NW * B * LT_STRIDE);  // [NW][4]
-    int *lexp = reinterpret_cast<int *>(mask + NW * 4);            // [NW][2] line exponents (A, q')
-    float4 *wyrow = reinterpret_cast<float4 *>(lexp + NW * 2);     // [NW]
-    float *shc = reinterpret_cast<float *>(wyrow + NW);            // [B]
+    const int B = g.B, W = a.W, S = a.S;
+    const int ltsz = (W * S * LTS + 3) & ~3;                      // keep K 16-byte aligned
+    int *LT = reinterpret_cast<int *>(smem);                      // [W][S][LTS]
+    float *K = reinterpret_cast<float *>(LT + ltsz);              // [W][S][32]  (entry*4 + n)
+    float *CT = K + W * S * 32;                                   // [S][4][32]
+    float *CB = CT + S * 128;                                     // [4][32] binless cell table
+    float *shc = CB + 128;                                        // [B]
+    unsigned char *smap = reinterpret_cast<unsigned char *>(shc + B);  // [B] bin -> slot
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = a.items[blockIdx.x];
-    const int hw = warp * 2 + (lane >> 4), e = lane & 15;
+    const int ns = it.nslots;
+    const int nwords = (ns + 31) >> 5;
 
-    for (int i = threadIdx.x; i < NW * B * LT_STRIDE; i += NT) LT[i] = 0;
-    for (int i = threadIdx.x; i < B; i += NT) shc[i] = STATIC ? 0.f : a.shiftc[i];
-
-    const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
-    const int x = it.x0 + lane;
-    const bool lane_ok = lane < it.xlen;
-    const int xc = min(x, g.nx - 1);
-    const int cbx = a.t.cb[0][xc];
-    const float4 cwx = a.t.cw[0][xc];
-    const float4 swx = a.t.sw[0][xc];
-    const int xn0 = a.t.cb[0][it.x0];
-    const int nxn = a.t.cb[0][it.x0 + it.xlen - 1] + 4 - xn0;
-    const int relx = cbx - xn0;
-    // fixed-point exponents of the line tables (dynamic mode): a value v_c * wx_l is
-    // scaled by 2^(274 - El - Ec) where 2^(El-126) bounds max_lanes wx_l (static per
-    // item) and 2^(Ec-126) bounds max_lanes |v_c| (per line), so |scaled| < 2^22
-    // (exact magic-number conversion) and a 32-lane sum stays < 2^27.
-    int El[4];
-#pragma unroll
-    for (int l = 0; l < 4; ++l)
-        El[l] = (int)(__reduce_max_sync(FULL, lane_ok ? __float_as_uint(f4(swx, l)) : 0u) >> 23);
-    const int El_e = El[0] * ((e >> 2) == 0) + El[1] * ((e >> 2) == 1) + El[2] * ((e >> 2) == 2) + El[3] * ((e >> 2) == 3);
-
-    float C[KB][16];
-    float acc[KB][4];
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) C[k][i] = 0.f;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[k][i] = 0.f;
+    for (int i = threadIdx.x; i < ltsz; i += blockDim.x) LT[i] = 0;
+    for (int i = threadIdx.x; i < W * S * 32; i += blockDim.x) K[i] = 0.f;
+    for (int i = threadIdx.x; i < ns * 128 + 128; i += blockDim.x) (i < ns * 128 ? CT[i] : CB[i - ns * 128]) = 0.f;
+    for (int i = threadIdx.x; i < B; i += blockDim.x) {
+        shc[i] = STATIC ? 0.f : a.shiftc[i];
+        smap[i] = 0xFF;
     }
     __syncthreads();
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) smap[a.slotbins[it.slot_off + s]] = (unsigned char)s;
 
-    for (int ys = it.y0; ys < it.y0 + it.ylen; ys += NW) {
-        const int y = ys + warp;
-        const bool row_ok = y < it.y0 + it.ylen;
-        const int yc = min(y, g.ny - 1);
-        const int cby = a.t.cb[1][yc];
-        const float4 cwy = a.t.cw[1][yc];
-        if (lane == 0) wyrow[warp] = row_ok ? a.t.sw[1][yc] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const bool ok = lane_ok && row_ok;
-
-        int gzl = a.t.cb[2][it.z0];
-        float U[4][3];
+    const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
+    const int xn0 = a.t.cb[0][it.x0];
+    const int nxn = a.t.cb[0][it.x0 + it.xlen - 1] + 4 - xn0;
+    int xv[XV], relx[XV];
+    float4 cwx[XV], swx[XV];
 #pragma unroll
-        for (int n = 0; n < 4; ++n) ffd_layer(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+    for (int v = 0; v < XV; ++v) {
+        const bool ok = lane + 32 * v < it.xlen;
+        xv[v] = ok ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+        relx[v] = a.t.cb[0][xv[v]] - xn0;
+        cwx[v] = a.t.cw[0][xv[v]];
+        swx[v] = ok ? a.t.sw[0][xv[v]] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    // fixed-point exponents (dynamic mode): value v_c * wx_l is scaled by 2^(274 - El - EA)
+    // where 2^(El-126) bounds max_lanes wx_l (static per item) and 2^(EA-126) bounds
+    // max_lanes |g1 - c| (per line): |scaled| < 2^22 (exact magic-number conversion) and a
+    // 64-value lane sum stays < 2^28.
+    int El[4];
+#pragma unroll
+    for (int l = 0; l < 4; ++l) {
+        float mx = 0.f;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) mx = fmaxf(mx, f4(swx[v], l));
+        El[l] = (int)(__reduce_max_sync(FULL, __float_as_uint(mx)) >> 23);
+    }
+    const int le = (lane & 7) >> 1;                               // fold lane's x-tap
+    const int El_e = le == 0 ? El[0] : le == 1 ? El[1] : le == 2 ? El[2] : El[3];
+    const float cI = it.cI;
+    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = g.nz - 2;
+    const int dzo = g.nz > 1 ? nxy : 0;
+    const float *__restrict__ Mv = a.M;
+    __syncthreads();
+
+    int *LTw = LT + warp * S * LTS;
+    float *Kw = K + warp * S * 32;
+
+    for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
+        const int cby = a.t.cb[1][y];
+        const float4 cwy = a.t.cw[1][y];
+        const float4 swy = a.t.sw[1][y];
+        const float *__restrict__ Frow = a.F + y * nx;
+        int gzl = a.t.cb[2][it.z0];
+        float U[4][XV][3];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+        float bacc = 0.f;
+        unsigned wmask[4] = {0u, 0u, 0u, 0u};
 
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
             const int bz = a.t.cb[2][z];
-            while (gzl < bz) {                           // slide the 4-layer window
+            while (gzl < bz) {                                   // slide the 4-layer window
 #pragma unroll
-                for (int n = 0; n < 3; ++n) { U[n][0] = U[n + 1][0]; U[n][1] = U[n + 1][1]; U[n][2] = U[n + 1][2]; }
+                for (int n = 0; n < 3; ++n)
+#pragma unroll
+                    for (int v = 0; v < XV; ++v) { U[n][v][0] = U[n + 1][v][0]; U[n][v][1] = U[n + 1][v][1]; U[n][v][2] = U[n + 1][v][2]; }
                 ++gzl;
-                ffd_layer(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
+                ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
             }
             const float4 cwz = a.t.cw[2][z];
-            float ux = 0.f, uy = 0.f, uz = 0.f;
+            const float4 wz = a.t.sw[2][z];
+            const float *__restrict__ Fz = Frow + z * nxy;
+            int a0[XV], slot[XV];
+            float lo[XV], hi[XV];
+            float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
+            float amax = 0.f;
 #pragma unroll
-            for (int n = 0; n < 4; ++n) {
-                float w = f4(cwz, n);
-                ux = fmaf(w, U[n][0], ux);
-                uy = fmaf(w, U[n][1], uy);
-                uz = fmaf(w, U[n][2], uz);
-            }
-            int a0 = 0;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
-            if (ok) {
-                const long long idx = (long long)z * g.nxy + (long long)y * g.nx + x;
-                const float Fv = __ldg(a.F + idx);
-                a0 = min((int)Fv, g.L - 1);
+            for (int v = 0; v < XV; ++v) {
+                const float Fv = __ldg(Fz + xv[v]);
+                a0[v] = min((int)Fv, g.L - 1);
+                slot[v] = smap[a0[v]];
                 float hlo, hhi;
-                parzen_pair(Fv - (float)a0, hlo, hhi);
+                parzen_pair(Fv - (float)a0[v], hlo, hhi);
                 if (STATIC) {
-                    v[0] = hlo;
-                    v[1] = hhi;
+                    lo[v] = hlo;
+                    hi[v] = hhi;
                 } else {
-                    float dgx, dgy, dgz;
-                    const float m = sample_m<false>(a.M, g, x, y, z, ux, uy, uz, dgx, dgy, dgz);
+                    const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
+                    const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
+                    const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
+                    float tx, ty, tz;
+                    const int ccx = axis_fast(xv[v], ux, nxm2, tx);
+                    const int ccy = axis_fast(y, uy, nym2, ty);
+                    const int ccz = axis_fast(z, uz, nzm2, tz);
+                    const float *__restrict__ b = Mv + (ccz * nxy + ccy * nx + ccx);
+                    const float *__restrict__ b3 = b + dzo;
+                    const float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + nx), c110 = __ldg(b + nx + 1);
+                    const float c001 = __ldg(b3), c101 = __ldg(b3 + 1), c011 = __ldg(b3 + nx), c111 = __ldg(b3 + nx + 1);
+                    const float f0 = lerpf(lerpf(c000, c100, tx), lerpf(c010, c110, tx), ty);
+                    const float f1 = lerpf(lerpf(c001, c101, tx), lerpf(c011, c111, tx), ty);
+                    const float m = lerpf(f0, f1, tz);
                     const int n = min(max((int)floorf(m), 0), g.L - 1);
-                    const float fm = m - (float)n;
                     float w1l, w1;
-                    parzen_pair(fm, w1l, w1);
-                    const float A = ((float)n - shc[a0]) + w1;       // g1 - c
-                    const float Bq = fmaf(A, A, w1 * w1l);           // (g1-c)^2 + w1(1-w1)
-                    v[0] = hlo * A;
-                    v[1] = hhi * A;
-                    v[2] = hlo * Bq;
-                    v[3] = hhi * Bq;
-                }
-            }
-            // ---- line table update
-            const unsigned okm = __ballot_sync(FULL, ok);
-            float sc[4][2];                                    // scale per (x-tap, channel group)
-            if (!STATIC) {
-                const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(fabsf(v[0]) + fabsf(v[1]))) >> 23);
-                const int EB = (int)(__reduce_max_sync(FULL, __float_as_uint(fabsf(v[2]) + fabsf(v[3]))) >> 23);
-                if (lane == 0) { lexp[warp * 2] = EA; lexp[warp * 2 + 1] = EB; }
-#pragma unroll
-                for (int l = 0; l < 4; ++l) {
-                    sc[l][0] = __int_as_float((min(274 - El[l] - EA, 120) + 127) << 23);
-                    sc[l][1] = __int_as_float((min(274 - El[l] - EB, 120) + 127) << 23);
-                }
-            }
-            if (okm) {
-                const int a0f = __shfl_sync(FULL, a0, __ffs(okm) - 1);
-                const bool uni = __all_sync(FULL, !ok || a0 == a0f);
-                int *row = LT + (warp * B + (uni ? a0f : a0)) * LT_STRIDE;
-                if (uni) {
-                    // recursive-halving warp reduction of the 16 values (x-tap l, channel c)
-                    float r8[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        int li = i >> 2, ci = i & 3;           // value i and i+8 (x-tap li+2)
-                        float lo = f4(swx, li) * v[ci], hi = f4(swx, li + 2) * v[ci];
-                        float send = (lane & 16) ? lo : hi, keep = (lane & 16) ? hi : lo;
-                        r8[i] = keep + __shfl_xor_sync(FULL, send, 16);
-                    }
-                    float r4[4];
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        float send = (lane & 8) ? r8[i] : r8[i + 4], keep = (lane & 8) ? r8[i + 4] : r8[i];
-                        r4[i] = keep + __shfl_xor_sync(FULL, send, 8);
-                    }
-                    float r2[2];
-#pragma unroll
-                    for (int i = 0; i < 2; ++i) {
-                        float send = (lane & 4) ? r4[i] : r4[i + 2], keep = (lane & 4) ? r4[i + 2] : r4[i];
-                        r2[i] = keep + __shfl_xor_sync(FULL, send, 4);
-                    }
-                    float send = (lane & 2) ? r2[0] : r2[1], keep = (lane & 2) ? r2[1] : r2[0];
-                    float r1 = keep + __shfl_xor_sync(FULL, send, 2);
-                    r1 += __shfl_xor_sync(FULL, r1, 1);
-                    // after the 5 halvings lane holds value index 8*b4 + 4*b3 + 2*b2 + b1 = lane>>1,
-                    // i.e. entry 4*xtap + channel (step 1 split the x-taps {0,1} | {2,3})
-                    const int ent = lane >> 1;
-                    if ((lane & 1) == 0) {
-                        if (STATIC) reinterpret_cast<float *>(row)[ent] += r1;
-                        // a 32-voxel sum can exceed the 2^22 range of the magic-number conversion
-                        else row[ent] += __float2int_rn(r1 * sc[ent >> 2][(ent & 3) >> 1]);
-                    }
-                } else if (ok) {
+                    parzen_pair(m - (float)n, w1l, w1);
+                    const float A = ((float)n - shc[a0[v]]) + w1;      // g1 - c_a0
+                    const float Ab = ((float)n - cI) + w1;            // g1 - cI
+                    const float q = fmaf(Ab, Ab, w1 * w1l);           // sum_b (b - cI)^2 h(b - m)
+                    lo[v] = hlo * A;
+                    hi[v] = hhi * A;
+                    amax = fmaxf(amax, fabsf(A));
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
-                        const float wl = f4(swx, l);
+                        bq[l] = fmaf(f4(swx[v], l), q, bq[l]);
+                        ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
+                    }
+                }
+            }
+            // ---- binless: warp-reduce (x-tap, channel) and fold the z-taps into bacc
+            if (!STATIC) {
+                const float bv[8] = {bq[0], ba[0], bq[1], ba[1], bq[2], ba[2], bq[3], ba[3]};
+                const float tot = halving8(bv, lane);          // value (lane>>2) = 2*l + ch
+                bacc = fmaf(f4(wz, lane & 3), tot, bacc);
+            }
+            // ---- binned: line table
+            float sc[4] = {1.f, 1.f, 1.f, 1.f}, isc_e = 1.f;
+            if (!STATIC) {
+                const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(amax)) >> 23);
 #pragma unroll
-                        for (int c = 0; c < (STATIC ? 2 : 4); ++c) {
-                            const float val = wl * v[c];
-                            if (STATIC) atomicAdd(reinterpret_cast<float *>(row) + l * 4 + c, val);
-                            else atomicAdd(row + l * 4 + c, __float_as_int(fmaf(val, sc[l][c >> 1], 12582912.f)) - 0x4B400000);
+                for (int l = 0; l < 4; ++l) sc[l] = exp2i(min(274 - El[l] - EA, 120));
+                isc_e = exp2i(-min(274 - El_e - EA, 120));
+            }
+            int amx = a0[0];
+#pragma unroll
+            for (int v = 1; v < XV; ++v) amx = max(amx, a0[v]);
+            const int af = (int)__reduce_max_sync(FULL, (unsigned)amx);
+            bool same = true;
+#pragma unroll
+            for (int v = 0; v < XV; ++v) same = same && a0[v] == af;
+            if (__all_sync(FULL, same)) {
+                float vv[8];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    float sl = 0.f, sh = 0.f;
+#pragma unroll
+                    for (int v = 0; v < XV; ++v) {
+                        sl = fmaf(f4(swx[v], l), lo[v], sl);
+                        sh = fmaf(f4(swx[v], l), hi[v], sh);
+                    }
+                    vv[2 * l] = sl;
+                    vv[2 * l + 1] = sh;
+                }
+                const float tot = halving8(vv, lane);
+                if ((lane & 3) == 0) {
+                    const int ent = lane >> 2;
+                    int *p = LTw + slot[0] * LTS + ent;
+                    if (STATIC) *reinterpret_cast<float *>(p) += tot;
+                    else *p += __float2int_rn(tot * (ent < 2 ? sc[0] : ent < 4 ? sc[1] : ent < 6 ? sc[2] : sc[3]));
+                }
+            } else {
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    int *row = LTw + slot[v] * LTS;
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        if (STATIC) {
+                            atomicAdd(reinterpret_cast<float *>(row) + 2 * l, f4(swx[v], l) * lo[v]);
+                            atomicAdd(reinterpret_cast<float *>(row) + 2 * l + 1, f4(swx[v], l) * hi[v]);
+                        } else {
+                            const float ws = f4(swx[v], l) * sc[l];
+                            atomicAdd(row + 2 * l, __float_as_int(fmaf(lo[v], ws, 12582912.f)) - 0x4B400000);
+                            atomicAdd(row + 2 * l + 1, __float_as_int(fmaf(hi[v], ws, 12582912.f)) - 0x4B400000);
                         }
                     }
                 }
             }
+            // ---- fold the line into the warp's column table, 4 slots per instruction:
+            //      K[slot][ent][n] += wz_n * LT[slot][ent]
+            unsigned bits[4] = {0u, 0u, 0u, 0u};
+            int cnt = 0;
+            for (int k = 0; k < nwords; ++k) {
+                unsigned mine = 0u;
 #pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                unsigned bits = __reduce_or_sync(FULL, (ok && (a0 >> 5) == k) ? (1u << (a0 & 31)) : 0u);
-                if (lane == 0) mask[warp * 4 + k] = bits;
+                for (int v = 0; v < XV; ++v) mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
+                bits[k] = __reduce_or_sync(FULL, mine);
+                wmask[k] |= bits[k];
+                cnt += __popc(bits[k]);
             }
-            __syncthreads();
-            // ---- fold the 16 line tables into the owners' registers
-            const float4 wz = a.t.sw[2][z];
-#pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                const int bin = hw + 32 * k;
-                const unsigned mw = mask[(lane & 15) * 4 + k];
-                const unsigned bal = __ballot_sync(FULL, bin < B && ((mw >> hw) & 1u));
-                const unsigned mine = (lane < 16) ? (bal & 0xFFFFu) : (bal >> 16);
-                unsigned uni = (bal & 0xFFFFu) | (bal >> 16);
-                while (uni) {
-                    const int j = __ffs(uni) - 1;
-                    uni &= uni - 1;
-                    if ((mine >> j) & 1u) {
-                        int *p = LT + (j * B + bin) * LT_STRIDE + e;
-                        float val;
-                        if (STATIC) val = __int_as_float(*p);
-                        else val = (float)(*p) * __int_as_float((127 - min(274 - El_e - lexp[j * 2 + ((e & 3) >> 1)], 120)) << 23);
-                        *p = 0;
-                        const float4 wy = wyrow[j];
-                        acc[k][0] = fmaf(wy.x, val, acc[k][0]);
-                        acc[k][1] = fmaf(wy.y, val, acc[k][1]);
-                        acc[k][2] = fmaf(wy.z, val, acc[k][2]);
-                        acc[k][3] = fmaf(wy.w, val, acc[k][3]);
-                    }
-                }
-                if (mine) {
-#pragma unroll
-                    for (int mm = 0; mm < 4; ++mm) {
-                        C[k][mm * 4 + 0] = fmaf(wz.x, acc[k][mm], C[k][mm * 4 + 0]);
-                        C[k][mm * 4 + 1] = fmaf(wz.y, acc[k][mm], C[k][mm * 4 + 1]);
-                        C[k][mm * 4 + 2] = fmaf(wz.z, acc[k][mm], C[k][mm * 4 + 2]);
-                        C[k][mm * 4 + 3] = fmaf(wz.w, acc[k][mm], C[k][mm * 4 + 3]);
-                        acc[k][mm] = 0.f;
+            __syncwarp();
+            const int ent = lane & 7;
+            for (int c0 = 0; c0 < cnt; c0 += 32) {
+                const int myslot = mask_select(bits, nwords, c0 + lane);
+                const int rmax = min(cnt - c0, 32);
+                for (int r = 0; r < rmax; r += 4) {
+                    const int idx = r + (lane >> 3);
+                    const int s = __shfl_sync(FULL, myslot, idx & 31);
+                    if (idx < rmax) {
+                        int *lp = LTw + s * LTS + ent;
+                        const int iv = *lp;
+                        *lp = 0;
+                        const float val = STATIC ? __int_as_float(iv) : (float)iv * isc_e;
+                        float4 *kp = reinterpret_cast<float4 *>(Kw + s * 32 + ent * 4);
+                        float4 k4 = *kp;
+                        k4.x = fmaf(wz.x, val, k4.x);
+                        k4.y = fmaf(wz.y, val, k4.y);
+                        k4.z = fmaf(wz.z, val, k4.z);
+                        k4.w = fmaf(wz.w, val, k4.w);
+                        *kp = k4;
                     }
                 }
             }
-            __syncthreads();
+            __syncwarp();
         }
-        __syncthreads();
-    }
-    // ---- flush: region (cz+n, cy+m, cx+l), bin, channel
-    const int l_e = e >> 2, ch = e & 3;
-#pragma unroll
-    for (int k = 0; k < KB; ++k) {
-        const int bin = hw + 32 * k;
-        if (bin >= B) continue;
-#pragma unroll
-        for (int mm = 0; mm < 4; ++mm)
-#pragma unroll
-            for (int n = 0; n < 4; ++n) {
-                const float val = C[k][mm * 4 + n];
+        // ---- row done: fold the column table with the row's y-weights into the cell table
+        for (int k = 0; k < nwords; ++k) {
+            unsigned bw = wmask[k];
+            while (bw) {
+                const int s = 32 * k + __ffs(bw) - 1;
+                bw &= bw - 1;
+                const float val = Kw[s * 32 + lane];
+                Kw[s * 32 + lane] = 0.f;
                 if (val != 0.f) {
-                    const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l_e);
-                    atomicAdd(a.SQ + (r * B + bin) * 4 + ch, (double)val);
+#pragma unroll
+                    for (int mm = 0; mm < 4; ++mm) atomicAdd(CT + (s * 4 + mm) * 32 + lane, f4(swy, mm) * val);
                 }
             }
+        }
+        if (!STATIC && bacc != 0.f) {
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) atomicAdd(CB + mm * 32 + lane, f4(swy, mm) * bacc);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    // ---- item done: flush to global.  CT entry (s, m, e): e = 8*l + 4*ch + n
+    for (int t = threadIdx.x; t < ns * 128; t += blockDim.x) {
+        const float val = CT[t];
+        if (val == 0.f) continue;
+        const int s = t >> 7, mm = (t >> 5) & 3, e = t & 31;
+        const int l = e >> 3, ch = (e >> 2) & 1, n = e & 3;
+        const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        atomicAdd(a.SQ + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
+    }
+    if (!STATIC && threadIdx.x < 64) {
+        // binless: Q_r += Q' + 2 cI S' + cI^2 N  with N = sum of the item's spatial weights
+        const int l = threadIdx.x >> 4, mm = (threadIdx.x >> 2) & 3, n = threadIdx.x & 3;
+        const double Qp = CB[mm * 32 + (2 * l) * 4 + n], Sp = CB[mm * 32 + (2 * l + 1) * 4 + n];
+        const ItemW &iw = a.itemw[blockIdx.x];
+        const double N = iw.sx[l] * iw.sy[mm] * iw.sz[n];
+        if (N > 0.0) {
+            const double c = cI;
+            const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+            atomicAdd(a.Qt + r, Qp + 2.0 * c * Sp + c * c * N);
+        }
     }
 }
 
 // ---------------------------------------------------------------- combine
 // One warp per region r (Eq 9-12 P:111-127 in moment form):
-//   N_ra = Nlo[r][a] + Nup[r][a-1];  S_ra, Q_ra unshifted from the pass-1 moments;
-//   T_r = Q_r - S_r^2/N_r;  V_r = Q_r - sum_{a:N_ra>0} S_ra^2/N_ra;
+//   N_ra = Nlo[r][a] + Nup[r][a-1];  S_ra unshifted from the binned pass-1 moments;
+//   mu_ra = S_ra/N_ra, mu_r = S_r/N_r;  T_r = Q_r - S_r^2/N_r (binless Q_r);
+//   V_r = T_r - sum_{a:N_ra>0} N_ra (mu_ra - mu_r)^2  (= Q_r - sum_a S_ra^2/N_ra);
 //   retained iff N_r/Z > eps_mass and sigma_r^2 = T_r/N_r > eps_sigma (reading c12);
 //   dterm[r] = N_r V_r / T_r (so D = sum dterm / Z), and the coefficients
 //   alpha_r = CR_r/sigma_r^2, beta_r = (1-CR_r) mu_r/sigma_r^2, gamma_ra = mu_r(a)/sigma_r^2.
 struct CombineArgs {
-    const double *SQ;           // [R][B][4]
+    const double *SQ;           // [R][B][2]
+    const double *Qt;           // [R]
     const double *Nlo, *Nup;    // [R][B]
     const float *shiftc;        // [B]
     int R, B;
     double Z, eps_mass, eps_sigma;
     double *dterm;              // [R]
     double *reg;                // [R][6] {p(r), sigma2, mu, 1-CR, retained, Z}
-    double *S_out, *Q_out;      // [R][B] unshifted (debug / parity), may be null
+    double *S_out;              // [R][B] unshifted (debug / parity), may be null
     float *alpha, *beta, *gamma;
 };
 
@@ -431,37 +570,51 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
+__device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, double &N, double &S) {
+    const int B = a.B;
+    const double *q = a.SQ + ((long long)r * B + b) * 2;
+    const double nlo = a.Nlo[(long long)r * B + b];
+    N = nlo;
+    S = q[0] + (double)a.shiftc[b] * nlo;
+    if (b > 0) {
+        const double nup = a.Nup[(long long)r * B + b - 1];
+        N += nup;
+        S += (q - 2)[1] + (double)a.shiftc[b - 1] * nup;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= a.R) return;
     const int B = a.B;
-    double Nr = 0, Sr = 0, Qr = 0, s2n = 0;
+    double Nr = 0, Sr = 0;
     for (int b = lane; b < B; b += 32) {
-        const double *q = a.SQ + ((long long)r * B + b) * 4;
-        const double c = a.shiftc[b];
-        const double nlo = a.Nlo[(long long)r * B + b];
-        double N = nlo, S = q[0] + c * nlo, Q = q[2] + 2.0 * c * q[0] + c * c * nlo;
-        if (b > 0) {
-            const double *qp = q - 4;
-            const double cp = a.shiftc[b - 1];
-            const double nup = a.Nup[(long long)r * B + b - 1];
-            N += nup;
-            S += qp[1] + cp * nup;
-            Q += qp[3] + 2.0 * cp * qp[1] + cp * cp * nup;
-        }
-        if (a.S_out) { a.S_out[(long long)r * B + b] = S; a.Q_out[(long long)r * B + b] = Q; }
-        Nr += N; Sr += S; Qr += Q;
-        if (N > 0.0) s2n += S * S / N;
+        double N, S;
+        bin_NS(a, r, b, N, S);
+        if (a.S_out) a.S_out[(long long)r * B + b] = S;
+        Nr += N;
+        Sr += S;
     }
-    Nr = warp_sum_d(Nr); Sr = warp_sum_d(Sr); Qr = warp_sum_d(Qr); s2n = warp_sum_d(s2n);
+    Nr = warp_sum_d(Nr);
+    Sr = warp_sum_d(Sr);
+    const double mu = Nr > 0 ? Sr / Nr : 0.0;
+    double btw = 0;
+    for (int b = lane; b < B; b += 32) {
+        double N, S;
+        bin_NS(a, r, b, N, S);
+        if (N > 0.0) {
+            const double d = S / N - mu;
+            btw += N * d * d;
+        }
+    }
+    btw = warp_sum_d(btw);
     const double pr = Nr / a.Z;
-    double sig2 = 0, mu = 0, omcr = 0;
+    double sig2 = 0, omcr = 0;
     bool ret = false;
     if (pr > a.eps_mass) {
-        const double Tr = Qr - Sr * Sr / Nr, Vr = Qr - s2n;
+        const double Tr = a.Qt[r] - Sr * Sr / Nr, Vr = Tr - btw;
         sig2 = Tr / Nr;
-        mu = Sr / Nr;
         if (sig2 > a.eps_sigma) { ret = true; omcr = Vr / Tr; }
     }
     if (lane == 0) {
@@ -472,16 +625,8 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
         rg[0] = pr; rg[1] = sig2; rg[2] = mu; rg[3] = omcr; rg[4] = ret ? 1.0 : 0.0; rg[5] = a.Z;
     }
     for (int b = lane; b < B; b += 32) {
-        const double *q = a.SQ + ((long long)r * B + b) * 4;
-        const double c = a.shiftc[b];
-        const double nlo = a.Nlo[(long long)r * B + b];
-        double N = nlo, S = q[0] + c * nlo;
-        if (b > 0) {
-            const double cp = a.shiftc[b - 1];
-            const double nup = a.Nup[(long long)r * B + b - 1];
-            N += nup;
-            S += (q - 4)[1] + cp * nup;
-        }
+        double N, S;
+        bin_NS(a, r, b, N, S);
         a.gamma[(long long)r * B + b] = (ret && N > 0.0) ? (float)((S / N) / sig2) : 0.f;
     }
 }
@@ -503,16 +648,11 @@ __global__ void __launch_bounds__(1024) k_reduce_D(const double *dterm, const do
     if (threadIdx.x == 0) { out[0] = sd[0] / Z; out[1] = sc[0]; }
 }
 
-
+// ----------------------------------------------- pass 2: exact-sample path (fp64)
 __device__ __forceinline__ double d4(const double4 &v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
 }
 
-// Exact-sample path of pass 2 (fp64), taken by the rare lanes whose fp32 sample
-// position lies within 1e-4 voxel of an integer (a trilinear cell or clamp boundary)
-// or whose warped intensity lies within 1e-4 of an integer (the Parzen kink of c4):
-// there the per-voxel derivative is discontinuous and the side must be decided as
-// the fp64 definition decides it.  Outputs m's gradient, g1' and c2.
 // fp64 sample coordinate along one axis, exactly as the definition (c2, c3)
 __device__ __forceinline__ void axis64(int i, double u, int N, long long &c0, double &t, bool &cl) {
     double yv = (double)i + u;
@@ -528,6 +668,10 @@ __device__ __forceinline__ void axis64(int i, double u, int N, long long &c0, do
 
 struct ExactGeo { int nx, ny, nz, L, Gx, Gy, GzExt, ndim; };
 
+// Taken by the rare lanes whose fp32 sample position lies within 1e-4 voxel of an
+// integer (a trilinear cell or clamp boundary) or whose warped intensity lies within
+// 1e-4 of an integer (the Parzen kink of c4): there the per-voxel derivative is
+// discontinuous and the side must be decided as the fp64 definition decides it.
 __device__ __noinline__ void exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
                                           int bx, int by, int bz, double4 wx, double4 wy, double4 wz, int x,
                                           int y, int z, float &gxo, float &gyo, float &gzo, float &g1po,
@@ -597,11 +741,15 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 //   (4 active control layers), x-contracted across lanes when a layer retires (segmented
 //   shuffle), y-contracted into a CTA node window in shared memory, flushed with fp64
 //   atomics at the end of the item.
-template <int KB>
-__global__ void __launch_bounds__(NT, 1) k_pass2(PassArgs a) {
+// The warp's row is fixed during its z-march: gamma, alpha, beta are contracted over the
+// y-taps once per row (GY[bin][xtap] = float4 over the z-taps); per line the bins the
+// line touches are contracted over z cooperatively (GZ[bin] = float4 over the x-taps),
+// so a voxel reads two float4.
+template <int XV>
+__global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
-    const int B = g.B;
+    const int B = g.B, W = a.W;
     const Item it = a.items[blockIdx.x];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
@@ -612,94 +760,139 @@ __global__ void __launch_bounds__(NT, 1) k_pass2(PassArgs a) {
     const int zn0 = a.t.cb[2][it.z0];
     const int nzn = a.t.cb[2][it.z0 + it.zlen - 1] + 4 - zn0;
 
-    float *gl = reinterpret_cast<float *>(smem);          // [64][B] gamma of the 64 regions
-    float *gz_t = gl + 64 * B;                            // [16][B] z-contracted gamma (m,l) x bin
-    float4 *GY = reinterpret_cast<float4 *>(gz_t + 16 * B);  // [NW][B] per-line y,z-contracted gamma
-    float *al = reinterpret_cast<float *>(GY + NW * B);   // [64]
-    float *bl = al + 64;                                  // [64]
-    float *abz = bl + 64;                                 // [32]: alpha_z[m][l], beta_z[m][l]
-    float *RB = abz + 32;                                 // [NW][3][32] retiring-layer row buffer
-    float *NP = RB + NW * 96;                             // [nzn][3][nyn][nxn] node window
+    float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][B][GYS]
+    float4 *GZ = GY + W * B * GYS;                                // [W][B]
+    float *gl = reinterpret_cast<float *>(GZ + W * B);            // [64][B] gamma of the 64 regions
+    int *gbins = reinterpret_cast<int *>(gl + 64 * B);            // [B+1] bins a0 and a0+1 of the item, count
+    float *al = reinterpret_cast<float *>(gbins + B + 1);         // [64]
+    float *bl = al + 64;                                          // [64]
+    float *RB = bl + 64;                                          // [W][3][64] retiring-layer row buffer
+    float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
 
     const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
-    for (int i = threadIdx.x; i < 64 * B; i += NT) {
+    // bin list of the item: every a0 slot and a0+1 (sorted, no duplicates)
+    int nb2 = 0;
+    if (threadIdx.x == 0) {
+        int last = -1;
+        for (int s2 = 0; s2 < it.nslots; ++s2) {
+            const int b0 = a.slotbins[it.slot_off + s2];
+            if (b0 != last) gbins[nb2++] = b0;
+            gbins[nb2++] = b0 + 1;
+            last = b0 + 1;
+        }
+        gbins[B] = nb2;
+    }
+    __syncthreads();
+    nb2 = gbins[B];
+    for (int i = threadIdx.x; i < 64 * B; i += blockDim.x) {
         const int reg = i / B, bin = i - reg * B;
         const int l = reg & 3, mm = (reg >> 2) & 3, n = reg >> 4;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
         gl[i] = __ldg(a.gamma + r * B + bin);
     }
-    for (int i = threadIdx.x; i < 64; i += NT) {
+    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
         const int l = i & 3, mm = (i >> 2) & 3, n = i >> 4;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
         al[i] = __ldg(a.alpha + r);
         bl[i] = __ldg(a.beta + r);
     }
     const int npsz = nzn * 3 * nyn * nxn;
-    for (int i = threadIdx.x; i < npsz; i += NT) NP[i] = 0.f;
-    for (int i = threadIdx.x; i < NW * 96; i += NT) RB[i] = 0.f;
+    for (int i = threadIdx.x; i < npsz; i += blockDim.x) NP[i] = 0.f;
+    for (int i = threadIdx.x; i < W * 192; i += blockDim.x) RB[i] = 0.f;
 
-    const int x = it.x0 + lane;
-    const bool lane_ok = lane < it.xlen;
-    const int xc = min(x, g.nx - 1);
-    const int cbx = a.t.cb[0][xc];
-    const float4 cwx = a.t.cw[0][xc];
-    const float4 swx = a.t.sw[0][xc];
-    const int relx = cbx - xn0;
-    // segment heads of equal control x-base (for the adjoint x-contraction)
-    const int cbx_prev = __shfl_up_sync(FULL, cbx, 1);
-    const bool head = lane == 0 || cbx_prev != cbx;
-    float *rbw = RB + warp * 96;
+    bool lok[XV], head[XV];
+    int xv[XV], relx[XV], cbx[XV];
+    float4 cwx[XV], swx[XV];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        lok[v] = lane + 32 * v < it.xlen;
+        xv[v] = lok[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+        cbx[v] = a.t.cb[0][xv[v]];
+        relx[v] = cbx[v] - xn0;
+        cwx[v] = a.t.cw[0][xv[v]];
+        swx[v] = a.t.sw[0][xv[v]];
+        const int prev = __shfl_up_sync(FULL, cbx[v], 1);
+        head[v] = lane == 0 || prev != cbx[v];
+    }
+    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = g.nz - 2;
+    const int dzo = g.nz > 1 ? nxy : 0;
+    const bool is2d = g.nz == 1;
+    const int nwb = (B + 31) >> 5;
+    const float *__restrict__ Mv = a.M;
+    float *rbw = RB + warp * 192;
+    float4 *GYw = GY + warp * B * GYS;
+    float4 *GZw = GZ + warp * B;
     __syncthreads();
 
-    for (int ys = it.y0; ys < it.y0 + it.ylen; ys += NW) {
-        const int y = ys + warp;
-        const bool row_ok = y < it.y0 + it.ylen;
-        const int yc = min(y, g.ny - 1);
-        const int cby = a.t.cb[1][yc];
-        const float4 cwy = a.t.cw[1][yc];
-        const float4 swy = a.t.sw[1][yc];
-        const bool ok = lane_ok && row_ok;
+    for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
+        const int cby = a.t.cb[1][y];
+        const float4 cwy = a.t.cw[1][y];
+        const float4 swy = a.t.sw[1][y];
+        const float *__restrict__ Frow = a.F + y * nx;
+
+        // gamma of the item's bins (a0 and a0+1 of every slot) contracted over the y-taps:
+        // GYw[bin][l] = float4_n( sum_m wy_m gamma[(n, m, l)][bin] )
+        for (int i = lane; i < it.nslots * 32; i += 32) {
+            const int s = i >> 5, e = i & 31;                     // e = (bin offset, l, n)
+            const int bin = a.slotbins[it.slot_off + s] + (e >> 4);
+            const int l = (e >> 2) & 3, n = e & 3;
+            const float *src = gl + (n * 16 + l) * B + bin;      // region (n, m, l): index n*16 + m*4 + l
+            const float val = swy.x * src[0] + swy.y * src[4 * B] + swy.z * src[8 * B] + swy.w * src[12 * B];
+            reinterpret_cast<float *>(GYw + bin * GYS + l)[n] = val;
+        }
+        // alpha (lanes 0-15) / beta (lanes 16-31) contracted over y: lane = 16*ab + 4*l + n
+        float abY;
+        {
+            const int l = (lane >> 2) & 3, n = lane & 3;
+            const float *src = (lane < 16 ? al : bl) + n * 16 + l;
+            abY = swy.x * src[0] + swy.y * src[4] + swy.z * src[8] + swy.w * src[12];
+        }
+        __syncwarp();
 
         int gzl = zn0;
-        float U[4][3], Ad[4][3];
+        float U[4][XV][3], Ad[4][XV][3];
 #pragma unroll
         for (int n = 0; n < 4; ++n) {
-            ffd_layer(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
-            Ad[n][0] = Ad[n][1] = Ad[n][2] = 0.f;
+            ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+#pragma unroll
+            for (int v = 0; v < XV; ++v) Ad[n][v][0] = Ad[n][v][1] = Ad[n][v][2] = 0.f;
         }
 
-        // retire control layer gzr with this lane's accumulated adjoint R[3]
-        auto retire = [&](int gzr, const float R[3]) {
-            float val[4][3];
+        // retire control layer gzr with this lane's accumulated adjoints R[v][3]
+        auto retire = [&](int gzr, const float (&R)[XV][3]) {
 #pragma unroll
-            for (int l = 0; l < 4; ++l)
-#pragma unroll
-                for (int c = 0; c < 3; ++c) val[l][c] = f4(cwx, l) * R[c];
-            for (int s = 0, off = 1; s < a.segsteps; ++s, off <<= 1) {
-                const int nb = __shfl_down_sync(FULL, cbx, off);
-                const bool same = (lane + off < 32) && nb == cbx;
+            for (int v = 0; v < XV; ++v) {
+                float val[4][3];
 #pragma unroll
                 for (int l = 0; l < 4; ++l)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) {
-                        const float t = __shfl_down_sync(FULL, val[l][c], off);
-                        if (same) val[l][c] += t;
-                    }
-            }
+                    for (int c = 0; c < 3; ++c) val[l][c] = f4(cwx[v], l) * R[v][c];
+                for (int st = 0, off = 1; st < a.segsteps; ++st, off <<= 1) {
+                    const int nb = __shfl_down_sync(FULL, cbx[v], off);
+                    const bool same = (lane + off < 32) && nb == cbx[v];
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                if (head)
+                    for (int l = 0; l < 4; ++l)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) rbw[c * 32 + relx + l] += val[l][c];
-                __syncwarp();
+                        for (int c = 0; c < 3; ++c) {
+                            const float t = __shfl_down_sync(FULL, val[l][c], off);
+                            if (same) val[l][c] += t;
+                        }
+                }
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    if (head[v])
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) rbw[c * 64 + relx[v] + l] += val[l][c];
+                    __syncwarp();
+                }
             }
             // y-contraction of the row buffer into the CTA node window
             const int lz = gzr - zn0;
             for (int i = lane; i < 3 * nxn; i += 32) {
                 const int c = i / nxn, gxl = i - c * nxn;
-                const float rv = rbw[c * 32 + gxl];
-                rbw[c * 32 + gxl] = 0.f;
-                if (rv != 0.f && row_ok) {
+                const float rv = rbw[c * 64 + gxl];
+                rbw[c * 64 + gxl] = 0.f;
+                if (rv != 0.f) {
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
                         const float w = f4(cwy, mm);
@@ -717,134 +910,99 @@ __global__ void __launch_bounds__(NT, 1) k_pass2(PassArgs a) {
 #pragma unroll
                 for (int n = 0; n < 3; ++n)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) { U[n][c] = U[n + 1][c]; Ad[n][c] = Ad[n + 1][c]; }
-                Ad[3][0] = Ad[3][1] = Ad[3][2] = 0.f;
+                    for (int v = 0; v < XV; ++v)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) { U[n][v][c] = U[n + 1][v][c]; Ad[n][v][c] = Ad[n + 1][v][c]; }
+#pragma unroll
+                for (int v = 0; v < XV; ++v) Ad[3][v][0] = Ad[3][v][1] = Ad[3][v][2] = 0.f;
                 ++gzl;
-                ffd_layer(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
+                ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
             }
-            // ---- per-slice region tables: gamma_z[(m,l)][bin], alpha_z, beta_z
-            const float4 swz = a.t.sw[2][z];
-            __syncthreads();
-            for (int i = threadIdx.x; i < 16 * B; i += NT) {
-                const int ml = i / B, bin = i - ml * B;
-                float s = swz.x * gl[ml * B + bin];
-                s = fmaf(swz.y, gl[(16 + ml) * B + bin], s);
-                s = fmaf(swz.z, gl[(32 + ml) * B + bin], s);
-                s = fmaf(swz.w, gl[(48 + ml) * B + bin], s);
-                gz_t[i] = s;
-            }
-            if (threadIdx.x < 32) {
-                const float *src = threadIdx.x < 16 ? al : bl;
-                const int ml = threadIdx.x & 15;
-                abz[threadIdx.x] = swz.x * src[ml] + swz.y * src[16 + ml] + swz.z * src[32 + ml] + swz.w * src[48 + ml];
-            }
-            __syncthreads();
-
             const float4 cwz = a.t.cw[2][z];
-            float ux = 0.f, uy = 0.f, uz = 0.f;
-#pragma unroll
-            for (int n = 0; n < 4; ++n) {
-                const float w = f4(cwz, n);
-                ux = fmaf(w, U[n][0], ux);
-                uy = fmaf(w, U[n][1], uy);
-                uz = fmaf(w, U[n][2], uz);
-            }
-            int a0 = 0;
-            float hlo = 0.f, hhi = 0.f, m = 0.f, dgx = 0.f, dgy = 0.f, dgz = 0.f;
-            if (ok) {
-                const long long idx = (long long)z * g.nxy + (long long)y * g.nx + x;
-                const float Fv = __ldg(a.F + idx);
-                a0 = min((int)Fv, g.L - 1);
-                parzen_pair(Fv - (float)a0, hlo, hhi);
-                m = sample_m<true>(a.M, g, x, y, z, ux, uy, uz, dgx, dgy, dgz);
-            }
-            // ---- the line's gamma, contracted over (m, n) for the bins it touches
-            unsigned bits[KB];
-            int tot = 0;
-#pragma unroll
-            for (int k = 0; k < KB; ++k) {
-                unsigned mine = 0u;
-                if (ok) {
-                    if ((a0 >> 5) == k) mine |= 1u << (a0 & 31);
-                    if (((a0 + 1) >> 5) == k) mine |= 1u << ((a0 + 1) & 31);
-                }
-                bits[k] = __reduce_or_sync(FULL, mine);
-                tot += __popc(bits[k]);
-            }
-            for (int o = lane; o < 4 * tot; o += 32) {
-                int bi = o >> 2;
-                const int l = o & 3;
-                int bin = 0;
-#pragma unroll
-                for (int k = 0; k < KB; ++k) {
-                    const int c = __popc(bits[k]);
-                    if (bi >= 0 && bi < c) {
-                        unsigned w = bits[k];
-                        int pos = 0, r = bi;
-#pragma unroll
-                        for (int s = 16; s > 0; s >>= 1) {
-                            const unsigned lo = w & ((1u << s) - 1u);
-                            const int cnt = __popc(lo);
-                            if (r >= cnt) { r -= cnt; w >>= s; pos += s; } else { w = lo; }
-                        }
-                        bin = 32 * k + pos;
-                    }
-                    bi -= c;
-                }
-                float s = swy.x * gz_t[(0 + l) * B + bin];
-                s = fmaf(swy.y, gz_t[(4 + l) * B + bin], s);
-                s = fmaf(swy.z, gz_t[(8 + l) * B + bin], s);
-                s = fmaf(swy.w, gz_t[(12 + l) * B + bin], s);
-                reinterpret_cast<float *>(GY + warp * B + bin)[l] = s;
-            }
-            // alpha/beta contracted over (m, n) for this line, x-taps 0..3
-            float abv = 0.f;
-            if (lane < 8) {
-                const int l = lane & 3, off = (lane >> 2) * 16;
-                abv = swy.x * abz[off + l] + swy.y * abz[off + 4 + l] + swy.z * abz[off + 8 + l] + swy.w * abz[off + 12 + l];
-            }
-            __syncwarp();
-            float At = 0.f, Bt = 0.f;
+            const float4 wz = a.t.sw[2][z];
+            const float *__restrict__ Fz = Frow + z * nxy;
+            // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
+            float t = f4(wz, lane & 3) * abY;
+            t += __shfl_xor_sync(FULL, t, 1);
+            t += __shfl_xor_sync(FULL, t, 2);
+            float ay[4], by4[4];
 #pragma unroll
             for (int l = 0; l < 4; ++l) {
-                At = fmaf(f4(swx, l), __shfl_sync(FULL, abv, l), At);
-                Bt = fmaf(f4(swx, l), __shfl_sync(FULL, abv, 4 + l), Bt);
+                ay[l] = __shfl_sync(FULL, t, 4 * l);
+                by4[l] = __shfl_sync(FULL, t, 16 + 4 * l);
             }
-            if (ok) {
-                const float4 G0 = GY[warp * B + a0], G1 = GY[warp * B + a0 + 1];
-                float Gt = 0.f;
+            // gamma of the item's bins contracted over z for this line: GZw[bin] = float4_l
+            for (int i = lane; i < 4 * nb2; i += 32) {
+                const int bin = gbins[i >> 2], l = i & 3;
+                reinterpret_cast<float *>(GZw + bin)[l] = dot4(wz, GYw[bin * GYS + l]);
+            }
+            int a0[XV];
+            float hlo[XV], hhi[XV];
 #pragma unroll
-                for (int l = 0; l < 4; ++l) Gt = fmaf(f4(swx, l), fmaf(hlo, f4(G0, l), hhi * f4(G1, l)), Gt);
+            for (int v = 0; v < XV; ++v) {
+                const float Fv = __ldg(Fz + xv[v]);
+                a0[v] = min((int)Fv, g.L - 1);
+                parzen_pair(Fv - (float)a0[v], hlo[v], hhi[v]);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
+                const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
+                const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
+                float tx, ty, tz;
+                bool clx, cly, clz, nrx, nry, nrz;
+                const int ccx = axis_fast_cl(xv[v], ux, nxm2, fmaf(1e-6f, fabsf(ux), 2e-5f), tx, clx, nrx);
+                const int ccy = axis_fast_cl(y, uy, nym2, fmaf(1e-6f, fabsf(uy), 2e-5f), ty, cly, nry);
+                const int ccz = axis_fast_cl(z, uz, nzm2, fmaf(1e-6f, fabsf(uz), 2e-5f), tz, clz, nrz);
+                const float *__restrict__ b = Mv + (ccz * nxy + ccy * nx + ccx);
+                const float *__restrict__ b3 = b + dzo;
+                const float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + nx), c110 = __ldg(b + nx + 1);
+                const float c001 = __ldg(b3), c101 = __ldg(b3 + 1), c011 = __ldg(b3 + nx), c111 = __ldg(b3 + nx + 1);
+                const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
+                const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
+                const float f0 = lerpf(e00, e10, ty), f1 = lerpf(e01, e11, ty);
+                const float m = lerpf(f0, f1, tz);
+                float dgx = lerpf(lerpf(c100 - c000, c110 - c010, ty), lerpf(c101 - c001, c111 - c011, ty), tz);
+                float dgy = lerpf(lerpf(c010 - c000, c110 - c100, tx), lerpf(c011 - c001, c111 - c101, tx), tz);
+                float dgz = f1 - f0;
+                dgx = clx ? 0.f : dgx;
+                dgy = cly ? 0.f : dgy;
+                dgz = (clz || is2d) ? 0.f : dgz;
+                const float4 G0 = GZw[a0[v]], G1 = GZw[a0[v] + 1];
+                const float4 sw = swx[v];
+                const float At = fmaf(sw.w, ay[3], fmaf(sw.z, ay[2], fmaf(sw.y, ay[1], sw.x * ay[0])));
+                const float Bt = fmaf(sw.w, by4[3], fmaf(sw.z, by4[2], fmaf(sw.y, by4[1], sw.x * by4[0])));
+                const float Gt = fmaf(hlo[v], dot4(sw, G0), hhi[v] * dot4(sw, G1));
                 const int n = min(max((int)floorf(m), 0), g.L - 1);
                 const float fm = m - (float)n;
                 float g1p, c2;
                 if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
                 else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
                 // discontinuities of the per-voxel derivative: decide them in fp64
-                const float tolu = 1e-4f;
-                if (near_integer(ux, tolu + 1e-6f * fabsf(ux)) || near_integer(uy, tolu + 1e-6f * fabsf(uy)) ||
-                    near_integer(uz, tolu + 1e-6f * fabsf(uz)) || near_integer(m, 1e-4f))
-                    exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M, cbx,
-                                 cby, a.t.cb[2][z], a.t.cw64[0][x], a.t.cw64[1][y], a.t.cw64[2][z], x, y, z, dgx,
-                                 dgy, dgz, g1p, c2);
-                const float d = g1p * a.invZ * (fmaf(c2, At, 2.0f * (Bt - Gt)));
+                if (nrx || nry || (nrz && !is2d) || fm < 5e-5f || fm > 1.0f - 5e-5f)
+                    exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
+                                 cbx[v], cby, bz, a.t.cw64[0][xv[v]], a.t.cw64[1][y], a.t.cw64[2][z], xv[v], y, z,
+                                 dgx, dgy, dgz, g1p, c2);
+                const float d = lok[v] ? g1p * a.invZ * fmaf(c2, At, 2.0f * (Bt - Gt)) : 0.f;
                 const float d0 = d * dgx, d1 = d * dgy, d2 = d * dgz;
 #pragma unroll
                 for (int n2 = 0; n2 < 4; ++n2) {
                     const float w = f4(cwz, n2);
-                    Ad[n2][0] = fmaf(w, d0, Ad[n2][0]);
-                    Ad[n2][1] = fmaf(w, d1, Ad[n2][1]);
-                    Ad[n2][2] = fmaf(w, d2, Ad[n2][2]);
+                    Ad[n2][v][0] = fmaf(w, d0, Ad[n2][v][0]);
+                    Ad[n2][v][1] = fmaf(w, d1, Ad[n2][v][1]);
+                    Ad[n2][v][2] = fmaf(w, d2, Ad[n2][v][2]);
                 }
             }
             __syncwarp();
         }
 #pragma unroll
         for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
+        __syncwarp();
     }
     __syncthreads();
     // ---- flush the node window: grad[c][gz][gy][gx] (external layout)
-    for (int i = threadIdx.x; i < npsz; i += NT) {
+    for (int i = threadIdx.x; i < npsz; i += blockDim.x) {
         const float v = NP[i];
         if (v == 0.f) continue;
         const int gxl = i % nxn;
@@ -875,7 +1033,7 @@ __global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict_
 }
 
 // min / max of a volume (exact; order independent)
-__global__ void k_minmax(const float *__restrict__ v, long long n, float *out /*[2], init +inf,-inf*/) {
+__global__ void k_minmax(const float *__restrict__ v, long long n, float *out /*[2] encoded keys*/) {
     float lo = INFINITY, hi = -INFINITY;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const float x = v[i];
@@ -888,9 +1046,9 @@ __global__ void k_minmax(const float *__restrict__ v, long long n, float *out /*
         hi = fmaxf(hi, __shfl_xor_sync(FULL, hi, o));
     }
     if ((threadIdx.x & 31) == 0) {
-        // float ordering == int ordering for non-negative; use CAS-free atomics on encoded keys
-        int ilo = __float_as_int(lo), ihi = __float_as_int(hi);
-        int klo = ilo >= 0 ? ilo : ilo ^ 0x7fffffff, khi = ihi >= 0 ? ihi : ihi ^ 0x7fffffff;
+        // monotone int keys of the floats, so integer atomics order them correctly
+        const int ilo = __float_as_int(lo), ihi = __float_as_int(hi);
+        const int klo = ilo >= 0 ? ilo : ilo ^ 0x7fffffff, khi = ihi >= 0 ? ihi : ihi ^ 0x7fffffff;
         atomicMin(reinterpret_cast<int *>(out), klo);
         atomicMax(reinterpret_cast<int *>(out) + 1, khi);
     }
@@ -914,6 +1072,38 @@ __global__ void k_a0_map(const float *__restrict__ F, short *__restrict__ out, l
         out[i] = (short)min((int)F[i], L - 1);
 }
 
+// per item: the set of fixed bins a0 present (bitmask, B <= 128) and the sum of the
+// normalised moving image over the box (for the item's binless shift)
+__global__ void k_item_scan(const float *__restrict__ F, const float *__restrict__ M, const Item *items, Geo g,
+                            unsigned *masks /*[items][4]*/, double *msum /*[items]*/) {
+    __shared__ unsigned sm[4];
+    __shared__ double ss[32];
+    const Item it = items[blockIdx.x];
+    if (threadIdx.x < 4) sm[threadIdx.x] = 0u;
+    __syncthreads();
+    double s = 0;
+    const long long n = (long long)it.xlen * it.ylen * it.zlen;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const int x = it.x0 + (int)(i % it.xlen);
+        const long long t = i / it.xlen;
+        const int y = it.y0 + (int)(t % it.ylen), z = it.z0 + (int)(t / it.ylen);
+        const long long idx = (long long)z * g.nxy + (long long)y * g.nx + x;
+        const int a0 = min((int)F[idx], g.L - 1);
+        atomicOr(&sm[a0 >> 5], 1u << (a0 & 31));
+        s += M[idx];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+    if ((threadIdx.x & 31) == 0) ss[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x < 4) masks[blockIdx.x * 4 + threadIdx.x] = sm[threadIdx.x];
+    if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ss[w];
+        msum[blockIdx.x] = t;
+    }
+}
+
 // per-bin moment shift c_a = global conditional mean of the moving image given fixed bin a
 // (from an identity-transform pass 1 with shift = bin index); bins without mass keep c_a = a
 __global__ void k_shift_update(const double *SQ, const double *Nlo, const double *Nup, const float *shift_in,
@@ -925,11 +1115,11 @@ __global__ void k_shift_update(const double *SQ, const double *Nlo, const double
     for (int r = 0; r < R; ++r) {
         const double nlo = Nlo[(long long)r * B + b];
         N += nlo;
-        S += SQ[((long long)r * B + b) * 4 + 0] + c * nlo;
+        S += SQ[((long long)r * B + b) * 2 + 0] + c * nlo;
         if (b > 0) {
             const double nup = Nup[(long long)r * B + b - 1];
             N += nup;
-            S += SQ[((long long)r * B + b - 1) * 4 + 1] + cp * nup;
+            S += SQ[((long long)r * B + b - 1) * 2 + 1] + cp * nup;
         }
     }
     shift_out[b] = N > 0.0 ? (float)(S / N) : (float)b;
@@ -938,8 +1128,8 @@ __global__ void k_shift_update(const double *SQ, const double *Nlo, const double
 // split the static-pass table into Nlo / Nup
 __global__ void k_split_counts(const double *SQ, double *Nlo, double *Nup, long long RB) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < RB; i += (long long)gridDim.x * blockDim.x) {
-        Nlo[i] = SQ[i * 4 + 0];
-        Nup[i] = SQ[i * 4 + 1];
+        Nlo[i] = SQ[i * 2 + 0];
+        Nup[i] = SQ[i * 2 + 1];
     }
 }
 

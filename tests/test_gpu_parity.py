@@ -95,7 +95,9 @@ def test_single_global_bin_is_textbook_cr():
     D, _ = g.eval(np.zeros(g.params_shape))
     a, b = A.ravel().astype(np.float64), B.ravel().astype(np.float64)
     within = sum((a == k).mean() * b[a == k].var() for k in np.unique(a))
-    assert rel(D, within / b.var()) <= 1e-6
+    # integer-valued images make the fixed-point rounding of the line tables coherent
+    # (every voxel of a (bin, value) pair rounds alike): held to the D gate, not tighter
+    assert rel(D, within / b.var()) <= D_TOL
     g.close()
 
 

@@ -1,0 +1,154 @@
+"""CPU-only checks of the product library and of the multi-rank host logic.
+
+* libsrwcr.so builds for sm_100a, loads without a GPU, and exports every function
+  declared in include/srwcr.h (no compute call is made here).
+* srwcr_plan_slab (host-only) partitions the slices.
+* The z-slab decomposition used by nranks > 1 -- rank-partial bin statistics summed
+  across ranks, then a rank-partial gradient summed across ranks -- reproduces the
+  single-process result, run as 2 gloo processes with the oracle standing in for the
+  kernels (the kernels themselves are covered on one GPU by
+  tests/test_gpu_parity.py::test_slab_decomposition_on_one_gpu).
+"""
+import ctypes
+import os
+import re
+import socket
+
+import numpy as np
+import pytest
+
+import paper_1804_05061_b200 as S
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    S.build()
+    return S.lib()
+
+
+def _declared_functions():
+    src = open(os.path.join(ROOT, "include", "srwcr.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(srwcr_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_header_symbols_are_exported(lib):
+    names = _declared_functions()
+    assert len(names) >= 15
+    so = ctypes.CDLL(S._LIB)
+    for n in names:
+        assert hasattr(so, n), f"{n} declared in include/srwcr.h but not exported"
+    # the binding lists the same set
+    assert set(S.EXPORTS) == set(names)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", S.build()], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_default_options_and_argument_errors(lib):
+    opt = S._Options()
+    assert lib.srwcr_default_options(ctypes.byref(opt)) == S.OK
+    assert opt.struct_size == ctypes.sizeof(S._Options)
+    assert (opt.nranks, opt.rank, opt.moment_shift, opt.use_graph) == (1, 0, 1, 1)
+    assert opt.eps_mass == 1e-12 and opt.eps_sigma == 1e-6
+    ctx = ctypes.c_void_p()
+    dims = (ctypes.c_int64 * 3)(8, 8, 8)
+    sp = (ctypes.c_double * 3)(1, 1, 1)
+    sb = (ctypes.c_int32 * 3)(1, 1, 1)
+    cs = (ctypes.c_double * 3)(4, 4, 4)
+    # NULL fixed image -> EINVAL with a message naming it (no CUDA call is reached)
+    st = lib.srwcr_create(ctypes.byref(ctx), None, None, dims, sp, 32, sb, cs, None)
+    assert st == S.EINVAL
+    assert b"fixed" in lib.srwcr_last_error(ctx)
+    lib.srwcr_destroy(ctx)
+    buf = np.zeros(512, np.float32)
+    p = buf.ctypes.data_as(ctypes.c_void_p)
+    for bad_bins in (1, 129):
+        ctx = ctypes.c_void_p()
+        assert lib.srwcr_create(ctypes.byref(ctx), p, p, dims, sp, bad_bins, sb, cs, None) == S.EINVAL
+        assert b"intensity_bins" in lib.srwcr_last_error(ctx)
+        lib.srwcr_destroy(ctx)
+    opt.orientation = 1
+    ctx = ctypes.c_void_p()
+    assert lib.srwcr_create(ctypes.byref(ctx), p, p, dims, sp, 32, sb, cs, ctypes.byref(opt)) == S.ENOTSUP
+    lib.srwcr_destroy(ctx)
+
+
+@pytest.mark.parametrize("nz,P", [(320, 8), (128, 3), (7, 4), (1, 1), (5, 5)])
+def test_plan_slab_partition(lib, nz, P):
+    cover = []
+    sizes = []
+    for r in range(P):
+        z0, z1 = S.plan_slab(nz, P, r)
+        assert 0 <= z0 <= z1 <= nz
+        cover.extend(range(z0, z1))
+        sizes.append(z1 - z0)
+    assert cover == list(range(nz))
+    assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(S.SrwcrError):
+        S.plan_slab(nz, P, P)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _rank_main(rank, world, port, q):
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import synth
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config("C3", (40, 36, 30))
+        F, M = synth.make_pair("C3", 1, cfg["dims"])
+        L = cfg["bins"] - 1
+        pb = O.Problem(dims=cfg["dims"], L=L, delta=tuple(c / s for c, s in zip(cfg["control_mm"], cfg["spacing"])),
+                       kcells=cfg["cells"], nthreads=1)
+        Fn, Mn = O.normalize(F, L), O.normalize(M, L)
+        params = synth.make_params(pb.params_shape, "small", 1)
+        # the nccl unique id is broadcast from rank 0 exactly as bench.py does
+        obj = [bytes(range(128)) if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        assert obj[0] == bytes(range(128))
+        z0, z1 = S.plan_slab(cfg["dims"][2], world, rank)
+        N, Sm, Q = (torch.from_numpy(t) for t in O.moments(pb, Fn, Mn, params, z0, z1))
+        for t in (N, Sm, Q):
+            dist.all_reduce(t)
+        D, al, be, ga, reg, Z = O.combine(pb, N.numpy(), Sm.numpy(), Q.numpy())
+        g = torch.from_numpy(O.grad_moments(pb, Fn, Mn, params, al, be, ga, Z, z0, z1))
+        dist.all_reduce(g)
+        if rank == 0:
+            D1, g1 = O.eval_moments(pb, Fn, Mn, params)
+            q.put((D, D1, float(np.linalg.norm(g.numpy() - g1) / np.linalg.norm(g1))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_zslab_decomposition_gloo_two_ranks():
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    D, D1, gerr = q.get(timeout=10)
+    assert abs(D - D1) <= 1e-12 * abs(D1)
+    assert gerr <= 1e-12
