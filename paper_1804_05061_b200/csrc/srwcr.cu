@@ -13,6 +13,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -73,10 +74,12 @@ struct srwcr_ctx {
     float4 *cw[3]{}, *sw[3]{};
     double4 *cw64[3]{};
     Item *items = nullptr, *items_full = nullptr;  // this rank's slab / whole volume
+    Item *items2 = nullptr;                          // pass 2 (its own x-chunking)
+    int nitems2 = 0, XV2 = 1;
     ItemW *itemw = nullptr, *itemw_full = nullptr;
     int *slotbins = nullptr;                         // slot lists of both item lists
     int nitems = 0, nitems_full = 0;
-    int W = 16, W2 = 16, XV = 1, S = 1;               // warps per CTA (pass 1, pass 2), voxels per lane, slots
+    int W = 16, W2 = 16, XV = 1, S = 1, S2 = 2;       // warps per CTA (pass 1, 2), voxels per lane, slots, bin list
     double *SQ = nullptr, *Qt = nullptr;             // stats: [R][B][2] binned, then [R] binless
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     double *S_out = nullptr;
@@ -84,6 +87,7 @@ struct srwcr_ctx {
     double Z = 0;
     size_t smem1 = 0, smem2 = 0;
     int segsteps = 0;
+    int pf1 = 0, pf2 = 1;                            // L2 prefetch per pass (SRWCR_PF1 / SRWCR_PF2)
     ncclComm_t comm = nullptr;
     bool external_exchange = false;
     bool begun = false;
@@ -127,6 +131,12 @@ static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
         ncclResult_t r_ = (call);                                                                       \
         if (r_ != ncclSuccess) return fail(c, SRWCR_ENCCL, "%s failed: %s", #call,                      \
                                            nccl().GetErrorString(r_));                                  \
+    } while (0)
+
+#define TRY(x)                                \
+    do {                                      \
+        srwcr_status s_ = (x);                \
+        if (s_ != SRWCR_OK) return s_;        \
     } while (0)
 
 // ------------------------------------------------------------------ host tables
@@ -209,7 +219,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     }
     a.p64 = c->cur_params;
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
-    a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S;
+    a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
     a.grad = c->grad64;
@@ -224,8 +234,14 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     a.items = full ? c->items_full : c->items;
     a.itemw = full ? c->itemw_full : c->itemw;
     if (n == 0) return SRWCR_OK;
-    if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
-    else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    a.pf = c->pf1;
+    if (c->W > 16) {
+        if (stat) k_pass1<XV, true, 768><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+        else k_pass1<XV, false, 768><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    } else {
+        if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+        else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    }
     CKL();
     return SRWCR_OK;
 }
@@ -237,23 +253,30 @@ template <int XV>
 static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     PassArgs a = pass_args(c);
     a.grad = grad;
-    if (c->nitems == 0) return SRWCR_OK;
+    a.items = c->items2;
+    if (c->nitems2 == 0) return SRWCR_OK;
     a.W = c->W2;
-    k_pass2<XV><<<c->nitems, 32 * c->W2, c->smem2, c->stream>>>(a);
+    a.pf = c->pf2;
+    k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
 static srwcr_status launch_pass2(srwcr_ctx *c, double *grad) {
-    return c->XV == 2 ? launch_pass2_t<2>(c, grad) : launch_pass2_t<1>(c, grad);
+    return c->XV2 == 2 ? launch_pass2_t<2>(c, grad) : launch_pass2_t<1>(c, grad);
 }
 template <int XV>
 static srwcr_status set_smem_t(srwcr_ctx *c) {
     CK(cudaFuncSetAttribute(k_pass1<XV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
     CK(cudaFuncSetAttribute(k_pass1<XV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass1<XV, false, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
+    CK(cudaFuncSetAttribute(k_pass1<XV, true, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
     CK(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
     return SRWCR_OK;
 }
-static srwcr_status set_smem(srwcr_ctx *c) { return c->XV == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c); }
+static srwcr_status set_smem(srwcr_ctx *c) {
+    TRY(c->XV == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c));
+    return c->XV2 == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c);
+}
 
 static size_t stats_count(const srwcr_ctx *c) { return (size_t)c->R * c->g.B * 2 + (size_t)c->R; }
 
@@ -277,11 +300,6 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     return SRWCR_OK;
 }
 
-#define TRY(x)                                \
-    do {                                      \
-        srwcr_status s_ = (x);                \
-        if (s_ != SRWCR_OK) return s_;        \
-    } while (0)
 
 static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *moving, const int64_t dims[3],
                                 const double sp[3], int32_t bins, const int32_t sbins[3], const double csp[3]) {
@@ -322,6 +340,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->nparams = (int64_t)g.ndim * G[0] * G[1] * G[2];
     c->nint = 3LL * g.Gx * g.Gy * g.Gz;
 
+    if (const char *e = getenv("SRWCR_PF1")) c->pf1 = atoi(e);
+    if (const char *e = getenv("SRWCR_PF2")) c->pf2 = atoi(e);
     c->dev = o.device;
     CK(cudaSetDevice(c->dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -413,13 +433,16 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         auto xr = runs(c->h_sb[0], 0, g.nx, 1 << 30);
         for (auto &r : xr) minw = std::min(minw, r.second);
         c->XV = minw >= 48 ? 2 : 1;
+        if (const char *e = getenv("SRWCR_XV")) c->XV = std::min(c->XV, std::max(1, atoi(e)));
+        c->XV2 = 1;
+        if (const char *e = getenv("SRWCR_XV2")) c->XV2 = std::min(c->XV, std::max(1, atoi(e)));
     }
     const int xmax = 32 * c->XV;
     int ymax = 64, zmax = 64;
-    std::vector<Item> items, items_full;
+    std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
-    auto build_items = [&](int zlo, int zhi, std::vector<Item> &out) {
-        auto xr = runs(c->h_sb[0], 0, g.nx, xmax);
+    auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
+        auto xr = runs(c->h_sb[0], 0, g.nx, xm);
         auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
         auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
         for (auto &zz : zr)
@@ -437,7 +460,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     for (;;) {
         items.clear();
         npmax = 0;
-        build_items((int)c->z0, (int)c->z1, items);
+        build_items((int)c->z0, (int)c->z1, items, xmax);
         const bool small = (long long)items.size() < 6LL * nsm;
         const bool big_np = npmax > 12288;
         if ((small || big_np) && (ymax > 16 || zmax > 4)) {
@@ -448,15 +471,18 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         }
         break;
     }
-    build_items(0, g.nz, items_full);
+    build_items(0, g.nz, items_full, xmax);
+    npmax = 0;
+    build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
     if (npmax > 16384) return fail(c, SRWCR_EINVAL, "control lattice too fine for the node window (%zu)", npmax);
     c->nitems = (int)items.size();
     c->nitems_full = (int)items_full.size();
+    c->nitems2 = (int)items2.size();
 
     // per item: fixed bins present (slot lists), binless shift cI, spatial weight sums
     std::vector<int> slotbins;
-    int smax = 1;
-    auto scan_items = [&](std::vector<Item> &its, ItemW **dw) -> srwcr_status {
+    int smax = 1, s2max = 2;
+    auto scan_items = [&](std::vector<Item> &its, ItemW **dw, bool pass2) -> srwcr_status {
         const size_t n = its.size();
         if (n == 0) return SRWCR_OK;
         Item *d_it = nullptr;
@@ -483,7 +509,16 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             for (int b = 0; b < g.B; ++b)
                 if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
             it.nslots = ns;
-            smax = std::max(smax, ns);
+            if (!pass2) smax = std::max(smax, ns);
+            if (pass2) {
+                int nb2 = 0, last = -1;
+                for (int k = it.slot_off; k < it.slot_off + ns; ++k) {
+                    if (slotbins[k] != last) ++nb2;
+                    ++nb2;
+                    last = slotbins[k] + 1;
+                }
+                s2max = std::max(s2max, nb2);
+            }
             it.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
             ItemW &iw = w[i];
             for (int l = 0; l < 4; ++l) iw.sx[l] = iw.sy[l] = iw.sz[l] = 0.0;
@@ -499,14 +534,24 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         CK(cudaMemcpy(*dw, w.data(), sizeof(ItemW) * n, cudaMemcpyHostToDevice));
         return SRWCR_OK;
     };
-    TRY(scan_items(items, &c->itemw));
-    TRY(scan_items(items_full, &c->itemw_full));
+    TRY(scan_items(items, &c->itemw, false));
+    TRY(scan_items(items_full, &c->itemw_full, false));
+    {
+        ItemW *tmpw = nullptr;
+        TRY(scan_items(items2, &tmpw, true));
+        if (tmpw) cudaFree(tmpw);
+    }
     c->S = smax;
+    c->S2 = s2max;
     CK(cudaMalloc(&c->slotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
     CK(cudaMemcpy(c->slotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
     if (c->nitems) {
         CK(cudaMalloc(&c->items, sizeof(Item) * items.size()));
         CK(cudaMemcpy(c->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+    }
+    if (c->nitems2) {
+        CK(cudaMalloc(&c->items2, sizeof(Item) * items2.size()));
+        CK(cudaMemcpy(c->items2, items2.data(), sizeof(Item) * items2.size(), cudaMemcpyHostToDevice));
     }
     CK(cudaMalloc(&c->items_full, sizeof(Item) * items_full.size()));
     CK(cudaMemcpy(c->items_full, items_full.data(), sizeof(Item) * items_full.size(), cudaMemcpyHostToDevice));
@@ -535,15 +580,18 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // shared memory and warps per CTA of each pass: the largest W in {16, 12, 8, 6, 4} that fits
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-    const int Wc[5] = {16, 12, 8, 6, 4};
+    const int Wc[6] = {24, 16, 12, 8, 6, 4};
+    int w1max = 16;
+    if (const char *e = getenv("SRWCR_W1")) w1max = atoi(e);
     c->W = c->W2 = 0;
     for (int W : Wc) {
         const size_t s1 = sizeof(int) * (((size_t)W * c->S * LTS + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * 32 +
                           sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16;
-        if (!c->W && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
-        const size_t s2 = sizeof(float4) * (size_t)W * g.B * (GYS + 1) +
-                          sizeof(float) * (64 * (size_t)g.B + (g.B + 1) + 128 + W * 192) + sizeof(float) * npmax;
-        if (!c->W2 && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
+        if (!c->W && W <= w1max && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
+        const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (GYS + 1) +
+                          sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192) + ((g.B + 15) & ~15) +
+                          sizeof(float) * npmax;
+        if (!c->W2 && W <= 16 && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
     }
     if (c->W == 0 || c->W2 == 0) return fail(c, SRWCR_EINVAL, "shared memory too small for %d bins / %d slots", g.B, c->S);
     TRY(set_smem(c));
@@ -803,7 +851,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->itemw, c->itemw_full,
+    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma};
     for (void *p : bufs)

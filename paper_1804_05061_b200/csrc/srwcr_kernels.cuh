@@ -61,12 +61,13 @@ struct PassArgs {
     const int *slotbins;        // concatenated per-item slot -> bin lists
     double *SQ;                 // pass 1 out: [R][B][2] shifted binned first moments (lo, hi)
     double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
-    int W, S;                   // warps per CTA, slot capacity of the smem tables
+    int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
     double *grad;               // pass 2 out: [ndim][GzExt][Gy][Gx] (fp64)
     int segsteps;               // pass 2: shuffle steps of the segmented x-reduction
+    int pf;                     // L2 prefetch of the next slices (per pass, tunable)
 };
 
 __device__ __forceinline__ float f4(const float4 &v, int i) {
@@ -75,6 +76,15 @@ __device__ __forceinline__ float f4(const float4 &v, int i) {
 __device__ __forceinline__ float dot4(const float4 &a, const float4 &b) {
     return fmaf(a.w, b.w, fmaf(a.z, b.z, fmaf(a.y, b.y, a.x * b.x)));
 }
+// streaming load (read once: do not allocate in L1, keep L1 for the gathers of M)
+__device__ __forceinline__ float ld_stream(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+constexpr int PFD = 4;          // z-slices of look-ahead of the L2 prefetches
+
 // 2^k as a float, k in [-126, 127]
 __device__ __forceinline__ float exp2i(int k) { return __int_as_float((k + 127) << 23); }
 
@@ -214,24 +224,24 @@ __device__ __forceinline__ int select_bit(unsigned w, int r) {
 // the j-th set bit of a (<= 128-bit) mask, or -1
 __device__ __forceinline__ int mask_select(const unsigned (&bits)[4], int nw, int j) {
     int pos = -1, base = 0;
-    for (int k = 0; k < nw; ++k) {
-        const int c = __popc(bits[k]);
-        if (pos < 0 && j >= base && j < base + c) pos = 32 * k + select_bit(bits[k], j - base);
-        base += c;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        if (k < nw) {
+            const int c = __popc(bits[k]);
+            if (pos < 0 && j >= base && j < base + c) pos = 32 * k + select_bit(bits[k], j - base);
+            base += c;
+        }
     }
     return pos;
 }
 
-// sample cell along one axis (pass 1: no clamp flag): one unsigned compare on the fast path
+// sample cell along one axis (pass 1: no clamp flag), branch free; nm2 = max(N-2, 0)
 __device__ __forceinline__ int axis_fast(int i, float u, int nm2, float &t) {
     const float fu = floorf(u);
-    int c = i + (int)fu;
-    t = u - fu;
-    if ((unsigned)c > (unsigned)nm2) {
-        if (c < 0) { c = 0; t = 0.f; }
-        else { c = nm2; t = 1.f; }
-    }
-    return c;
+    const int c = i + (int)fu;
+    const float tt = u - fu;
+    t = c < 0 ? 0.f : (c > nm2 ? 1.f : tt);
+    return min(max(c, 0), nm2);
 }
 // same with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
 // flag telling that the fp32 position lies within tol of an integer, i.e. of a cell or
@@ -242,7 +252,7 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
     t = u - fu;
     cl = false;
     near = t < tol || t > 1.0f - tol;
-    if ((unsigned)c > (unsigned)nm2) {
+    if ((unsigned)c > (unsigned)nm2) {       // rare: outside [0, N-2]
         if (c < 0) { near = c == -1 && t > 1.0f - tol; c = 0; t = 0.f; cl = true; }
         else { near = c == nm2 + 1 && t < tol; cl = !(c == nm2 + 1 && t == 0.f); c = nm2; t = 1.f; }
     }
@@ -270,8 +280,8 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
 // line tables) so that the zero pattern of N is exact.
 // Lanes past the item's x-extent sample the item's last column with zero weights, so
 // the voxel loop has no divergent branches.
-template <int XV, bool STATIC>
-__global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
+template <int XV, bool STATIC, int MAXT = 512>
+__global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
     const int B = g.B, W = a.W, S = a.S;
@@ -326,8 +336,8 @@ __global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
     const int le = (lane & 7) >> 1;                               // fold lane's x-tap
     const int El_e = le == 0 ? El[0] : le == 1 ? El[1] : le == 2 ? El[2] : El[3];
     const float cI = it.cI;
-    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = g.nz - 2;
-    const int dzo = g.nz > 1 ? nxy : 0;
+    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
+    const int dzo = g.nz > 1 ? nxy : 0, nzl = g.nz - 1;
     const float *__restrict__ Mv = a.M;
     __syncthreads();
 
@@ -365,7 +375,7 @@ __global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
             float amax = 0.f;
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                const float Fv = __ldg(Fz + xv[v]);
+                const float Fv = ld_stream(Fz + xv[v]);
                 a0[v] = min((int)Fv, g.L - 1);
                 slot[v] = smap[a0[v]];
                 float hlo, hhi;
@@ -381,10 +391,17 @@ __global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
                     const int ccx = axis_fast(xv[v], ux, nxm2, tx);
                     const int ccy = axis_fast(y, uy, nym2, ty);
                     const int ccz = axis_fast(z, uz, nzm2, tz);
-                    const float *__restrict__ b = Mv + (ccz * nxy + ccy * nx + ccx);
-                    const float *__restrict__ b3 = b + dzo;
-                    const float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + nx), c110 = __ldg(b + nx + 1);
-                    const float c001 = __ldg(b3), c101 = __ldg(b3 + 1), c011 = __ldg(b3 + nx), c111 = __ldg(b3 + nx + 1);
+                    const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
+                    const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
+                    const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
+                    {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
+                        const int po = (min(ccz + PFD, nzl) - ccz) * nxy;
+                        prefetch_l2(Fz + PFD * nxy * (z + PFD <= nzl) + xv[v]);
+                        prefetch_l2(Mv + o0 + po);
+                        prefetch_l2(Mv + o1 + po);
+                        prefetch_l2(Mv + o2 + po);
+                        prefetch_l2(Mv + o3 + po);
+                    }
                     const float f0 = lerpf(lerpf(c000, c100, tx), lerpf(c010, c110, tx), ty);
                     const float f1 = lerpf(lerpf(c001, c101, tx), lerpf(c011, c111, tx), ty);
                     const float m = lerpf(f0, f1, tz);
@@ -466,13 +483,16 @@ __global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
             //      K[slot][ent][n] += wz_n * LT[slot][ent]
             unsigned bits[4] = {0u, 0u, 0u, 0u};
             int cnt = 0;
-            for (int k = 0; k < nwords; ++k) {
-                unsigned mine = 0u;
 #pragma unroll
-                for (int v = 0; v < XV; ++v) mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
-                bits[k] = __reduce_or_sync(FULL, mine);
-                wmask[k] |= bits[k];
-                cnt += __popc(bits[k]);
+            for (int k = 0; k < 4; ++k) {
+                if (k < nwords) {
+                    unsigned mine = 0u;
+#pragma unroll
+                    for (int v = 0; v < XV; ++v) mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
+                    bits[k] = __reduce_or_sync(FULL, mine);
+                    wmask[k] |= bits[k];
+                    cnt += __popc(bits[k]);
+                }
             }
             __syncwarp();
             const int ent = lane & 7;
@@ -500,8 +520,9 @@ __global__ void __launch_bounds__(512, 1) k_pass1(PassArgs a) {
             __syncwarp();
         }
         // ---- row done: fold the column table with the row's y-weights into the cell table
-        for (int k = 0; k < nwords; ++k) {
-            unsigned bw = wmask[k];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            unsigned bw = k < nwords ? wmask[k] : 0u;
             while (bw) {
                 const int s = 32 * k + __ffs(bw) - 1;
                 bw &= bw - 1;
@@ -760,11 +781,15 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
     const int zn0 = a.t.cb[2][it.z0];
     const int nzn = a.t.cb[2][it.z0 + it.zlen - 1] + 4 - zn0;
 
-    float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][B][GYS]
-    float4 *GZ = GY + W * B * GYS;                                // [W][B]
-    float *gl = reinterpret_cast<float *>(GZ + W * B);            // [64][B] gamma of the 64 regions
-    int *gbins = reinterpret_cast<int *>(gl + 64 * B);            // [B+1] bins a0 and a0+1 of the item, count
-    float *al = reinterpret_cast<float *>(gbins + B + 1);         // [64]
+    // gamma tables are indexed by the item's bin list (a0 and a0+1 of every slot,
+    // sorted, so bin a0+1 always sits right after a0): capacity GB = a.S2
+    const int GB = a.S2;
+    float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][GB][GYS]
+    float4 *GZ = GY + W * GB * GYS;                               // [W][GB]
+    float *gl = reinterpret_cast<float *>(GZ + W * GB);           // [64][GB] gamma of the 64 regions
+    int *gbins = reinterpret_cast<int *>(gl + 64 * GB);           // [GB+1] the bin list, count
+    unsigned char *gmap = reinterpret_cast<unsigned char *>(gbins + GB + 1);  // [B] bin -> list index
+    float *al = reinterpret_cast<float *>(gmap + ((B + 15) & ~15)); // [64]
     float *bl = al + 64;                                          // [64]
     float *RB = bl + 64;                                          // [W][3][64] retiring-layer row buffer
     float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
@@ -780,15 +805,16 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
             gbins[nb2++] = b0 + 1;
             last = b0 + 1;
         }
-        gbins[B] = nb2;
+        gbins[GB] = nb2;
     }
     __syncthreads();
-    nb2 = gbins[B];
-    for (int i = threadIdx.x; i < 64 * B; i += blockDim.x) {
-        const int reg = i / B, bin = i - reg * B;
+    nb2 = gbins[GB];
+    for (int i = threadIdx.x; i < nb2; i += blockDim.x) gmap[gbins[i]] = (unsigned char)i;
+    for (int i = threadIdx.x; i < 64 * nb2; i += blockDim.x) {
+        const int reg = i / nb2, k = i - reg * nb2;
         const int l = reg & 3, mm = (reg >> 2) & 3, n = reg >> 4;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        gl[i] = __ldg(a.gamma + r * B + bin);
+        gl[reg * GB + k] = __ldg(a.gamma + r * B + gbins[k]);
     }
     for (int i = threadIdx.x; i < 64; i += blockDim.x) {
         const int l = i & 3, mm = (i >> 2) & 3, n = i >> 4;
@@ -814,14 +840,14 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
         const int prev = __shfl_up_sync(FULL, cbx[v], 1);
         head[v] = lane == 0 || prev != cbx[v];
     }
-    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = g.nz - 2;
-    const int dzo = g.nz > 1 ? nxy : 0;
+    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
+    const int dzo = g.nz > 1 ? nxy : 0, nzl = g.nz - 1;
     const bool is2d = g.nz == 1;
     const int nwb = (B + 31) >> 5;
     const float *__restrict__ Mv = a.M;
     float *rbw = RB + warp * 192;
-    float4 *GYw = GY + warp * B * GYS;
-    float4 *GZw = GZ + warp * B;
+    float4 *GYw = GY + warp * GB * GYS;
+    float4 *GZw = GZ + warp * GB;
     __syncthreads();
 
     for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
@@ -830,15 +856,13 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
         const float4 swy = a.t.sw[1][y];
         const float *__restrict__ Frow = a.F + y * nx;
 
-        // gamma of the item's bins (a0 and a0+1 of every slot) contracted over the y-taps:
-        // GYw[bin][l] = float4_n( sum_m wy_m gamma[(n, m, l)][bin] )
-        for (int i = lane; i < it.nslots * 32; i += 32) {
-            const int s = i >> 5, e = i & 31;                     // e = (bin offset, l, n)
-            const int bin = a.slotbins[it.slot_off + s] + (e >> 4);
-            const int l = (e >> 2) & 3, n = e & 3;
-            const float *src = gl + (n * 16 + l) * B + bin;      // region (n, m, l): index n*16 + m*4 + l
-            const float val = swy.x * src[0] + swy.y * src[4 * B] + swy.z * src[8 * B] + swy.w * src[12 * B];
-            reinterpret_cast<float *>(GYw + bin * GYS + l)[n] = val;
+        // gamma of the item's bins contracted over the y-taps:
+        // GYw[k][l] = float4_n( sum_m wy_m gamma[(n, m, l)][bin k] )
+        for (int i = lane; i < nb2 * 16; i += 32) {
+            const int k = i >> 4, l = (i >> 2) & 3, n = i & 3;
+            const float *src = gl + (n * 16 + l) * GB + k;       // region (n, m, l): index n*16 + m*4 + l
+            const float val = swy.x * src[0] + swy.y * src[4 * GB] + swy.z * src[8 * GB] + swy.w * src[12 * GB];
+            reinterpret_cast<float *>(GYw + k * GYS + l)[n] = val;
         }
         // alpha (lanes 0-15) / beta (lanes 16-31) contracted over y: lane = 16*ab + 4*l + n
         float abY;
@@ -933,14 +957,14 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
             }
             // gamma of the item's bins contracted over z for this line: GZw[bin] = float4_l
             for (int i = lane; i < 4 * nb2; i += 32) {
-                const int bin = gbins[i >> 2], l = i & 3;
-                reinterpret_cast<float *>(GZw + bin)[l] = dot4(wz, GYw[bin * GYS + l]);
+                const int k = i >> 2, l = i & 3;
+                reinterpret_cast<float *>(GZw + k)[l] = dot4(wz, GYw[k * GYS + l]);
             }
             int a0[XV];
             float hlo[XV], hhi[XV];
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                const float Fv = __ldg(Fz + xv[v]);
+                const float Fv = ld_stream(Fz + xv[v]);
                 a0[v] = min((int)Fv, g.L - 1);
                 parzen_pair(Fv - (float)a0[v], hlo[v], hhi[v]);
             }
@@ -955,10 +979,17 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
                 const int ccx = axis_fast_cl(xv[v], ux, nxm2, fmaf(1e-6f, fabsf(ux), 2e-5f), tx, clx, nrx);
                 const int ccy = axis_fast_cl(y, uy, nym2, fmaf(1e-6f, fabsf(uy), 2e-5f), ty, cly, nry);
                 const int ccz = axis_fast_cl(z, uz, nzm2, fmaf(1e-6f, fabsf(uz), 2e-5f), tz, clz, nrz);
-                const float *__restrict__ b = Mv + (ccz * nxy + ccy * nx + ccx);
-                const float *__restrict__ b3 = b + dzo;
-                const float c000 = __ldg(b), c100 = __ldg(b + 1), c010 = __ldg(b + nx), c110 = __ldg(b + nx + 1);
-                const float c001 = __ldg(b3), c101 = __ldg(b3 + 1), c011 = __ldg(b3 + nx), c111 = __ldg(b3 + nx + 1);
+                const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
+                const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
+                const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
+                {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
+                    const int po = (min(ccz + PFD, nzl) - ccz) * nxy;
+                    prefetch_l2(Fz + PFD * nxy * (z + PFD <= nzl) + xv[v]);
+                    prefetch_l2(Mv + o0 + po);
+                    prefetch_l2(Mv + o1 + po);
+                    prefetch_l2(Mv + o2 + po);
+                    prefetch_l2(Mv + o3 + po);
+                }
                 const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
                 const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
                 const float f0 = lerpf(e00, e10, ty), f1 = lerpf(e01, e11, ty);
@@ -969,7 +1000,8 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
                 dgx = clx ? 0.f : dgx;
                 dgy = cly ? 0.f : dgy;
                 dgz = (clz || is2d) ? 0.f : dgz;
-                const float4 G0 = GZw[a0[v]], G1 = GZw[a0[v] + 1];
+                const int gk = gmap[a0[v]];
+                const float4 G0 = GZw[gk], G1 = GZw[gk + 1];
                 const float4 sw = swx[v];
                 const float At = fmaf(sw.w, ay[3], fmaf(sw.z, ay[2], fmaf(sw.y, ay[1], sw.x * ay[0])));
                 const float Bt = fmaf(sw.w, by4[3], fmaf(sw.z, by4[2], fmaf(sw.y, by4[1], sw.x * by4[0])));
