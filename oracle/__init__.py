@@ -81,6 +81,8 @@ def _load():
         lib.orc_combine.restype = ctypes.c_double
         lib.orc_grad_moments.argtypes = [c_cfg, vp, vp, vp, vp, vp, vp, ctypes.c_double, i64, i64, vp, vp]
         lib.orc_eval_moments.argtypes = [c_cfg, vp, vp, vp, vp]
+        lib.orc_bending.argtypes = [c_cfg, vp, vp]
+        lib.orc_bending.restype = ctypes.c_double
         lib.orc_eval_moments.restype = ctypes.c_double
         _lib = lib
     return _lib
@@ -322,3 +324,14 @@ def eval_moments(pb: Problem, F, M, params, want_grad: bool = True):
     grad = np.zeros(pb.params_shape) if want_grad else None
     D = _load().orc_eval_moments(ctypes.byref(c), _p(F), _p(M), _p(params), _p(grad))
     return D, grad
+
+
+# ------------------------------------------------------------ bending energy
+
+def bending(pb: Problem, params, want_grad: bool = True):
+    """(C_p, dC_p/dphi): bending energy of Eq 1 (reading c19)."""
+    c = pb.cfg()
+    params = _f64(params)
+    grad = np.zeros(pb.params_shape) if want_grad else None
+    E = _load().orc_bending(ctypes.byref(c), _p(params), _p(grad))
+    return E, grad

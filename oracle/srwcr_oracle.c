@@ -22,6 +22,8 @@
  *   (2) MOMENT route -- the exact algebraic rewrite of SURVEY.md Appendix A
  *       (weighted counts N, Parzen moments S, Q per region and fixed bin), the
  *       combine of SURVEY 8(a) a7 and the per-voxel derivative a8.
+ *   (3) the bending energy C_p of Eq 1 (reading c19), per
+ *       voxel from B-spline second-derivative tensor products.
  *
  * Geometry (SURVEY 8 "Conventions", readings c14-c16):
  *   volumes x-fastest [Nz][Ny][Nx]; Nz == 1 means 2-D.
@@ -738,4 +740,103 @@ double orc_eval_moments(const orc_cfg *c, const float *F, const float *M, const 
     }
     free(N); free(S); free(Q); free(al); free(be); free(ga);
     return D;
+}
+
+/* ============================================ (3) bending energy C_p (F1) === */
+
+/* First and second derivatives of the Eq 8 pieces with respect to t. */
+static void beta_d1(double t, double w[4]) {
+    w[0] = -(1.0 - t) * (1.0 - t) / 2.0;
+    w[1] = (3.0 * t * t - 4.0 * t) / 2.0;
+    w[2] = (-3.0 * t * t + 2.0 * t + 1.0) / 2.0;
+    w[3] = t * t / 2.0;
+}
+static void beta_d2(double t, double w[4]) {
+    w[0] = 1.0 - t;
+    w[1] = 3.0 * t - 2.0;
+    w[2] = -3.0 * t + 1.0;
+    w[3] = t;
+}
+
+/* Derivative-order-p tap weights of voxel i on the control lattice of axis ax,
+ * with respect to the voxel coordinate (d/di = (1/delta) d/dt).  The 2-D z axis
+ * is constant: weights (1,0,0,0) for p = 0 and 0 for p >= 1. */
+static void ctrl_taps_d(const orc_cfg *c, int ax, int64_t i, int64_t *b, double w[3][4]) {
+    double t;
+    if (ax == 2 && c->n[2] == 1) {
+        *b = 0;
+        for (int p = 0; p < 3; ++p)
+            for (int k = 0; k < 4; ++k) w[p][k] = (p == 0 && k == 0) ? 1.0 : 0.0;
+        return;
+    }
+    double s = (double)i / c->delta[ax];
+    double fl = floor(s);
+    *b = (int64_t)fl;
+    t = s - fl;
+    orc_beta(t, w[0]);
+    beta_d1(t, w[1]);
+    beta_d2(t, w[2]);
+    double d = c->delta[ax];
+    for (int k = 0; k < 4; ++k) {
+        w[1][k] /= d;
+        w[2][k] /= d * d;
+    }
+}
+
+/* Bending energy of the FFD, the constraint C_p of Eq 1 (form of
+ * Rueckert et al. [26], reading c19):
+ *   C_p = (1/V) sum_x sum_c [ u_c,xx^2 + u_c,yy^2 + u_c,zz^2
+ *                             + 2 u_c,xy^2 + 2 u_c,xz^2 + 2 u_c,yz^2 ]
+ * over every voxel x of the volume (V voxels) and displacement component c, with
+ * derivatives in voxel coordinates (u in voxels); in 2-D only the x,y terms.
+ * Each second derivative is the tensor product of Eq 8 derivative weights (Eq 17
+ * taps).  grad (nullable, zeroed here) receives dC_p/dphi.  Written per voxel:
+ * plain and slow. */
+double orc_bending(const orc_cfg *c, const double *params, double *grad) {
+    int64_t G[3], K[3];
+    orc_derived(c, G, K);
+    int nd = ndim_of(c);
+    int64_t nodes = G[0] * G[1] * G[2];
+    double V = (double)c->n[0] * (double)c->n[1] * (double)c->n[2];
+    /* the six (ordered-pair-folded) terms: derivative orders per axis, weight */
+    static const int ord[6][3] = {{2, 0, 0}, {0, 2, 0}, {0, 0, 2}, {1, 1, 0}, {1, 0, 1}, {0, 1, 1}};
+    static const double tw[6] = {1.0, 1.0, 1.0, 2.0, 2.0, 2.0};
+    int use[6];
+    for (int t = 0; t < 6; ++t) use[t] = nd == 3 || ord[t][2] == 0;
+    if (grad) memset(grad, 0, sizeof(double) * (size_t)(nd * nodes));
+    double E = 0.0;
+    for (int64_t z = 0; z < c->n[2]; ++z)
+        for (int64_t y = 0; y < c->n[1]; ++y)
+            for (int64_t x = 0; x < c->n[0]; ++x) {
+                int64_t bx, by, bz;
+                double wx[3][4], wy[3][4], wz[3][4];
+                ctrl_taps_d(c, 0, x, &bx, wx);
+                ctrl_taps_d(c, 1, y, &by, wy);
+                ctrl_taps_d(c, 2, z, &bz, wz);
+                int nzt = nd == 3 ? 4 : 1;
+                for (int comp = 0; comp < nd; ++comp) {
+                    double h[6] = {0, 0, 0, 0, 0, 0};
+                    for (int n = 0; n < nzt; ++n)
+                        for (int m = 0; m < 4; ++m)
+                            for (int l = 0; l < 4; ++l) {
+                                double phi = params[comp * nodes + node_index(G, bx + l, by + m, bz + n)];
+                                for (int t = 0; t < 6; ++t)
+                                    if (use[t])
+                                        h[t] += wx[ord[t][0]][l] * wy[ord[t][1]][m] * wz[ord[t][2]][n] * phi;
+                            }
+                    for (int t = 0; t < 6; ++t)
+                        if (use[t]) E += tw[t] * h[t] * h[t];
+                    if (!grad) continue;
+                    for (int n = 0; n < nzt; ++n)
+                        for (int m = 0; m < 4; ++m)
+                            for (int l = 0; l < 4; ++l) {
+                                double s = 0.0;
+                                for (int t = 0; t < 6; ++t)
+                                    if (use[t])
+                                        s += 2.0 * tw[t] * h[t] * wx[ord[t][0]][l] * wy[ord[t][1]][m] * wz[ord[t][2]][n];
+                                grad[comp * nodes + node_index(G, bx + l, by + m, bz + n)] += s / V;
+                            }
+                }
+            }
+    return E / V;
 }

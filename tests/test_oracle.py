@@ -386,3 +386,83 @@ def test_slab_partials_sum_to_full():
     g_full = O.grad_moments(pb, F, M, params, al, be, ga, Z)
     g_parts = sum(O.grad_moments(pb, F, M, params, al, be, ga, Z, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
     assert np.linalg.norm(g_parts - g_full) <= 1e-13 * np.linalg.norm(g_full)
+
+
+# ------------------------------------------------ bending energy C_p (F1, c19)
+
+def _node_coords(pb):
+    """Positions (voxels) of the control nodes: node j at (j - 1) * delta (reading c15)."""
+    G = pb.derived()[0]
+    xs = [(np.arange(G[a]) - 1.0) * pb.delta[a] for a in range(3)]
+    if pb.dims[2] == 1:
+        xs[2] = np.zeros(1)
+    Z, Y, X = np.meshgrid(xs[2], xs[1], xs[0], indexing="ij")
+    return X, Y, Z
+
+
+@pytest.mark.parametrize("dims,delta", [((21, 17, 13), (4.0, 3.5, 5.0)), ((19, 23, 1), (3.0, 4.5, 1.0))])
+def test_bending_zero_and_affine_fields_vanish(dims, delta):
+    pb = O.Problem(dims=dims, L=15, delta=delta, kcells=(2, 2, 2 if dims[2] > 1 else 0))
+    E, g = O.bending(pb, np.zeros(pb.params_shape))
+    assert E == 0.0 and not g.any()
+    # B-splines reproduce linear functions: an affine displacement has no curvature
+    X, Y, Z = _node_coords(pb)
+    rng = np.random.default_rng(3)
+    phi = np.stack([rng.normal() * X + rng.normal() * Y + rng.normal() * Z + rng.normal()
+                    for _ in range(pb.ndim)])
+    E, _ = O.bending(pb, phi)
+    assert abs(E) < 1e-20
+
+
+@pytest.mark.parametrize("dims,delta", [((21, 17, 13), (4.0, 3.5, 5.0)), ((16, 16, 16), (2.5, 3.0, 4.0))])
+def test_bending_closed_forms_3d(dims, delta):
+    """Cubic B-splines reproduce quadratics with coefficients xi^2 - delta^2/3 (variance
+    of the cubic B-spline kernel = delta^2/3) and products xi*eta exactly, so u = x^2
+    gives u_xx = 2 everywhere (C_p = 4), u = x*y gives u_xy = 1 (C_p = 2, cross terms
+    doubled), and terms on different components / second derivatives add."""
+    pb = O.Problem(dims=dims, L=15, delta=delta, kcells=(2, 2, 2))
+    X, Y, Z = _node_coords(pb)
+    dx, dy, dz = pb.delta
+    zero = np.zeros_like(X)
+    cases = [
+        ((X**2 - dx * dx / 3, zero, zero), 4.0),
+        ((zero, Y**2 - dy * dy / 3, zero), 4.0),
+        ((zero, zero, Z**2 - dz * dz / 3), 4.0),
+        ((zero, X * Y, zero), 2.0),
+        ((X * Z, zero, zero), 2.0),
+        ((zero, zero, Y * Z), 2.0),
+        ((zero, zero, Z**2 - dz * dz / 3 + X * Y), 6.0),
+        ((0.5 * (X**2 - dx * dx / 3), 3 * Y * Z, zero), 1.0 + 18.0),
+    ]
+    for phi, want in cases:
+        E, _ = O.bending(pb, np.stack(phi))
+        assert E == pytest.approx(want, rel=1e-12), (want, E)
+
+
+def test_bending_closed_forms_2d():
+    pb = O.Problem(dims=(19, 23, 1), L=15, delta=(3.0, 4.5, 1.0), kcells=(2, 2, 0))
+    X, Y, _ = _node_coords(pb)
+    dx, dy = pb.delta[:2]
+    E, _ = O.bending(pb, np.stack([X**2 - dx * dx / 3 + Y**2 - dy * dy / 3, np.zeros_like(X)]))
+    assert E == pytest.approx(8.0, rel=1e-12)
+    E, _ = O.bending(pb, np.stack([np.zeros_like(X), X * Y]))
+    assert E == pytest.approx(2.0, rel=1e-12)
+
+
+@pytest.mark.parametrize("dims,delta", [((13, 11, 9), (3.0, 2.5, 3.5)), ((14, 12, 1), (3.0, 4.0, 1.0))])
+def test_bending_gradient_central_differences(dims, delta):
+    pb = O.Problem(dims=dims, L=15, delta=delta, kcells=(1, 1, 1 if dims[2] > 1 else 0))
+    rng = np.random.default_rng(5)
+    phi = rng.normal(size=pb.params_shape)
+    E, g = O.bending(pb, phi)
+    assert E > 0
+    flat = phi.reshape(-1)
+    idx = rng.choice(flat.size, 40, replace=False)
+    h = 1e-3
+    for i in idx:   # C_p is quadratic: central differences are exact up to rounding
+        p = flat.copy(); p[i] += h
+        m = flat.copy(); m[i] -= h
+        fd = (O.bending(pb, p.reshape(phi.shape), False)[0] - O.bending(pb, m.reshape(phi.shape), False)[0]) / (2 * h)
+        assert g.reshape(-1)[i] == pytest.approx(fd, rel=1e-7, abs=1e-12)
+    # quadratic form: phi . grad = 2 C_p
+    assert float((phi * g).sum()) == pytest.approx(2 * E, rel=1e-12)
