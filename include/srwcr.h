@@ -53,7 +53,8 @@ typedef enum {
     SRWCR_ENCCL = -4,       /* NCCL error or NCCL library not loadable */
     SRWCR_EDEGENERATE = -5, /* no region passed the retention test (reading c12) */
     SRWCR_ENOTSUP = -6,     /* option not supported by this build */
-    SRWCR_ESTATE = -7       /* context poisoned by an earlier CUDA error, or call out of order */
+    SRWCR_ESTATE = -7,      /* context poisoned by an earlier CUDA error, or call out of order */
+    SRWCR_ENONFINITE = -8   /* srwcr_register: cost or gradient not finite */
 } srwcr_status;
 
 typedef struct {
@@ -122,24 +123,60 @@ srwcr_status srwcr_eval_end(srwcr_ctx *ctx, double *value, double *grad);
  * Host-only (no GPU needed).  Slabs split the slices as evenly as possible. */
 srwcr_status srwcr_plan_slab(int64_t nz, int32_t nranks, int32_t rank, int64_t *z0, int64_t *z1);
 
+/* Bending energy C_p of the FFD (the constraint of Eq 1; Rueckert et
+ * al. [26]; reading c19 of DESIGN.md):
+ *   C_p = (1/V) sum_voxels sum_c [u_c,xx^2 + u_c,yy^2 + u_c,zz^2
+ *                                 + 2u_c,xy^2 + 2u_c,xz^2 + 2u_c,yz^2]
+ * V = Nx*Ny*Nz, derivatives in voxel coordinates (u in voxels), x,y terms only in
+ * 2-D.  Evaluated on the device as phi . H phi / V with H the separable sum of
+ * 1-D B-spline derivative Gram matrices (banded, 7 diagonals).
+ *   params  fp64 [ndim][Gz][Gy][Gx], host or device pointer (read only)
+ *   value   out: C_p (host pointer, required)
+ *   grad    out (nullable): dC_p/dphi, host or device, same layout (overwritten)
+ * Deterministic (no atomics).  Errors: EINVAL (NULL ctx/params/value), ECUDA. */
+srwcr_status srwcr_bending(srwcr_ctx *ctx, const double *params, double *value, double *grad);
+
 /* L-BFGS registration of C = D + w_p * C_p (Eq 1).  params_inout is a
- * host fp64 array (layout above): the start point on entry, the result on return.
- * cfg may be NULL for defaults (m = 5, max_iter 200, w_p = 0.1).  report may be NULL. */
+ * host fp64 array (layout above): the start point on entry, the result on return
+ * (the last accepted iterate, also on a line-search failure).
+ * cfg may be NULL for defaults (srwcr_default_lbfgs_config); report may be NULL;
+ * when given, each must carry struct_size = sizeof(its type) (EINVAL otherwise).
+ * Algorithm (reading c20): two-loop recursion with m corrections, initial step
+ * 1/||g|| then 1 with the y.s/y.y initial-Hessian scaling; backtracking line search
+ * (x0.5 on an Armijo failure with constant ftol, x2.1 on a curvature failure with
+ * constant wolfe -- the regular Wolfe condition); each trial first runs the value
+ * only (pass 1 + combine) and computes the gradient (pass 2) only once the Armijo
+ * test passes; pairs with y.s <= 0 are not stored.  Stops when (a) ||g|| <=
+ * epsilon * max(1, ||phi||), (b) the spread (max - min) of C over the last
+ * stable_window accepted iterates is < stable_tol * max(|C|, 1e-12) ("stable within
+ * the last 20 steps"), (c) max_iter iterations, (d) the line search fails.
+ * With nranks > 1 every rank runs the same replicated loop (all reductions are
+ * deterministic, so the iterates stay identical across ranks).
+ * Errors: EINVAL, ESTATE (caller-driven exchange mode), EDEGENERATE, ECUDA, and
+ * SRWCR_ENONFINITE when C or the gradient is not finite. */
 typedef struct {
     int32_t struct_size;
     int32_t m;                 /* number of corrections (paper: 5) */
     int32_t max_iter;          /* paper: 200/200/120 per resolution level */
-    int32_t max_linesearch;    /* backtracking steps per iteration */
+    int32_t max_linesearch;    /* trials per iteration (default 20) */
     double w_p;                /* penalty weight (paper: 0.1 mono-modal, 30 multi-modal) */
-    double ftol, wolfe;        /* Armijo and curvature constants of the backtracking search */
-    int32_t stable_window;     /* stop when C changed < stable_tol over this many steps (paper: 20) */
-    double stable_tol;
+    double ftol, wolfe;        /* Armijo and curvature constants (defaults 1e-4, 0.9) */
+    int32_t stable_window;     /* stop when C is stable over this many iterates (paper: 20) */
+    int32_t verbose;           /* 1: one line per iteration on stderr */
+    double stable_tol;         /* default 1e-5 */
+    double epsilon;            /* gradient-norm test (default 0 = off; P:226 names only
+                                  the stability and iteration rules) */
 } srwcr_lbfgs_config;
 
 typedef struct {
     int32_t struct_size;
-    int32_t iterations, evaluations, status; /* status: 0 converged/stable, 1 max_iter, 2 line search failed */
-    double initial_cost, final_cost, final_value;
+    int32_t iterations, evaluations, status; /* status: 0 converged (gradient test), 1 stable
+                                                (C stable over the window), 2 max_iter,
+                                                3 line search failed */
+    int32_t gradient_evaluations;
+    double initial_cost, final_cost;         /* C = D + w_p C_p */
+    double final_value, final_penalty;       /* D and C_p at the result */
+    double grad_norm;                        /* ||dC/dphi|| at the result */
 } srwcr_register_report;
 
 srwcr_status srwcr_default_lbfgs_config(srwcr_lbfgs_config *cfg);

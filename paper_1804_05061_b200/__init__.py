@@ -26,7 +26,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
               "-Xcompiler", "-fPIC", "-shared"]
 
 # status codes (include/srwcr.h)
-OK, EINVAL, ENOMEM, ECUDA, ENCCL, EDEGENERATE, ENOTSUP, ESTATE = 0, -1, -2, -3, -4, -5, -6, -7
+OK, EINVAL, ENOMEM, ECUDA, ENCCL, EDEGENERATE, ENOTSUP, ESTATE, ENONFINITE = 0, -1, -2, -3, -4, -5, -6, -7, -8
 DUMP = dict(fixed=1, moving=2, a0=3, ctrl_taps=4, spat_taps=5, N=6, SQ=7, regions=8, coefs=9)
 
 
@@ -63,11 +63,28 @@ class _Stats(ctypes.Structure):
                 ("voxels_per_lane", ctypes.c_int32), ("items", ctypes.c_int32)]
 
 
+class _LbfgsConfig(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("m", ctypes.c_int32), ("max_iter", ctypes.c_int32),
+                ("max_linesearch", ctypes.c_int32), ("w_p", ctypes.c_double), ("ftol", ctypes.c_double),
+                ("wolfe", ctypes.c_double), ("stable_window", ctypes.c_int32), ("verbose", ctypes.c_int32),
+                ("stable_tol", ctypes.c_double), ("epsilon", ctypes.c_double)]
+
+
+class _Report(ctypes.Structure):
+    _fields_ = [("struct_size", ctypes.c_int32), ("iterations", ctypes.c_int32), ("evaluations", ctypes.c_int32),
+                ("status", ctypes.c_int32), ("gradient_evaluations", ctypes.c_int32),
+                ("initial_cost", ctypes.c_double), ("final_cost", ctypes.c_double),
+                ("final_value", ctypes.c_double), ("final_penalty", ctypes.c_double),
+                ("grad_norm", ctypes.c_double)]
+
+
+REGISTER_STATUS = {0: "converged", 1: "stable", 2: "max_iter", 3: "line_search_failed"}
+
 _lib = None
 
 EXPORTS = ["srwcr_default_options", "srwcr_create", "srwcr_num_params", "srwcr_eval", "srwcr_eval_begin",
            "srwcr_stats_buffer", "srwcr_eval_end", "srwcr_plan_slab", "srwcr_default_lbfgs_config",
-           "srwcr_register", "srwcr_debug_size", "srwcr_debug_dump", "srwcr_set_timing", "srwcr_get_stats",
+           "srwcr_register", "srwcr_bending", "srwcr_debug_size", "srwcr_debug_dump", "srwcr_set_timing", "srwcr_get_stats",
            "srwcr_stream", "srwcr_last_error", "srwcr_destroy"]
 
 
@@ -96,8 +113,9 @@ def lib():
         L.srwcr_last_error.argtypes = [vp]
         L.srwcr_last_error.restype = ctypes.c_char_p
         L.srwcr_destroy.argtypes = [vp]
-        L.srwcr_register.argtypes = [vp, vp, vp, vp]
-        L.srwcr_default_lbfgs_config.argtypes = [vp]
+        L.srwcr_register.argtypes = [vp, vp, P(_LbfgsConfig), P(_Report)]
+        L.srwcr_default_lbfgs_config.argtypes = [P(_LbfgsConfig)]
+        L.srwcr_bending.argtypes = [vp, vp, P(dbl), vp]
         for name in EXPORTS:
             if name not in ("srwcr_last_error", "srwcr_destroy"):
                 getattr(L, name).restype = ctypes.c_int
@@ -214,6 +232,37 @@ class Srwcr:
         D = ctypes.c_double()
         self._check(lib().srwcr_eval_end(self._ctx, ctypes.byref(D), gp))
         return D.value, (grad if want_grad else None)
+
+    def bending(self, params, grad=None, want_grad=True):
+        """(C_p, dC_p/dPhi): bending energy of the FFD (Eq 1; reading c19)."""
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        if want_grad and grad is None:
+            grad = np.empty(self.params_shape, dtype=np.float64)
+        gp, gk = _ptr(grad) if want_grad else (None, None)
+        E = ctypes.c_double()
+        self._check(lib().srwcr_bending(self._ctx, pp, ctypes.byref(E), gp))
+        return E.value, (grad if want_grad else None)
+
+    def register(self, params=None, **cfg):
+        """L-BFGS minimisation of C = D + w_p C_p (Eq 1) from params (default 0).
+
+        cfg: any field of srwcr_lbfgs_config (m, max_iter, max_linesearch, w_p, ftol,
+        wolfe, stable_window, verbose, stable_tol, epsilon).  Returns (params, report)."""
+        c = _LbfgsConfig()
+        lib().srwcr_default_lbfgs_config(ctypes.byref(c))
+        for k, v in cfg.items():
+            if k not in dict(_LbfgsConfig._fields_) or k == "struct_size":
+                raise TypeError(f"unknown L-BFGS option {k}")
+            setattr(c, k, v)
+        x = np.zeros(self.params_shape) if params is None else np.array(params, dtype=np.float64, copy=True)
+        x = np.ascontiguousarray(x)
+        rep = _Report()
+        rep.struct_size = ctypes.sizeof(_Report)
+        self._check(lib().srwcr_register(self._ctx, x.ctypes.data_as(ctypes.c_void_p), ctypes.byref(c),
+                                         ctypes.byref(rep)))
+        out = {f: getattr(rep, f) for f, _ in _Report._fields_ if f != "struct_size"}
+        out["status_name"] = REGISTER_STATUS.get(rep.status, "?")
+        return x, out
 
     def debug_dump(self, what: str) -> np.ndarray:
         code = DUMP[what]

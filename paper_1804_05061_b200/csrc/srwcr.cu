@@ -67,7 +67,7 @@ struct srwcr_ctx {
     std::vector<int> h_cb[3], h_sb[3];
     std::vector<float4> h_sw[3];
     // device
-    float *F = nullptr, *M = nullptr, *phi = nullptr;
+    float *F = nullptr, *M = nullptr, *phi = nullptr, *phimax = nullptr;
     double *params64 = nullptr, *grad64 = nullptr;
     const double *cur_params = nullptr;  // device fp64 params of the current evaluation
     int *cb[3]{}, *sb[3]{};
@@ -98,6 +98,12 @@ struct srwcr_ctx {
     cudaEvent_t ev[4]{};
     float ms[4]{};
     double *pinned = nullptr;  // 2 doubles
+    // bending energy / L-BFGS (srwcr_register.inc)
+    double *bend_gram = nullptr;  // [3 axes][3 orders][Gmax][7] banded 1-D Gram matrices
+    double *bend_ws = nullptr;    // 8 vectors of nparams: Hphi, Z0..Z2, A0..A2, staging
+    double *dot_part = nullptr;   // deterministic dot-product partials
+    double *dot_host = nullptr;   // pinned, 16 doubles
+    int64_t gram_G = 0;
 };
 
 static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
@@ -219,6 +225,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     }
     a.p64 = c->cur_params;
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
+    a.phimax = c->phimax; a.pmcs = (long long)c->g.Gx * c->g.Gy * c->g.Gz;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
@@ -559,6 +566,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // buffers
     const long long RB = c->R * g.B;
     CK(cudaMalloc(&c->phi, sizeof(float) * c->nint));
+    CK(cudaMalloc(&c->phimax, sizeof(float) * c->nint * 2));  // result + scratch
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->SQ, sizeof(double) * stats_count(c)));
@@ -640,7 +648,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             cudaFree(tmp);
         }
     }
-    c->launches_per_eval = 5;  // params->f32, pass 1, combine, reduce_D, pass 2
+    c->launches_per_eval = 8;  // params->f32, 3 window-max, pass 1, combine, reduce_D, pass 2
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -686,6 +694,15 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
     CKL();
+    {   // tap-window max |phi_c| for pass 2's rounding bound (x, y into scratch, z into phimax)
+        float *scr = c->phimax + c->nint;
+        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, c->phimax, c->g);
+        CKL();
+        k_window_max<1><<<592, 256, 0, c->stream>>>(c->phimax, scr, c->g);
+        CKL();
+        k_window_max<2><<<592, 256, 0, c->stream>>>(scr, c->phimax, c->g);
+        CKL();
+    }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
     TRY(launch_pass1(c, false));
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
@@ -851,7 +868,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void *bufs[] = {c->F, c->M, c->phi, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
+    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma};
     for (void *p : bufs)
@@ -866,6 +883,9 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     for (int i = 0; i < 4; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->dot_host) cudaFreeHost(c->dot_host);
+    for (double *p : {c->bend_gram, c->bend_ws, c->dot_part})
+        if (p) cudaFree(p);
     if (c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }

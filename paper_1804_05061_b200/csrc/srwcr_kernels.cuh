@@ -63,6 +63,8 @@ struct PassArgs {
     double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
+    const float *phimax;        // pass 2: [3][Gz][Gy][Gx] max |phi_c| over the tap window
+    long long pmcs;             //         component stride of phimax
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
     double *grad;               // pass 2 out: [ndim][GzExt][Gy][Gx] (fp64)
@@ -93,33 +95,34 @@ __device__ __forceinline__ float exp2i(int k) { return __int_as_float((k + 127) 
 // contracted over the 4x4 (x, y) taps: U[v][c] = sum_{l,m} cwx_l cwy_m phi[c][gz][cby+m][cbx_v+l].
 // The warp shares one row y, so lanes j < nxn first contract y for x-node xn0+j
 // (coalesced loads), then every lane gathers its 4 x-taps per voxel by shuffle.
-template <int XV>
+template <int XV, int NC = 3>
 __device__ __forceinline__ void ffd_layer(const float *__restrict__ phi, const Geo &g, int gz, int cby, float4 cwy,
                                           int xn0, int nxn, const int (&relx)[XV], const float4 (&cwx)[XV],
-                                          int lane, float (&U)[XV][3]) {
-    float p0 = 0.f, p1 = 0.f, p2 = 0.f;
+                                          int lane, float (&U)[XV][NC]) {
+    float p[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) p[c] = 0.f;
     if (lane < nxn) {
         const long long plane = (long long)g.Gx * g.Gy;
         const long long cs = plane * g.Gz;
-        const float *p = phi + (long long)gz * plane + (long long)cby * g.Gx + xn0 + lane;
+        const float *q = phi + (long long)gz * plane + (long long)cby * g.Gx + xn0 + lane;
 #pragma unroll
         for (int m = 0; m < 4; ++m) {
             const float w = f4(cwy, m);
-            p0 = fmaf(w, __ldg(p + m * g.Gx), p0);
-            p1 = fmaf(w, __ldg(p + cs + m * g.Gx), p1);
-            p2 = fmaf(w, __ldg(p + 2 * cs + m * g.Gx), p2);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) p[c] = fmaf(w, __ldg(q + c * cs + m * g.Gx), p[c]);
         }
     }
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
-        U[v][0] = U[v][1] = U[v][2] = 0.f;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) U[v][c] = 0.f;
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
             const int src = relx[v] + l;
             const float w = f4(cwx[v], l);
-            U[v][0] = fmaf(w, __shfl_sync(FULL, p0, src), U[v][0]);
-            U[v][1] = fmaf(w, __shfl_sync(FULL, p1, src), U[v][1]);
-            U[v][2] = fmaf(w, __shfl_sync(FULL, p2, src), U[v][2]);
+#pragma unroll
+            for (int c = 0; c < NC; ++c) U[v][c] = fmaf(w, __shfl_sync(FULL, p[c], src), U[v][c]);
         }
     }
 }
@@ -245,16 +248,18 @@ __device__ __forceinline__ int axis_fast(int i, float u, int nm2, float &t) {
 }
 // same with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
 // flag telling that the fp32 position lies within tol of an integer, i.e. of a cell or
-// clamp boundary where the derivative of the interpolant jumps
+// clamp boundary where the derivative of the interpolant jumps.  tol bounds |u32 - u64|
+// (see k_pass2); tol = 0 (all tap nodes of the component at rest) never flags.
 __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, float &t, bool &cl, bool &near) {
     const float fu = floorf(u);
     int c = i + (int)fu;
     t = u - fu;
     cl = false;
-    near = t < tol || t > 1.0f - tol;
+    // cell and clamp boundaries sit at integer u; u - rint(u) is exact in fp32
+    near = fabsf(u - rintf(u)) < tol;
     if ((unsigned)c > (unsigned)nm2) {       // rare: outside [0, N-2]
-        if (c < 0) { near = c == -1 && t > 1.0f - tol; c = 0; t = 0.f; cl = true; }
-        else { near = c == nm2 + 1 && t < tol; cl = !(c == nm2 + 1 && t == 0.f); c = nm2; t = 1.f; }
+        if (c < 0) { near = near && c == -1; c = 0; t = 0.f; cl = true; }
+        else { near = near && c == nm2 + 1; cl = !(c == nm2 + 1 && t == 0.f); c = nm2; t = 1.f; }
     }
     return c;
 }
@@ -843,7 +848,6 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
     const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
     const int dzo = g.nz > 1 ? nxy : 0, nzl = g.nz - 1;
     const bool is2d = g.nz == 1;
-    const int nwb = (B + 31) >> 5;
     const float *__restrict__ Mv = a.M;
     float *rbw = RB + warp * 192;
     float4 *GYw = GY + warp * GB * GYS;
@@ -974,11 +978,16 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
                 const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
                 const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
                 const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
+                // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi and
+                // weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that
+                const int wo = (gzl * g.Gy + cby) * g.Gx + cbx[v];
+                const float tlx = 4e-6f * __ldg(a.phimax + wo), tly = 4e-6f * __ldg(a.phimax + a.pmcs + wo),
+                            tlz = 4e-6f * __ldg(a.phimax + 2 * a.pmcs + wo);
                 float tx, ty, tz;
                 bool clx, cly, clz, nrx, nry, nrz;
-                const int ccx = axis_fast_cl(xv[v], ux, nxm2, fmaf(1e-6f, fabsf(ux), 2e-5f), tx, clx, nrx);
-                const int ccy = axis_fast_cl(y, uy, nym2, fmaf(1e-6f, fabsf(uy), 2e-5f), ty, cly, nry);
-                const int ccz = axis_fast_cl(z, uz, nzm2, fmaf(1e-6f, fabsf(uz), 2e-5f), tz, clz, nrz);
+                const int ccx = axis_fast_cl(xv[v], ux, nxm2, tlx, tx, clx, nrx);
+                const int ccy = axis_fast_cl(y, uy, nym2, tly, ty, cly, nry);
+                const int ccz = axis_fast_cl(z, uz, nzm2, tlz, tz, clz, nrz);
                 const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
                 const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
                 const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
@@ -1011,8 +1020,13 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
                 float g1p, c2;
                 if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
                 else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
-                // discontinuities of the per-voxel derivative: decide them in fp64
-                if (nrx || nry || (nrz && !is2d) || fm < 5e-5f || fm > 1.0f - 5e-5f)
+                // discontinuities of the per-voxel derivative: decide them in fp64.  A flat
+                // cell (8 equal corners) gives m = that corner exactly in fp32 and fp64, so
+                // its Parzen-kink side needs no fp64 re-evaluation (flat background).
+                if (nrx || nry || (nrz && !is2d) ||
+                    ((fm < 5e-5f || fm > 1.0f - 5e-5f) &&
+                     !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 && c101 == c000 &&
+                       c011 == c000 && c111 == c000)))
                     exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
                                  cbx[v], cby, bz, a.t.cw64[0][xv[v]], a.t.cw64[1][y], a.t.cw64[2][z], xv[v], y, z,
                                  dgx, dgy, dgz, g1p, c2);
@@ -1051,16 +1065,39 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
 // ---------------------------------------------------------------- small kernels
 
 // fp64 external params [ndim][GzExt][Gy][Gx] -> fp32 internal [3][Gz][Gy][Gx] (zeros padded)
+// phi[c][Gz][Gy][Gx] fp32 (internal layout, Gz padded to 4 in 2-D with zeros)
 __global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict__ phi, Geo g) {
     const long long plane = (long long)g.Gx * g.Gy;
-    const long long total = 3LL * g.Gz * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total; i += (long long)gridDim.x * blockDim.x) {
-        const long long c = i / (g.Gz * plane);
-        const long long rem = i - c * g.Gz * plane;
-        const long long gz = rem / plane, xy = rem - gz * plane;
-        float v = 0.f;
-        if (c < g.ndim && gz < g.GzExt) v = (float)p[(c * g.GzExt + gz) * plane + xy];
-        phi[i] = v;
+    const long long cs = (long long)g.Gz * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cs; i += (long long)gridDim.x * blockDim.x) {
+        const long long gz = i / plane, xy = i - gz * plane;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            double v = 0.0;
+            if (c < g.ndim && gz < g.GzExt) v = p[(c * g.GzExt + gz) * plane + xy];
+            phi[c * cs + i] = (float)v;
+        }
+    }
+}
+
+// max of |phi_c| over the 4 nodes [k, k+3] along axis AX (clipped to the grid), for all
+// 3 components: three passes give the max over each voxel's 4x4x4 tap window keyed by
+// its base node -- the scale of pass 2's rounding bound (k_pass2)
+template <int AX>
+__global__ void k_window_max(const float *__restrict__ in, float *__restrict__ out, Geo g) {
+    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * cs; i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i % cs;
+        int k, G;
+        long long st;
+        if (AX == 0) { k = (int)(r % g.Gx); G = g.Gx; st = 1; }
+        else if (AX == 1) { k = (int)((r / g.Gx) % g.Gy); G = g.Gy; st = g.Gx; }
+        else { k = (int)(r / plane); G = g.Gz; st = plane; }
+        float m = 0.f;
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+            if (k + d < G) m = fmaxf(m, fabsf(in[i + d * st]));
+        out[i] = m;
     }
 }
 

@@ -108,9 +108,10 @@ def test_host_and_device_pointers_agree():
     pt = torch.from_numpy(params).cuda()
     gt = torch.empty_like(pt)
     D2, _ = g.eval(pt, grad=gt)
-    # atomics make the summation order (not the arithmetic) differ between evaluations
-    assert rel(D2, D1) <= 1e-12
-    assert rel_l2(gt.cpu().numpy(), g1) <= 1e-6
+    # fp32 shared-memory atomics (column/cell tables) make the summation
+    # order -- not the arithmetic -- differ between evaluations: fp32-rounding-sized noise
+    assert rel(D2, D1) <= 2e-7
+    assert rel_l2(gt.cpu().numpy(), g1) <= 1e-5
     g.close()
 
 
@@ -155,8 +156,8 @@ def test_slab_decomposition_on_one_gpu(P):
         assert rt.cudaMemcpy(ctypes.c_void_p(p), tot.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(8 * n), 4) == 0
     outs = [r.eval_end() for r in ranks]
     for D, _ in outs:
-        assert rel(D, D1) <= 1e-9
+        assert rel(D, D1) <= 2e-7   # fp32 atomic summation order (see above)
     gsum = np.sum([gk for _, gk in outs], axis=0)
-    assert rel_l2(gsum, grad1) <= 1e-6
+    assert rel_l2(gsum, grad1) <= 1e-5
     for r in ranks + [g1]:
         r.close()

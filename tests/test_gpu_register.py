@@ -1,0 +1,123 @@
+"""GPU checks of SURVEY 8(f) row F1: the bending energy C_p (srwcr_bending) against the
+fp64 oracle (element by element on reduced sizes; quadratic-form properties and
+closed forms at full size), and the L-BFGS driver srwcr_register by its
+contract: monotone accepted costs, a report consistent with independent evaluations
+of the result, identity registration staying at identity, and a synthetic
+misalignment reduced."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+import paper_1804_05061_b200 as S
+from gpu_common import REDUCED, problem, rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_bending_matches_oracle(name):
+    g, pb, Fn, Mn, params = problem(name, 1, params_kind="large")
+    E, grad = g.bending(params)
+    Eo, go = O.bending(pb, params)
+    assert rel(E, Eo) <= 1e-10, (E, Eo)
+    assert rel_l2(grad, go) <= 1e-10
+    g.close()
+
+
+def _node_coords(shape, delta, is2d):
+    nd, Gz, Gy, Gx = shape
+    xs = [(np.arange(n) - 1.0) * d for n, d in zip((Gx, Gy, Gz), delta)]
+    if is2d:
+        xs[2] = np.zeros(1)
+    return np.meshgrid(xs[2], xs[1], xs[0], indexing="ij")[::-1]
+
+
+def test_bending_full_size_properties():
+    """C5 at its full size: quadratic-form identity phi.grad = 2 C_p, affine -> 0,
+    and the closed forms u = x^2 -> 4, u = y*z -> 2 (B-spline reproduction)."""
+    cfg = synth.config("C5")
+    F, M = synth.make_pair("C5", 1, cfg["dims"])
+    g = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    delta = [c / s for c, s in zip(cfg["control_mm"], cfg["spacing"])]
+    params = synth.make_params(g.params_shape, "large", 1)
+    E, grad = g.bending(params)
+    assert E > 0 and float((params * grad).sum()) == pytest.approx(2 * E, rel=1e-10)
+    X, Y, Z = _node_coords(g.params_shape, delta, False)
+    zero = np.zeros_like(X)
+    E, _ = g.bending(np.stack([0.3 * X - 0.2 * Y + 0.1 * Z + 2, 0.5 * Z, zero - 1]), want_grad=False)
+    assert abs(E) < 1e-10   # node coordinates reach ~500: rounding of phi^2-sized sums
+    E, _ = g.bending(np.stack([X * X - delta[0] ** 2 / 3, zero, zero]), want_grad=False)
+    assert E == pytest.approx(4.0, rel=1e-9)
+    E, _ = g.bending(np.stack([zero, zero, Y * Z]), want_grad=False)
+    assert E == pytest.approx(2.0, rel=1e-9)
+    g.close()
+
+
+def _check_report(g, x, rep, w_p):
+    D, _ = g.eval(x, want_grad=False)
+    E, _ = g.bending(x, want_grad=False)
+    assert rel(D, rep["final_value"]) <= 1e-5
+    assert rel(E, rep["final_penalty"]) <= 1e-9 or abs(E - rep["final_penalty"]) < 1e-15
+    assert rep["final_cost"] == pytest.approx(rep["final_value"] + w_p * rep["final_penalty"], rel=1e-12)
+    assert rep["final_cost"] <= rep["initial_cost"]
+    assert rep["evaluations"] >= rep["iterations"] + 1
+    assert rep["gradient_evaluations"] <= rep["evaluations"]
+
+
+@pytest.mark.parametrize("name,w_p", [("C1", 0.1), ("C3", 0.1), ("C4", 30.0)])
+def test_register_reduces_cost(name, w_p):
+    g, pb, Fn, Mn, _ = problem(name, 1)
+    x, rep = g.register(None, w_p=w_p, max_iter=40)
+    assert rep["status_name"] in ("converged", "stable", "max_iter", "line_search_failed")
+    assert rep["iterations"] >= 1
+    assert rep["final_cost"] < rep["initial_cost"] * (1 - 1e-3), rep
+    _check_report(g, x, rep, w_p)
+    g.close()
+
+
+def test_register_identity_stays_at_identity():
+    """F = M: the identity is (up to the Parzen smoothing) optimal; the result stays
+    within 0.1 voxel mean displacement (SPEC pipeline example)."""
+    cfg = synth.config("C3", REDUCED["C3"])
+    F, _ = synth.make_pair("C3", 1, cfg["dims"])
+    g = S.Srwcr(F, F.copy(), cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    x, rep = g.register(None, w_p=0.1, max_iter=30)
+    assert np.abs(x).mean() < 0.1, np.abs(x).mean()
+    assert rep["final_cost"] <= rep["initial_cost"]
+    g.close()
+
+
+def test_register_recovers_translation():
+    """A rigid shift of 1.5 voxels along x is a displacement the FFD represents exactly
+    (constant field); registration must bring D well below its starting value and
+    move the mean x-displacement toward the shift."""
+    cfg = synth.config("C3", REDUCED["C3"])
+    F, _ = synth.make_pair("C3", 1, cfg["dims"])
+    # moving(x) = fixed(x - s) : the correct displacement is u_x = +s ... sampled
+    # M(x + u) = F(x + u - s) = F(x) at u = s
+    s = 1.5
+    xi = np.arange(F.shape[2], dtype=np.float64) - s
+    i0 = np.clip(np.floor(xi).astype(int), 0, F.shape[2] - 1)
+    i1 = np.clip(i0 + 1, 0, F.shape[2] - 1)
+    t = (xi - np.floor(xi)).astype(np.float32)
+    M = (F[:, :, i0] * (1 - t) + F[:, :, i1] * t).astype(np.float32)
+    g = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    D0, _ = g.eval(np.zeros(g.params_shape), want_grad=False)
+    x, rep = g.register(None, w_p=0.1, max_iter=60)
+    _check_report(g, x, rep, 0.1)
+    assert rep["final_value"] < 0.7 * D0, (D0, rep)
+    ux = x[0, 1:-1, 1:-1, 1:-1].mean()
+    assert 0.5 < ux < 2.5, ux
+    g.close()
+
+
+def test_register_argument_errors():
+    g, *_ = problem("C1", 1)
+    with pytest.raises(S.SrwcrError):
+        g.register(None, ftol=0.95, wolfe=0.9)
+    with pytest.raises(S.SrwcrError):
+        g.register(None, m=0)
+    with pytest.raises(TypeError):
+        g.register(None, bogus=1)
+    g.close()

@@ -18,7 +18,14 @@ else:
     F, M = synth.make_pair(name, 1); np.savez(cache, F=F, M=M)
 cfg = synth.config(name)
 g = S.Srwcr(torch.from_numpy(F).cuda(), torch.from_numpy(M).cuda(), cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
-p = torch.from_numpy(synth.make_params(g.params_shape, phi, 1)).cuda()
+if phi == "reg":   # an L-BFGS iterate (large, irregular displacements)
+    x, _ = g.register(None, max_iter=20)
+    np.save(f"/tmp/srwcr_{name}_reg.npy", x)
+    p = torch.from_numpy(x).cuda()
+elif phi == "regload":
+    p = torch.from_numpy(np.load(f"/tmp/srwcr_{name}_reg.npy")).cuda()
+else:
+    p = torch.from_numpy(synth.make_params(g.params_shape, phi, 1)).cuda()
 gr = torch.empty_like(p)
 g.set_timing(True)
 for _ in range(3): g.eval(p, grad=gr)
