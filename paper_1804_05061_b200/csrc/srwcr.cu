@@ -68,6 +68,7 @@ struct srwcr_ctx {
     std::vector<float4> h_sw[3];
     // device
     float *F = nullptr, *M = nullptr, *phi = nullptr, *phimax = nullptr;
+    float4 *MG = nullptr;  // pass 1 -> pass 2: (m, dM/dy) per slab voxel
     double *params64 = nullptr, *grad64 = nullptr;
     const double *cur_params = nullptr;  // device fp64 params of the current evaluation
     int *cb[3]{}, *sb[3]{};
@@ -226,6 +227,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     a.p64 = c->cur_params;
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
     a.phimax = c->phimax; a.pmcs = (long long)c->g.Gx * c->g.Gy * c->g.Gz;
+    a.MG = c->MG; a.mgz0 = (int)c->z0;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
@@ -240,6 +242,7 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     const int n = full ? c->nitems_full : c->nitems;
     a.items = full ? c->items_full : c->items;
     a.itemw = full ? c->itemw_full : c->itemw;
+    if (full) a.MG = nullptr;   // whole-volume create-time passes: no (m, dM/dy) output
     if (n == 0) return SRWCR_OK;
     a.pf = c->pf1;
     if (c->W > 16) {
@@ -264,7 +267,9 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     if (c->nitems2 == 0) return SRWCR_OK;
     a.W = c->W2;
     a.pf = c->pf2;
-    k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+    if (c->W2 > 21) k_pass2<XV, 1024><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+    else if (c->W2 > 16) k_pass2<XV, 672><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+    else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
@@ -278,6 +283,8 @@ static srwcr_status set_smem_t(srwcr_ctx *c) {
     CK(cudaFuncSetAttribute(k_pass1<XV, false, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
     CK(cudaFuncSetAttribute(k_pass1<XV, true, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
     CK(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+    CK(cudaFuncSetAttribute(k_pass2<XV, 672>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+    CK(cudaFuncSetAttribute(k_pass2<XV, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
     return SRWCR_OK;
 }
 static srwcr_status set_smem(srwcr_ctx *c) {
@@ -441,11 +448,12 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         for (auto &r : xr) minw = std::min(minw, r.second);
         c->XV = minw >= 48 ? 2 : 1;
         if (const char *e = getenv("SRWCR_XV")) c->XV = std::min(c->XV, std::max(1, atoi(e)));
-        c->XV2 = 1;
+        c->XV2 = c->XV;  // pass 2 amortises its per-line gamma/alpha/beta contractions over XV2 x 32 voxels
         if (const char *e = getenv("SRWCR_XV2")) c->XV2 = std::min(c->XV, std::max(1, atoi(e)));
     }
     const int xmax = 32 * c->XV;
     int ymax = 64, zmax = 64;
+    const bool yfirst = true;  // pass 1: split rows before z (longer z-marches), measured ~1% on C5
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
@@ -471,7 +479,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         const bool small = (long long)items.size() < 6LL * nsm;
         const bool big_np = npmax > 12288;
         if ((small || big_np) && (ymax > 16 || zmax > 4)) {
-            if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
+            if (yfirst && ymax > 16) ymax /= 2;
+            else if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
             else if (ymax > 16) ymax /= 2;
             else zmax /= 2;
             continue;
@@ -479,8 +488,23 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         break;
     }
     build_items(0, g.nz, items_full, xmax);
-    npmax = 0;
-    build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
+    // pass 2 has its own (narrower) x-chunks, hence more items: keep its z-marches as
+    // long as the load balance allows (fewer FFD-layer loads and retires per voxel)
+    ymax = 64;
+    zmax = 64;
+    for (;;) {
+        items2.clear();
+        npmax = 0;
+        build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
+        const bool small = (long long)items2.size() < 6LL * nsm;
+        if ((small || npmax > 16384) && (ymax > 16 || zmax > 4)) {
+            if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
+            else if (ymax > 16) ymax /= 2;
+            else zmax /= 2;
+            continue;
+        }
+        break;
+    }
     if (npmax > 16384) return fail(c, SRWCR_EINVAL, "control lattice too fine for the node window (%zu)", npmax);
     c->nitems = (int)items.size();
     c->nitems_full = (int)items_full.size();
@@ -567,6 +591,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     const long long RB = c->R * g.B;
     CK(cudaMalloc(&c->phi, sizeof(float) * c->nint));
     CK(cudaMalloc(&c->phimax, sizeof(float) * c->nint * 2));  // result + scratch
+    CK(cudaMemset(c->phimax, 0, sizeof(float) * c->nint * 2));
+    CK(cudaMalloc(&c->MG, sizeof(float4) * (size_t)std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy)));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->SQ, sizeof(double) * stats_count(c)));
@@ -588,18 +614,19 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // shared memory and warps per CTA of each pass: the largest W in {16, 12, 8, 6, 4} that fits
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-    const int Wc[6] = {24, 16, 12, 8, 6, 4};
-    int w1max = 16;
+    const int Wc[8] = {32, 24, 20, 16, 12, 8, 6, 4};
+    int w1max = 16, w2max = 16;
     if (const char *e = getenv("SRWCR_W1")) w1max = atoi(e);
+    if (const char *e = getenv("SRWCR_W2")) w2max = atoi(e);
     c->W = c->W2 = 0;
     for (int W : Wc) {
         const size_t s1 = sizeof(int) * (((size_t)W * c->S * LTS + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * 32 +
                           sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16;
-        if (!c->W && W <= w1max && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
+        if (!c->W && W <= w1max && W != 32 && W != 20 && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
         const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (GYS + 1) +
                           sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192) + ((g.B + 15) & ~15) +
                           sizeof(float) * npmax;
-        if (!c->W2 && W <= 16 && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
+        if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
     }
     if (c->W == 0 || c->W2 == 0) return fail(c, SRWCR_EINVAL, "shared memory too small for %d bins / %d slots", g.B, c->S);
     TRY(set_smem(c));
@@ -694,7 +721,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
     CKL();
-    {   // tap-window max |phi_c| for pass 2's rounding bound (x, y into scratch, z into phimax)
+    {   // tap-window max |phi_c| for pass 1's rounding bound (x, y into scratch, z into phimax)
         float *scr = c->phimax + c->nint;
         k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, c->phimax, c->g);
         CKL();
@@ -868,7 +895,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
+    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma};
     for (void *p : bufs)

@@ -63,8 +63,10 @@ struct PassArgs {
     double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
-    const float *phimax;        // pass 2: [3][Gz][Gy][Gx] max |phi_c| over the tap window
+    const float *phimax;        // pass 1: [3][Gz][Gy][Gx] max |phi_c| over the tap window
     long long pmcs;             //         component stride of phimax
+    float4 *MG;                 // pass 1 out / pass 2 in: per slab voxel (m, dM/dy) -- m < 0
+    int mgz0;                   //   encodes -1 - m for voxels that need the fp64 exact path
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
     double *grad;               // pass 2 out: [ndim][GzExt][Gy][Gx] (fp64)
@@ -83,6 +85,16 @@ __device__ __forceinline__ float ld_stream(const float *p) {
     float v;
     asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
     return v;
+}
+__device__ __forceinline__ float4 ld_stream4(const float4 *p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p));
+    return v;
+}
+// streaming store (written once, read once by the next pass)
+__device__ __forceinline__ void st_stream4(float4 *p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 constexpr int PFD = 4;          // z-slices of look-ahead of the L2 prefetches
@@ -246,7 +258,18 @@ __device__ __forceinline__ int axis_fast(int i, float u, int nm2, float &t) {
     t = c < 0 ? 0.f : (c > nm2 ? 1.f : tt);
     return min(max(c, 0), nm2);
 }
-// same with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
+// branch-free, with the clamp flag of reading c2 and the near-integer flag (below)
+__device__ __forceinline__ int axis_fast_fl(int i, float u, int nm2, float tol, float &t, bool &cl, bool &near) {
+    const float fu = floorf(u);
+    const int c = i + (int)fu;
+    const float tt = u - fu;
+    const bool lo = c < 0, hi = c > nm2;
+    t = lo ? 0.f : (hi ? 1.f : tt);
+    cl = lo || (hi && !(c == nm2 + 1 && tt == 0.f));
+    near = fabsf(u - rintf(u)) < tol && (!lo || c == -1) && (!hi || c == nm2 + 1);
+    return min(max(c, 0), nm2);
+}
+// same (branchy) with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
 // flag telling that the fp32 position lies within tol of an integer, i.e. of a cell or
 // clamp boundary where the derivative of the interpolant jumps.  tol bounds |u32 - u64|
 // (see k_pass2); tol = 0 (all tap nodes of the component at rest) never flags.
@@ -392,10 +415,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
                     const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
                     const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
+                    // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
+                    // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
+                    // The max is over this voxel's own 4x4x4 tap window (k_window_max).
+                    const int wo = (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0;
+                    const float tlx = 4e-6f * __ldg(a.phimax + wo), tly = 4e-6f * __ldg(a.phimax + a.pmcs + wo),
+                                tlz = 4e-6f * __ldg(a.phimax + 2 * a.pmcs + wo);
                     float tx, ty, tz;
-                    const int ccx = axis_fast(xv[v], ux, nxm2, tx);
-                    const int ccy = axis_fast(y, uy, nym2, ty);
-                    const int ccz = axis_fast(z, uz, nzm2, tz);
+                    bool clx, cly, clz, nrx, nry, nrz;
+                    const int ccx = axis_fast_fl(xv[v], ux, nxm2, tlx, tx, clx, nrx);
+                    const int ccy = axis_fast_fl(y, uy, nym2, tly, ty, cly, nry);
+                    const int ccz = axis_fast_fl(z, uz, nzm2, tlz, tz, clz, nrz);
                     const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
                     const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
                     const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
@@ -413,6 +443,25 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     const int n = min(max((int)floorf(m), 0), g.L - 1);
                     float w1l, w1;
                     parzen_pair(m - (float)n, w1l, w1);
+                    {   // (m, dM/dy) for pass 2 (Eq 16-17 chain); the fp64 path is needed where
+                        // the per-voxel derivative jumps: a sample coordinate within rounding of
+                        // an integer (cell / clamp boundary) or m within 5e-5 of an integer (the
+                        // Parzen kink, reading c4) unless the cell is flat (m exact in fp32)
+                        float dgx = lerpf(lerpf(c100 - c000, c110 - c010, ty), lerpf(c101 - c001, c111 - c011, ty), tz);
+                        float dgy = lerpf(lerpf(c010 - c000, c110 - c100, tx), lerpf(c011 - c001, c111 - c101, tx), tz);
+                        float dgz = f1 - f0;
+                        dgx = clx ? 0.f : dgx;
+                        dgy = cly ? 0.f : dgy;
+                        dgz = (clz || dzo == 0) ? 0.f : dgz;
+                        const float fm = m - (float)n;
+                        const bool ex = nrx || nry || (nrz && dzo != 0) ||
+                                        ((fm < 5e-5f || fm > 1.0f - 5e-5f) &&
+                                         !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 &&
+                                           c101 == c000 && c011 == c000 && c111 == c000));
+                        if (a.MG && lane + 32 * v < it.xlen)
+                            st_stream4(a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx + xv[v],
+                                       make_float4(ex ? -1.0f - m : m, dgx, dgy, dgz));
+                    }
                     const float A = ((float)n - shc[a0[v]]) + w1;      // g1 - c_a0
                     const float Ab = ((float)n - cI) + w1;            // g1 - cI
                     const float q = fmaf(Ab, Ab, w1 * w1l);           // sum_b (b - cI)^2 h(b - m)
@@ -771,8 +820,8 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 // y-taps once per row (GY[bin][xtap] = float4 over the z-taps); per line the bins the
 // line touches are contracted over z cooperatively (GZ[bin] = float4 over the x-taps),
 // so a voxel reads two float4.
-template <int XV>
-__global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
+template <int XV, int MAXT = 512>
+__global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
     const int B = g.B, W = a.W;
@@ -845,10 +894,7 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
         const int prev = __shfl_up_sync(FULL, cbx[v], 1);
         head[v] = lane == 0 || prev != cbx[v];
     }
-    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
-    const int dzo = g.nz > 1 ? nxy : 0, nzl = g.nz - 1;
-    const bool is2d = g.nz == 1;
-    const float *__restrict__ Mv = a.M;
+    const int nx = g.nx, nxy = (int)g.nxy;
     float *rbw = RB + warp * 192;
     float4 *GYw = GY + warp * GB * GYS;
     float4 *GZw = GZ + warp * GB;
@@ -878,13 +924,11 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
         __syncwarp();
 
         int gzl = zn0;
-        float U[4][XV][3], Ad[4][XV][3];
+        float Ad[4][XV][3];
 #pragma unroll
-        for (int n = 0; n < 4; ++n) {
-            ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+        for (int n = 0; n < 4; ++n)
 #pragma unroll
             for (int v = 0; v < XV; ++v) Ad[n][v][0] = Ad[n][v][1] = Ad[n][v][2] = 0.f;
-        }
 
         // retire control layer gzr with this lane's accumulated adjoints R[v][3]
         auto retire = [&](int gzr, const float (&R)[XV][3]) {
@@ -940,15 +984,15 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
 #pragma unroll
                     for (int v = 0; v < XV; ++v)
 #pragma unroll
-                        for (int c = 0; c < 3; ++c) { U[n][v][c] = U[n + 1][v][c]; Ad[n][v][c] = Ad[n + 1][v][c]; }
+                        for (int c = 0; c < 3; ++c) Ad[n][v][c] = Ad[n + 1][v][c];
 #pragma unroll
                 for (int v = 0; v < XV; ++v) Ad[3][v][0] = Ad[3][v][1] = Ad[3][v][2] = 0.f;
                 ++gzl;
-                ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
             }
             const float4 cwz = a.t.cw[2][z];
             const float4 wz = a.t.sw[2][z];
             const float *__restrict__ Fz = Frow + z * nxy;
+            const float4 *__restrict__ MGz = a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx;
             // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
             float t = f4(wz, lane & 3) * abY;
             t += __shfl_xor_sync(FULL, t, 1);
@@ -975,40 +1019,17 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
             __syncwarp();
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
-                const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
-                const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
-                // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi and
-                // weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that
-                const int wo = (gzl * g.Gy + cby) * g.Gx + cbx[v];
-                const float tlx = 4e-6f * __ldg(a.phimax + wo), tly = 4e-6f * __ldg(a.phimax + a.pmcs + wo),
-                            tlz = 4e-6f * __ldg(a.phimax + 2 * a.pmcs + wo);
-                float tx, ty, tz;
-                bool clx, cly, clz, nrx, nry, nrz;
-                const int ccx = axis_fast_cl(xv[v], ux, nxm2, tlx, tx, clx, nrx);
-                const int ccy = axis_fast_cl(y, uy, nym2, tly, ty, cly, nry);
-                const int ccz = axis_fast_cl(z, uz, nzm2, tlz, tz, clz, nrz);
-                const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
-                const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
-                const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
-                {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
-                    const int po = (min(ccz + PFD, nzl) - ccz) * nxy;
-                    prefetch_l2(Fz + PFD * nxy * (z + PFD <= nzl) + xv[v]);
-                    prefetch_l2(Mv + o0 + po);
-                    prefetch_l2(Mv + o1 + po);
-                    prefetch_l2(Mv + o2 + po);
-                    prefetch_l2(Mv + o3 + po);
+                // (m, dM/dy) of this voxel from pass 1 (same fp32 arithmetic); m < 0 flags the
+                // voxels whose per-voxel derivative is decided by the fp64 definition
+                const float4 mg = ld_stream4(MGz + xv[v]);
+                {
+                    const int pz = PFD * nxy * (z + PFD < it.z0 + it.zlen);
+                    prefetch_l2(MGz + pz + xv[v]);
+                    prefetch_l2(Fz + pz + xv[v]);
                 }
-                const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
-                const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
-                const float f0 = lerpf(e00, e10, ty), f1 = lerpf(e01, e11, ty);
-                const float m = lerpf(f0, f1, tz);
-                float dgx = lerpf(lerpf(c100 - c000, c110 - c010, ty), lerpf(c101 - c001, c111 - c011, ty), tz);
-                float dgy = lerpf(lerpf(c010 - c000, c110 - c100, tx), lerpf(c011 - c001, c111 - c101, tx), tz);
-                float dgz = f1 - f0;
-                dgx = clx ? 0.f : dgx;
-                dgy = cly ? 0.f : dgy;
-                dgz = (clz || is2d) ? 0.f : dgz;
+                float m = mg.x, dgx = mg.y, dgy = mg.z, dgz = mg.w;
+                const bool ex = m < 0.f;
+                m = ex ? -1.0f - m : m;
                 const int gk = gmap[a0[v]];
                 const float4 G0 = GZw[gk], G1 = GZw[gk + 1];
                 const float4 sw = swx[v];
@@ -1020,13 +1041,7 @@ __global__ void __launch_bounds__(512, 1) k_pass2(PassArgs a) {
                 float g1p, c2;
                 if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
                 else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
-                // discontinuities of the per-voxel derivative: decide them in fp64.  A flat
-                // cell (8 equal corners) gives m = that corner exactly in fp32 and fp64, so
-                // its Parzen-kink side needs no fp64 re-evaluation (flat background).
-                if (nrx || nry || (nrz && !is2d) ||
-                    ((fm < 5e-5f || fm > 1.0f - 5e-5f) &&
-                     !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 && c101 == c000 &&
-                       c011 == c000 && c111 == c000)))
+                if (ex)
                     exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
                                  cbx[v], cby, bz, a.t.cw64[0][xv[v]], a.t.cw64[1][y], a.t.cw64[2][z], xv[v], y, z,
                                  dgx, dgy, dgz, g1p, c2);
@@ -1082,7 +1097,7 @@ __global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict_
 
 // max of |phi_c| over the 4 nodes [k, k+3] along axis AX (clipped to the grid), for all
 // 3 components: three passes give the max over each voxel's 4x4x4 tap window keyed by
-// its base node -- the scale of pass 2's rounding bound (k_pass2)
+// its base node -- the scale of pass 1's rounding bound of u (k_pass1)
 template <int AX>
 __global__ void k_window_max(const float *__restrict__ in, float *__restrict__ out, Geo g) {
     const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane;
