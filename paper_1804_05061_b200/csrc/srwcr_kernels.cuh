@@ -266,7 +266,9 @@ __device__ __forceinline__ int axis_fast_fl(int i, float u, int nm2, float tol, 
     const bool lo = c < 0, hi = c > nm2;
     t = lo ? 0.f : (hi ? 1.f : tt);
     cl = lo || (hi && !(c == nm2 + 1 && tt == 0.f));
-    near = fabsf(u - rintf(u)) < tol && (!lo || c == -1) && (!hi || c == nm2 + 1);
+    // (far outside the volume the flag may be raised needlessly: harmless, the fp64 path
+    // then confirms the clamp)
+    near = fabsf(u - rintf(u)) < tol;
     return min(max(c, 0), nm2);
 }
 // same (branchy) with the clamp flag of reading c2 (derivative 0 along a clamped axis) and a
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
                     const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
                     const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
-                    {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
+                    if (a.pf & 1) {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
                         const int po = (min(ccz + PFD, nzl) - ccz) * nxy;
                         prefetch_l2(Fz + PFD * nxy * (z + PFD <= nzl) + xv[v]);
                         prefetch_l2(Mv + o0 + po);
@@ -437,8 +439,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         prefetch_l2(Mv + o2 + po);
                         prefetch_l2(Mv + o3 + po);
                     }
-                    const float f0 = lerpf(lerpf(c000, c100, tx), lerpf(c010, c110, tx), ty);
-                    const float f1 = lerpf(lerpf(c001, c101, tx), lerpf(c011, c111, tx), ty);
+                    const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
+                    const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
+                    const float f0 = lerpf(e00, e10, ty);
+                    const float f1 = lerpf(e01, e11, ty);
                     const float m = lerpf(f0, f1, tz);
                     const int n = min(max((int)floorf(m), 0), g.L - 1);
                     float w1l, w1;
@@ -448,7 +452,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         // an integer (cell / clamp boundary) or m within 5e-5 of an integer (the
                         // Parzen kink, reading c4) unless the cell is flat (m exact in fp32)
                         float dgx = lerpf(lerpf(c100 - c000, c110 - c010, ty), lerpf(c101 - c001, c111 - c011, ty), tz);
-                        float dgy = lerpf(lerpf(c010 - c000, c110 - c100, tx), lerpf(c011 - c001, c111 - c101, tx), tz);
+                        float dgy = lerpf(e10 - e00, e11 - e01, tz);
                         float dgz = f1 - f0;
                         dgx = clx ? 0.f : dgx;
                         dgy = cly ? 0.f : dgy;
@@ -1022,7 +1026,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 // (m, dM/dy) of this voxel from pass 1 (same fp32 arithmetic); m < 0 flags the
                 // voxels whose per-voxel derivative is decided by the fp64 definition
                 const float4 mg = ld_stream4(MGz + xv[v]);
-                {
+                if (a.pf & 1) {
                     const int pz = PFD * nxy * (z + PFD < it.z0 + it.zlen);
                     prefetch_l2(MGz + pz + xv[v]);
                     prefetch_l2(Fz + pz + xv[v]);
