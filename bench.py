@@ -221,14 +221,14 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     l0 = g.stats()["launches_total"]
-    p1, p2, cb = [], [], []
+    p1, p2, cb, pp = [], [], [], []
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         e0.record(stream)
         for _ in range(args.steps):
             D, _ = g.eval(params, grad=grad)
             st = g.stats()
-            p1.append(st["ms_pass1"]); p2.append(st["ms_pass2"]); cb.append(st["ms_combine"])
+            p1.append(st["ms_pass1"]); p2.append(st["ms_pass2"]); cb.append(st["ms_combine"]); pp.append(st["ms_prep"])
         e1.record(stream)
         e1.synchronize()
     torch.cuda.synchronize()
@@ -298,7 +298,7 @@ def main():
                        "parallelism": f"z-slab x{ws}", "l2": "inputs 671 MB > 126 MB L2 (no flush needed)"
                        if args.config in ("C4", "C5") else "inputs may be L2-resident (no flush)"},
             "gvoxel_per_s": evals * nvox / 1e9,
-            "pass_ms": {"pass1": t1, "combine": statistics.mean(cb), "pass2": t2},
+            "pass_ms": {"prep": statistics.mean(pp), "pass1": t1, "combine": statistics.mean(cb), "pass2": t2},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                          "bytes_per_launch": bdom, "pass1_frac": bytes_p1 / (t1 * 1e-3) / 1e9 / peak,
@@ -307,7 +307,8 @@ def main():
             "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": int(params_np.nbytes),
                     "d2h_bytes_per_step": int(params_np.nbytes) + 8},
             "gpu_launches": int(launches),
-            "decomposition": {k: g.stats()[k] for k in ("warps_per_cta", "slot_capacity", "voxels_per_lane", "items")},
+            "decomposition": {k: g.stats()[k] for k in ("warps_per_cta", "slot_capacity", "voxels_per_lane", "items",
+                                                        "warps_per_cta2", "items2")},
             "clocks": clk.summary(),
             "D": D,
         }

@@ -207,11 +207,13 @@ srwcr_status srwcr_debug_dump(srwcr_ctx *ctx, int32_t what, void *out, size_t by
 typedef struct {
     int64_t launches_total;     /* kernels launched by this context since creation */
     int32_t launches_per_eval;  /* kernels in one srwcr_eval (graph nodes that are kernels) */
-    float ms_pass1, ms_combine, ms_pass2, ms_total;
+    float ms_pass1, ms_combine, ms_pass2, ms_total;  /* pass 1 = the k_pass1 launch alone */
     int32_t warps_per_cta;      /* decomposition chosen at create */
     int32_t slot_capacity;      /* max distinct fixed bins of one work item */
     int32_t voxels_per_lane;    /* 1 or 2 along x */
     int32_t items;              /* CTAs per pass on this rank */
+    float ms_prep;              /* params -> fp32 and tap-window max kernels before pass 1 */
+    int32_t warps_per_cta2, items2;  /* pass 2's decomposition */
 } srwcr_stats;
 srwcr_status srwcr_set_timing(srwcr_ctx *ctx, int32_t enable);
 srwcr_status srwcr_get_stats(const srwcr_ctx *ctx, srwcr_stats *out);

@@ -88,7 +88,7 @@ struct srwcr_ctx {
     double Z = 0;
     size_t smem1 = 0, smem2 = 0;
     int segsteps = 0;
-    int pf1 = 0, pf2 = 1;                            // L2 prefetch per pass (SRWCR_PF1 / SRWCR_PF2)
+    int pf1 = 0, pf2 = 1;                            // L2 prefetch: pass 2 only (SRWCR_PF2; pass 1 measured no gain)
     ncclComm_t comm = nullptr;
     bool external_exchange = false;
     bool begun = false;
@@ -96,8 +96,8 @@ struct srwcr_ctx {
     int64_t launches = 0;
     int launches_per_eval = 0;
     bool timing = false;
-    cudaEvent_t ev[4]{};
-    float ms[4]{};
+    cudaEvent_t ev[5]{};  // pass1 start, pass1 end, combine end, pass2 end, prep start
+    float ms[5]{};
     double *pinned = nullptr;  // 2 doubles
     // bending energy / L-BFGS (srwcr_register.inc)
     double *bend_gram = nullptr;  // [3 axes][3 orders][Gmax][7] banded 1-D Gram matrices
@@ -359,7 +359,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->dev = o.device;
     CK(cudaSetDevice(c->dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    for (int i = 0; i < 4; ++i) CK(cudaEventCreate(&c->ev[i]));
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&c->ev[i]));
     CK(cudaMallocHost(&c->pinned, 4 * sizeof(double)));
 
     // per-axis tables (fp64 on host -> device), control and spatial lattices
@@ -718,7 +718,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
         pd = c->params64;
     }
     c->cur_params = pd;
-    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    if (c->timing) CK(cudaEventRecord(c->ev[4], c->stream));
     k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
     CKL();
     {   // tap-window max |phi_c| for pass 1's rounding bound (x, y into scratch, z into phimax)
@@ -731,6 +731,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
+    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
     TRY(launch_pass1(c, false));
     if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
     return SRWCR_OK;
@@ -755,7 +756,8 @@ static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, boo
         cudaEventElapsedTime(&c->ms[0], c->ev[0], c->ev[1]);
         cudaEventElapsedTime(&c->ms[1], c->ev[1], c->ev[2]);
         cudaEventElapsedTime(&c->ms[2], c->ev[2], c->ev[3]);
-        c->ms[3] = c->ms[0] + c->ms[1] + c->ms[2];
+        cudaEventElapsedTime(&c->ms[4], c->ev[4], c->ev[0]);
+        c->ms[3] = c->ms[4] + c->ms[0] + c->ms[1] + c->ms[2];
     }
     if (value) *value = c->pinned[0];
     if (c->pinned[1] < 0.5) {
@@ -881,6 +883,9 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->slot_capacity = c->S;
     out->voxels_per_lane = c->XV;
     out->items = c->nitems;
+    out->ms_prep = c->ms[4];
+    out->warps_per_cta2 = c->W2;
+    out->items2 = c->nitems2;
     return SRWCR_OK;
 }
 extern "C" srwcr_status srwcr_stream(const srwcr_ctx *c, void **stream) {
@@ -907,7 +912,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
         if (c->sb[i]) cudaFree(c->sb[i]);
         if (c->sw[i]) cudaFree(c->sw[i]);
     }
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < 5; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->dot_host) cudaFreeHost(c->dot_host);

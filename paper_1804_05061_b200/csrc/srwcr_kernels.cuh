@@ -367,7 +367,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     const int El_e = le == 0 ? El[0] : le == 1 ? El[1] : le == 2 ? El[2] : El[3];
     const float cI = it.cI;
     const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
-    const int dzo = g.nz > 1 ? nxy : 0, nzl = g.nz - 1;
+    const int dzo = g.nz > 1 ? nxy : 0;
     const float *__restrict__ Mv = a.M;
     __syncthreads();
 
@@ -385,8 +385,22 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
         for (int n = 0; n < 4; ++n) ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
         float bacc = 0.f;
         unsigned wmask[4] = {0u, 0u, 0u, 0u};
+        // F is software-pipelined one slice ahead (its DRAM latency is otherwise exposed:
+        // the bin a0 it decides gates the whole line's accumulation)
+        float Fnext[XV];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) Fnext[v] = ld_stream(Frow + it.z0 * nxy + xv[v]);
 
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
+            float Fcur[XV];
+            {
+                const int nz1 = z + 1 < it.z0 + it.zlen ? nxy : 0;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    Fcur[v] = Fnext[v];
+                    Fnext[v] = ld_stream(Frow + z * nxy + nz1 + xv[v]);
+                }
+            }
             const int bz = a.t.cb[2][z];
             while (gzl < bz) {                                   // slide the 4-layer window
 #pragma unroll
@@ -398,14 +412,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             }
             const float4 cwz = a.t.cw[2][z];
             const float4 wz = a.t.sw[2][z];
-            const float *__restrict__ Fz = Frow + z * nxy;
             int a0[XV], slot[XV];
             float lo[XV], hi[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
             float amax = 0.f;
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                const float Fv = ld_stream(Fz + xv[v]);
+                const float Fv = Fcur[v];
                 a0[v] = min((int)Fv, g.L - 1);
                 slot[v] = smap[a0[v]];
                 float hlo, hhi;
@@ -431,14 +444,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
                     const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
                     const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
-                    if (a.pf & 1) {   // L2 prefetch PFD slices ahead at the current u (clamped inside the volume)
-                        const int po = (min(ccz + PFD, nzl) - ccz) * nxy;
-                        prefetch_l2(Fz + PFD * nxy * (z + PFD <= nzl) + xv[v]);
-                        prefetch_l2(Mv + o0 + po);
-                        prefetch_l2(Mv + o1 + po);
-                        prefetch_l2(Mv + o2 + po);
-                        prefetch_l2(Mv + o3 + po);
-                    }
                     const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
                     const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
                     const float f0 = lerpf(e00, e10, ty);
@@ -997,6 +1002,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             const float4 wz = a.t.sw[2][z];
             const float *__restrict__ Fz = Frow + z * nxy;
             const float4 *__restrict__ MGz = a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx;
+            // issue this line's streaming loads first: their latency overlaps the per-line
+            // alpha/beta/gamma contractions below
+            float Fl[XV];
+            float4 mgl[XV];
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                Fl[v] = ld_stream(Fz + xv[v]);
+                mgl[v] = ld_stream4(MGz + xv[v]);
+            }
             // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
             float t = f4(wz, lane & 3) * abY;
             t += __shfl_xor_sync(FULL, t, 1);
@@ -1016,7 +1030,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             float hlo[XV], hhi[XV];
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                const float Fv = ld_stream(Fz + xv[v]);
+                const float Fv = Fl[v];
                 a0[v] = min((int)Fv, g.L - 1);
                 parzen_pair(Fv - (float)a0[v], hlo[v], hhi[v]);
             }
@@ -1025,7 +1039,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             for (int v = 0; v < XV; ++v) {
                 // (m, dM/dy) of this voxel from pass 1 (same fp32 arithmetic); m < 0 flags the
                 // voxels whose per-voxel derivative is decided by the fp64 definition
-                const float4 mg = ld_stream4(MGz + xv[v]);
+                const float4 mg = mgl[v];
                 if (a.pf & 1) {
                     const int pz = PFD * nxy * (z + PFD < it.z0 + it.zlen);
                     prefetch_l2(MGz + pz + xv[v]);
