@@ -88,7 +88,7 @@ struct srwcr_ctx {
     double Z = 0;
     size_t smem1 = 0, smem2 = 0;
     int segsteps = 0;
-    int pf1 = 0, pf2 = 1;                            // L2 prefetch: pass 2 only (SRWCR_PF2; pass 1 measured no gain)
+    int pf1 = 0, pf2 = 0;                            // software L2 prefetch: measured no gain once loads issue early
     ncclComm_t comm = nullptr;
     bool external_exchange = false;
     bool begun = false;
@@ -226,7 +226,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     }
     a.p64 = c->cur_params;
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
-    a.phimax = c->phimax; a.pmcs = (long long)c->g.Gx * c->g.Gy * c->g.Gz;
+    a.tolw = reinterpret_cast<const float4 *>(c->phimax);
     a.MG = c->MG; a.mgz0 = (int)c->z0;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
@@ -590,8 +590,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // buffers
     const long long RB = c->R * g.B;
     CK(cudaMalloc(&c->phi, sizeof(float) * c->nint));
-    CK(cudaMalloc(&c->phimax, sizeof(float) * c->nint * 2));  // result + scratch
-    CK(cudaMemset(c->phimax, 0, sizeof(float) * c->nint * 2));
+    // [0, 4G) float4 tolerances, [4G, 7G) and [7G, 10G) scratch of the window-max passes
+    CK(cudaMalloc(&c->phimax, sizeof(float) * (size_t)g.Gx * g.Gy * g.Gz * 10));
+    CK(cudaMemset(c->phimax, 0, sizeof(float) * (size_t)g.Gx * g.Gy * g.Gz * 10));
     CK(cudaMalloc(&c->MG, sizeof(float4) * (size_t)std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy)));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
@@ -721,13 +722,14 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     if (c->timing) CK(cudaEventRecord(c->ev[4], c->stream));
     k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
     CKL();
-    {   // tap-window max |phi_c| for pass 1's rounding bound (x, y into scratch, z into phimax)
-        float *scr = c->phimax + c->nint;
-        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, c->phimax, c->g);
+    {   // tap-window max |phi_c| for pass 1's rounding bound (x, y into scratch, z -> float4)
+        const size_t G = (size_t)c->g.Gx * c->g.Gy * c->g.Gz;
+        float *s1 = c->phimax + 4 * G, *s2 = c->phimax + 7 * G;
+        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, s1, c->g);
         CKL();
-        k_window_max<1><<<592, 256, 0, c->stream>>>(c->phimax, scr, c->g);
+        k_window_max<1><<<592, 256, 0, c->stream>>>(s1, s2, c->g);
         CKL();
-        k_window_max<2><<<592, 256, 0, c->stream>>>(scr, c->phimax, c->g);
+        k_window_max_z4<<<592, 256, 0, c->stream>>>(s2, reinterpret_cast<float4 *>(c->phimax), c->g);
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));

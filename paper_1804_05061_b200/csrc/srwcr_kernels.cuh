@@ -63,8 +63,7 @@ struct PassArgs {
     double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
-    const float *phimax;        // pass 1: [3][Gz][Gy][Gx] max |phi_c| over the tap window
-    long long pmcs;             //         component stride of phimax
+    const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 4e-6 max |phi_c| over the tap window (c = x,y,z)
     float4 *MG;                 // pass 1 out / pass 2 in: per slab voxel (m, dM/dy) -- m < 0
     int mgz0;                   //   encodes -1 - m for voxels that need the fp64 exact path
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
@@ -433,9 +432,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
                     // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
                     // The max is over this voxel's own 4x4x4 tap window (k_window_max).
-                    const int wo = (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0;
-                    const float tlx = 4e-6f * __ldg(a.phimax + wo), tly = 4e-6f * __ldg(a.phimax + a.pmcs + wo),
-                                tlz = 4e-6f * __ldg(a.phimax + 2 * a.pmcs + wo);
+                    const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
+                    const float tlx = tl.x, tly = tl.y, tlz = tl.z;
                     float tx, ty, tz;
                     bool clx, cly, clz, nrx, nry, nrz;
                     const int ccx = axis_fast_fl(xv[v], ux, nxm2, tlx, tx, clx, nrx);
@@ -1040,11 +1038,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 // (m, dM/dy) of this voxel from pass 1 (same fp32 arithmetic); m < 0 flags the
                 // voxels whose per-voxel derivative is decided by the fp64 definition
                 const float4 mg = mgl[v];
-                if (a.pf & 1) {
-                    const int pz = PFD * nxy * (z + PFD < it.z0 + it.zlen);
-                    prefetch_l2(MGz + pz + xv[v]);
-                    prefetch_l2(Fz + pz + xv[v]);
-                }
                 float m = mg.x, dgx = mg.y, dgy = mg.z, dgz = mg.w;
                 const bool ex = m < 0.f;
                 m = ex ? -1.0f - m : m;
@@ -1131,6 +1124,22 @@ __global__ void k_window_max(const float *__restrict__ in, float *__restrict__ o
         for (int d = 0; d < 4; ++d)
             if (k + d < G) m = fmaxf(m, fabsf(in[i + d * st]));
         out[i] = m;
+    }
+}
+
+// last (z) pass of the window max, all 3 components of a node into one float4, already
+// scaled to pass 1's tolerance 4e-6 max |phi_c|
+__global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict__ out, Geo g) {
+    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cs; i += (long long)gridDim.x * blockDim.x) {
+        const int k = (int)(i / plane);
+        float m[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int d = 0; d < 4; ++d)
+                if (k + d < g.Gz) m[c] = fmaxf(m[c], fabsf(in[c * cs + i + d * plane]));
+        out[i] = make_float4(4e-6f * m[0], 4e-6f * m[1], 4e-6f * m[2], 0.f);
     }
 }
 
