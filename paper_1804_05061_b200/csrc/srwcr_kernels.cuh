@@ -364,6 +364,23 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     }
     const int le = (lane & 7) >> 1;                               // fold lane's x-tap
     const int El_e = le == 0 ? El[0] : le == 1 ? El[1] : le == 2 ? El[2] : El[3];
+    // mixed-bin path: lane q = lane & 3 visits the x-taps in the rotated order (k + q) & 3,
+    // so runs of up to 4 neighbouring lanes with the same bin hit distinct line-table
+    // entries in each atomic instruction (same-address lanes serialise)
+    const int q4 = lane & 3;
+    float4 swr[XV];
+    int Elr[4];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        const float4 w = swx[v];
+        swr[v] = q4 == 0 ? w : q4 == 1 ? make_float4(w.y, w.z, w.w, w.x)
+                             : q4 == 2 ? make_float4(w.z, w.w, w.x, w.y) : make_float4(w.w, w.x, w.y, w.z);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int src = (k + q4) & 3;
+        Elr[k] = src == 0 ? El[0] : src == 1 ? El[1] : src == 2 ? El[2] : El[3];
+    }
     const float cI = it.cI;
     const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
     const int dzo = g.nz > 1 ? nxy : 0;
@@ -490,8 +507,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             }
             // ---- binned: line table
             float sc[4] = {1.f, 1.f, 1.f, 1.f}, isc_e = 1.f;
+            int EA = 0;
             if (!STATIC) {
-                const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(amax)) >> 23);
+                EA = (int)(__reduce_max_sync(FULL, __float_as_uint(amax)) >> 23);
 #pragma unroll
                 for (int l = 0; l < 4; ++l) sc[l] = exp2i(min(274 - El[l] - EA, 120));
                 isc_e = exp2i(-min(274 - El_e - EA, 120));
@@ -523,20 +541,34 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     if (STATIC) *reinterpret_cast<float *>(p) += tot;
                     else *p += __float2int_rn(tot * (ent < 2 ? sc[0] : ent < 4 ? sc[1] : ent < 6 ? sc[2] : sc[3]));
                 }
-            } else {
+            } else if (STATIC) {
 #pragma unroll
                 for (int v = 0; v < XV; ++v) {
-                    int *row = LTw + slot[v] * LTS;
+                    float *row = reinterpret_cast<float *>(LTw + slot[v] * LTS);
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
-                        if (STATIC) {
-                            atomicAdd(reinterpret_cast<float *>(row) + 2 * l, f4(swx[v], l) * lo[v]);
-                            atomicAdd(reinterpret_cast<float *>(row) + 2 * l + 1, f4(swx[v], l) * hi[v]);
-                        } else {
-                            const float ws = f4(swx[v], l) * sc[l];
-                            atomicAdd(row + 2 * l, __float_as_int(fmaf(lo[v], ws, 12582912.f)) - 0x4B400000);
-                            atomicAdd(row + 2 * l + 1, __float_as_int(fmaf(hi[v], ws, 12582912.f)) - 0x4B400000);
-                        }
+                        const int lr = (l + q4) & 3;
+                        atomicAdd(row + 2 * lr, f4(swr[v], l) * lo[v]);
+                        atomicAdd(row + 2 * lr + 1, f4(swr[v], l) * hi[v]);
+                    }
+                }
+            } else {
+                float scr[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) scr[k] = exp2i(min(274 - Elr[k] - EA, 120));
+                // lanes 4-7 (mod 8) also swap the channel order: 8 neighbouring lanes of one
+                // bin touch 8 distinct entries per instruction
+                const int chA = (lane >> 2) & 1;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    int *row = LTw + slot[v] * LTS + chA;
+                    const float va = chA ? hi[v] : lo[v], vb = chA ? lo[v] : hi[v];
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        const int lr = (l + q4) & 3;
+                        const float ws = f4(swr[v], l) * scr[l];
+                        atomicAdd(row + 2 * lr, __float_as_int(fmaf(va, ws, 12582912.f)) - 0x4B400000);
+                        atomicAdd(row + 2 * lr + 1 - 2 * chA, __float_as_int(fmaf(vb, ws, 12582912.f)) - 0x4B400000);
                     }
                 }
             }

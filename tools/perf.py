@@ -28,10 +28,15 @@ else:
     p = torch.from_numpy(synth.make_params(g.params_shape, phi, 1)).cuda()
 gr = torch.empty_like(p)
 g.set_timing(True)
-for _ in range(3): g.eval(p, grad=gr)
+def ev():
+    try:
+        return g.eval(p, grad=gr)[0]
+    except S.SrwcrError as e:   # ablation experiments may zero the statistics
+        return float("nan")
+for _ in range(3): ev()
 t1 = []; t2 = []; tt = []
 for _ in range(steps):
-    D, _ = g.eval(p, grad=gr); s = g.stats(); t1.append(s["ms_pass1"]); t2.append(s["ms_pass2"]); tt.append(s["ms_total"])
+    D = ev(); s = g.stats(); t1.append(s["ms_pass1"]); t2.append(s["ms_pass2"]); tt.append(s["ms_total"])
 s = g.stats()
 env = {k: v for k, v in os.environ.items() if k.startswith("SRWCR_")}
 print(json.dumps({"cfg": name, "phi": phi, "env": env, "pass1": float(np.median(t1)), "pass2": float(np.median(t2)),
