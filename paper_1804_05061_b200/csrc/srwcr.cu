@@ -454,6 +454,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     const int xmax = 32 * c->XV;
     int ymax = 64, zmax = 64;
     const bool yfirst = true;  // pass 1: split rows before z (longer z-marches), measured ~1% on C5
+    const bool yfirst2 = true; // pass 2 likewise (C5 pass 2 -7 %)
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
@@ -498,7 +499,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
         const bool small = (long long)items2.size() < 6LL * nsm;
         if ((small || npmax > 16384) && (ymax > 16 || zmax > 4)) {
-            if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
+            if (yfirst2 && ymax > 16) ymax /= 2;
+            else if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
             else if (ymax > 16) ymax /= 2;
             else zmax /= 2;
             continue;

@@ -919,9 +919,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
     for (int i = threadIdx.x; i < npsz; i += blockDim.x) NP[i] = 0.f;
     for (int i = threadIdx.x; i < W * 192; i += blockDim.x) RB[i] = 0.f;
 
-    bool lok[XV], head[XV];
+    bool lok[XV];
     int xv[XV], relx[XV], cbx[XV];
-    float4 cwx[XV], swx[XV];
+    float4 cwx[XV], swx[XV], cwr[XV];
+    const int q4 = lane & 3;
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
         lok[v] = lane + 32 * v < it.xlen;
@@ -930,8 +931,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
         relx[v] = cbx[v] - xn0;
         cwx[v] = a.t.cw[0][xv[v]];
         swx[v] = a.t.sw[0][xv[v]];
-        const int prev = __shfl_up_sync(FULL, cbx[v], 1);
-        head[v] = lane == 0 || prev != cbx[v];
+        const float4 w = cwx[v];
+        cwr[v] = q4 == 0 ? w : q4 == 1 ? make_float4(w.y, w.z, w.w, w.x)
+                             : q4 == 2 ? make_float4(w.z, w.w, w.x, w.y) : make_float4(w.w, w.x, w.y, w.z);
     }
     const int nx = g.nx, nxy = (int)g.nxy;
     float *rbw = RB + warp * 192;
@@ -971,38 +973,41 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
 
         // retire control layer gzr with this lane's accumulated adjoints R[v][3]
         auto retire = [&](int gzr, const float (&R)[XV][3]) {
+            // x-contraction across lanes into the row buffer as int32 fixed point (native
+            // ATOMS.ADD): 2^(EA-126) bounds max |R| over the warp, so |w R 2^ks| < 2^22
+            // (exact magic-number conversion) and a node's <= 32 contributions stay < 2^27.
+            // Lane q = lane & 3 visits the x-taps in rotated order so neighbouring lanes of
+            // one control cell hit distinct nodes in each atomic instruction.
+            float mx = 0.f;
+#pragma unroll
+            for (int v = 0; v < XV; ++v)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) mx = fmaxf(mx, fabsf(R[v][c]));
+            const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(mx)) >> 23);
+            if (EA == 0) return;   // all adjoints zero (or denormal): nothing to retire
+            const int ks = min(148 - EA, 120);
+            const float sc = exp2i(ks);
+            int *rbi = reinterpret_cast<int *>(rbw);
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                float val[4][3];
-#pragma unroll
-                for (int l = 0; l < 4; ++l)
-#pragma unroll
-                    for (int c = 0; c < 3; ++c) val[l][c] = f4(cwx[v], l) * R[v][c];
-                for (int st = 0, off = 1; st < a.segsteps; ++st, off <<= 1) {
-                    const int nb = __shfl_down_sync(FULL, cbx[v], off);
-                    const bool same = (lane + off < 32) && nb == cbx[v];
-#pragma unroll
-                    for (int l = 0; l < 4; ++l)
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) {
-                            const float t = __shfl_down_sync(FULL, val[l][c], off);
-                            if (same) val[l][c] += t;
-                        }
-                }
+                const float R0 = R[v][0] * sc, R1 = R[v][1] * sc, R2 = R[v][2] * sc;
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {
-                    if (head[v])
-#pragma unroll
-                        for (int c = 0; c < 3; ++c) rbw[c * 64 + relx[v] + l] += val[l][c];
-                    __syncwarp();
+                    const int nd = relx[v] + ((l + q4) & 3);
+                    const float w = f4(cwr[v], l);
+                    atomicAdd(rbi + nd, __float_as_int(fmaf(w, R0, 12582912.f)) - 0x4B400000);
+                    atomicAdd(rbi + 64 + nd, __float_as_int(fmaf(w, R1, 12582912.f)) - 0x4B400000);
+                    atomicAdd(rbi + 128 + nd, __float_as_int(fmaf(w, R2, 12582912.f)) - 0x4B400000);
                 }
             }
+            __syncwarp();
+            const float isc = exp2i(-ks);
             // y-contraction of the row buffer into the CTA node window
             const int lz = gzr - zn0;
             for (int i = lane; i < 3 * nxn; i += 32) {
                 const int c = i / nxn, gxl = i - c * nxn;
-                const float rv = rbw[c * 64 + gxl];
-                rbw[c * 64 + gxl] = 0.f;
+                const float rv = (float)rbi[c * 64 + gxl] * isc;
+                rbi[c * 64 + gxl] = 0;
                 if (rv != 0.f) {
 #pragma unroll
                     for (int mm = 0; mm < 4; ++mm) {
