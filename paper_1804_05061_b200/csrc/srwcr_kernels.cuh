@@ -521,7 +521,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             bool same = true;
 #pragma unroll
             for (int v = 0; v < XV; ++v) same = same && a0[v] == af;
-            if (__all_sync(FULL, same)) {
+            const bool uniform = __all_sync(FULL, same);
+            if (uniform) {
                 float vv[8];
 #pragma unroll
                 for (int l = 0; l < 4; ++l) {
@@ -535,11 +536,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     vv[2 * l + 1] = sh;
                 }
                 const float tot = halving8(vv, lane);
-                if ((lane & 3) == 0) {
+                if ((lane & 3) == 0) {   // one bin: straight into the column table (no line table, no fold)
                     const int ent = lane >> 2;
-                    int *p = LTw + slot[0] * LTS + ent;
-                    if (STATIC) *reinterpret_cast<float *>(p) += tot;
-                    else *p += __float2int_rn(tot * (ent < 2 ? sc[0] : ent < 4 ? sc[1] : ent < 6 ? sc[2] : sc[3]));
+                    float4 *kp = reinterpret_cast<float4 *>(Kw + slot[0] * 32 + ent * 4);
+                    float4 k4 = *kp;
+                    k4.x = fmaf(wz.x, tot, k4.x);
+                    k4.y = fmaf(wz.y, tot, k4.y);
+                    k4.z = fmaf(wz.z, tot, k4.z);
+                    k4.w = fmaf(wz.w, tot, k4.w);
+                    *kp = k4;
                 }
             } else if (STATIC) {
 #pragma unroll
@@ -576,9 +581,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             //      K[slot][ent][n] += wz_n * LT[slot][ent]
             unsigned bits[4] = {0u, 0u, 0u, 0u};
             int cnt = 0;
+            if (uniform) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if ((slot[0] >> 5) == k) wmask[k] |= 1u << (slot[0] & 31);
+            }
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
-                if (k < nwords) {
+                if (k < nwords && !uniform) {
                     unsigned mine = 0u;
 #pragma unroll
                     for (int v = 0; v < XV; ++v) mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
