@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     float *K = reinterpret_cast<float *>(LT + ltsz);              // [W][S][32]  (entry*4 + n)
     float *CT = K + W * S * 32;                                   // [S][4][32]
     float *CB = CT + S * 128;                                     // [4][32] binless cell table
-    float *shc = CB + 128;                                        // [B]
+    float4 *ZT = reinterpret_cast<float4 *>(CB + 128);            // [2][64] the item's z-tap tables
+    float *shc = reinterpret_cast<float *>(ZT + 128);             // [B]
     unsigned char *smap = reinterpret_cast<unsigned char *>(shc + B);  // [B] bin -> slot
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -333,6 +334,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
         shc[i] = STATIC ? 0.f : a.shiftc[i];
         smap[i] = 0xFF;
+    }
+    for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {   // z-tap tables in shared memory
+        ZT[i] = a.t.cw[2][it.z0 + i];
+        ZT[64 + i] = a.t.sw[2][it.z0 + i];
     }
     __syncthreads();
     for (int s = threadIdx.x; s < ns; s += blockDim.x) smap[a.slotbins[it.slot_off + s]] = (unsigned char)s;
@@ -426,8 +431,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 ++gzl;
                 ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
             }
-            const float4 cwz = a.t.cw[2][z];
-            const float4 wz = a.t.sw[2][z];
+            const float4 cwz = ZT[z - it.z0];
+            const float4 wz = ZT[64 + z - it.z0];
             int a0[XV], slot[XV];
             float lo[XV], hi[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
