@@ -539,19 +539,22 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             Item &it = its[i];
             it.slot_off = (int)slotbins.size();
             int ns = 0;
-            for (int b = 0; b < g.B; ++b)
-                if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
-            it.nslots = ns;
-            if (!pass2) smax = std::max(smax, ns);
-            if (pass2) {
-                int nb2 = 0, last = -1;
-                for (int k = it.slot_off; k < it.slot_off + ns; ++k) {
-                    if (slotbins[k] != last) ++nb2;
-                    ++nb2;
-                    last = slotbins[k] + 1;
-                }
-                s2max = std::max(s2max, nb2);
+            if (!pass2) {   // pass 1: the fixed bins a0 present in the item ("slots")
+                for (int b = 0; b < g.B; ++b)
+                    if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
+                smax = std::max(smax, ns);
+            } else {        // pass 2: every a0 present and a0 + 1, sorted, no duplicates
+                int last = -1;
+                for (int b = 0; b < g.B; ++b)
+                    if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) {
+                        if (b != last) { slotbins.push_back(b); ++ns; }
+                        slotbins.push_back(b + 1);
+                        ++ns;
+                        last = b + 1;
+                    }
+                s2max = std::max(s2max, ns);
             }
+            it.nslots = ns;
             it.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
             ItemW &iw = w[i];
             for (int l = 0; l < 4; ++l) iw.sx[l] = iw.sy[l] = iw.sz[l] = 0.0;

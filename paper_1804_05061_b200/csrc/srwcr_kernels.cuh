@@ -903,21 +903,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
     float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
 
     const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
-    // bin list of the item: every a0 slot and a0+1 (sorted, no duplicates)
-    int nb2 = 0;
-    if (threadIdx.x == 0) {
-        int last = -1;
-        for (int s2 = 0; s2 < it.nslots; ++s2) {
-            const int b0 = a.slotbins[it.slot_off + s2];
-            if (b0 != last) gbins[nb2++] = b0;
-            gbins[nb2++] = b0 + 1;
-            last = b0 + 1;
-        }
-        gbins[GB] = nb2;
+    // bin list of the item (host-built): every a0 present and a0+1, sorted, no duplicates
+    const int nb2 = it.nslots;
+    for (int i = threadIdx.x; i < nb2; i += blockDim.x) {
+        const int b = a.slotbins[it.slot_off + i];
+        gbins[i] = b;
+        gmap[b] = (unsigned char)i;
     }
     __syncthreads();
-    nb2 = gbins[GB];
-    for (int i = threadIdx.x; i < nb2; i += blockDim.x) gmap[gbins[i]] = (unsigned char)i;
     for (int i = threadIdx.x; i < 64 * nb2; i += blockDim.x) {
         const int reg = i / nb2, k = i - reg * nb2;
         const int l = reg & 3, mm = (reg >> 2) & 3, n = reg >> 4;
