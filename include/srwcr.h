@@ -214,6 +214,8 @@ typedef struct {
     int32_t items;              /* CTAs per pass on this rank */
     float ms_prep;              /* params -> fp32 and tap-window max kernels before pass 1 */
     int32_t warps_per_cta2, items2;  /* pass 2's decomposition */
+    int32_t exact_voxels;       /* voxels of the last eval's pass 2 decided in fp64 (k_exact_fix) */
+    int32_t exact_capacity;     /* list capacity; more fall back to a scan of the slab */
 } srwcr_stats;
 srwcr_status srwcr_set_timing(srwcr_ctx *ctx, int32_t enable);
 srwcr_status srwcr_get_stats(const srwcr_ctx *ctx, srwcr_stats *out);

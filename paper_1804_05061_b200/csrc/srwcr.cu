@@ -69,6 +69,8 @@ struct srwcr_ctx {
     // device
     float *F = nullptr, *M = nullptr, *phi = nullptr, *phimax = nullptr;
     float4 *MG = nullptr;  // pass 1 -> pass 2: (m, dM/dy) per slab voxel
+    int *xlist = nullptr, *xcount = nullptr;  // voxels deferred to k_exact_fix
+    int xcap = 0;
     double *params64 = nullptr, *grad64 = nullptr;
     const double *cur_params = nullptr;  // device fp64 params of the current evaluation
     int *cb[3]{}, *sb[3]{};
@@ -227,7 +229,8 @@ static PassArgs pass_args(srwcr_ctx *c) {
     a.p64 = c->cur_params;
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
     a.tolw = reinterpret_cast<const float4 *>(c->phimax);
-    a.MG = c->MG; a.mgz0 = (int)c->z0;
+    a.MG = c->MG; a.mgz0 = (int)c->z0; a.mgz1 = (int)(c->z1 - c->z0);
+    a.xlist = c->xlist; a.xcount = c->xcount; a.xcap = c->xcap;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
@@ -267,9 +270,12 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     if (c->nitems2 == 0) return SRWCR_OK;
     a.W = c->W2;
     a.pf = c->pf2;
+    CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
     if (c->W2 > 21) k_pass2<XV, 1024><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
     else if (c->W2 > 16) k_pass2<XV, 672><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
     else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+    CKL();
+    k_exact_fix<<<296, 128, 0, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
@@ -361,6 +367,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&c->ev[i]));
     CK(cudaMallocHost(&c->pinned, 4 * sizeof(double)));
+    memset(c->pinned, 0, 4 * sizeof(double));
 
     // per-axis tables (fp64 on host -> device), control and spatial lattices
     for (int ax = 0; ax < 3; ++ax) {
@@ -598,6 +605,14 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // [0, 4G) float4 tolerances, [4G, 7G) and [7G, 10G) scratch of the window-max passes
     CK(cudaMalloc(&c->phimax, sizeof(float) * (size_t)g.Gx * g.Gy * g.Gz * 10));
     CK(cudaMemset(c->phimax, 0, sizeof(float) * (size_t)g.Gx * g.Gy * g.Gz * 10));
+    {   // deferred exact-path voxels: 1/16 of the slab (more falls back to an MG scan)
+        const int64_t sv = std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy);
+        c->xcap = (int)std::min<int64_t>(std::max<int64_t>(4096, sv / 16), 1 << 30);
+        if (const char *e = getenv("SRWCR_XCAP")) c->xcap = std::max(1, atoi(e));  // tests: force the scan fallback
+        CK(cudaMalloc(&c->xlist, sizeof(int) * (size_t)c->xcap));
+        CK(cudaMalloc(&c->xcount, sizeof(int)));
+        CK(cudaMemset(c->xcount, 0, sizeof(int)));
+    }
     CK(cudaMalloc(&c->MG, sizeof(float4) * (size_t)std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy)));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
@@ -681,7 +696,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             cudaFree(tmp);
         }
     }
-    c->launches_per_eval = 8;  // params->f32, 3 window-max, pass 1, combine, reduce_D, pass 2
+    c->launches_per_eval = 9;  // params->f32, 3 window-max, pass 1, combine, reduce_D, pass 2, exact fix
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -757,6 +772,7 @@ static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, boo
     }
     if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
     CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (grad) CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (grad && !grad_dev) CK(cudaMemcpyAsync(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (c->timing) {
@@ -893,6 +909,8 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->ms_prep = c->ms[4];
     out->warps_per_cta2 = c->W2;
     out->items2 = c->nitems2;
+    out->exact_capacity = c->xcap;
+    out->exact_voxels = c->pinned ? reinterpret_cast<const int *>(c->pinned + 2)[0] : 0;
     return SRWCR_OK;
 }
 extern "C" srwcr_status srwcr_stream(const srwcr_ctx *c, void **stream) {
@@ -907,7 +925,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
-    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
+    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma};
     for (void *p : bufs)

@@ -64,6 +64,9 @@ struct PassArgs {
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
     const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 4e-6 max |phi_c| over the tap window (c = x,y,z)
+    int *xlist, *xcount;        // pass 2: slab-linear indices of the voxels deferred to k_exact_fix
+    int xcap;                   //         capacity of xlist
+    int mgz1;                   //         slab slices (k_exact_fix scan fallback)
     float4 *MG;                 // pass 1 out / pass 2 in: per slab voxel (m, dM/dy) -- m < 0
     int mgz0;                   //   encodes -1 - m for voxels that need the fp64 exact path
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
@@ -801,10 +804,14 @@ struct ExactGeo { int nx, ny, nz, L, Gx, Gy, GzExt, ndim; };
 // integer (a trilinear cell or clamp boundary) or whose warped intensity lies within
 // 1e-4 of an integer (the Parzen kink of c4): there the per-voxel derivative is
 // discontinuous and the side must be decided as the fp64 definition decides it.
-__device__ __noinline__ void exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
-                                          int bx, int by, int bz, double4 wx, double4 wy, double4 wz, int x,
-                                          int y, int z, float &gxo, float &gyo, float &gzo, float &g1po,
-                                          float &c2o) {
+// (returned by value: reference outputs would force the caller's locals into local memory)
+struct ExactOut { float gx, gy, gz, g1p, c2; };
+__device__ __noinline__ ExactOut exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
+                                              const double4 *__restrict__ cwx64, const double4 *__restrict__ cwy64,
+                                              const double4 *__restrict__ cwz64, int bx, int by, int bz, int x,
+                                              int y, int z) {
+    const double4 wx = cwx64[x], wy = cwy64[y], wz = cwz64[z];
+    ExactOut o;
     const long long plane = (long long)g.Gx * g.Gy, cs = plane * g.GzExt;
     const long long nxy = (long long)g.nx * g.ny;
     double u[3] = {0.0, 0.0, 0.0};
@@ -848,14 +855,15 @@ __device__ __noinline__ void exact_sample(ExactGeo g, const double *__restrict__
                       (1 - tx) * tz * (c011 - c001) + tx * tz * (c111 - c101);
     const double gz = (1 - tx) * (1 - ty) * (c001 - c000) + tx * (1 - ty) * (c101 - c100) +
                       (1 - tx) * ty * (c011 - c010) + tx * ty * (c111 - c110);
-    gxo = clx ? 0.f : (float)gx;
-    gyo = cly ? 0.f : (float)gy;
-    gzo = (clz || g.nz == 1) ? 0.f : (float)gz;
+    o.gx = clx ? 0.f : (float)gx;
+    o.gy = cly ? 0.f : (float)gy;
+    o.gz = (clz || g.nz == 1) ? 0.f : (float)gz;
     int n = (int)floor(m);
     n = n > g.L - 1 ? g.L - 1 : (n < 0 ? 0 : n);
     const double f = m - (double)n;
-    if (m == floor(m)) { g1po = 0.1f; c2o = (float)(2.0 * m); }
-    else { g1po = (float)(f < 0.5 ? 0.1 + 3.6 * f : 3.7 - 3.6 * f); c2o = (float)(2.0 * n + 1.0); }
+    if (m == floor(m)) { o.g1p = 0.1f; o.c2 = (float)(2.0 * m); }
+    else { o.g1p = (float)(f < 0.5 ? 0.1 + 3.6 * f : 3.7 - 3.6 * f); o.c2 = (float)(2.0 * n + 1.0); }
+    return o;
 }
 
 __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(v - rintf(v)) < tol; }
@@ -929,7 +937,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
 
     bool lok[XV];
     int xv[XV], relx[XV], cbx[XV];
-    float4 cwx[XV], swx[XV], cwr[XV];
+    float4 swx[XV], cwr[XV];
     const int q4 = lane & 3;
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
@@ -937,9 +945,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
         xv[v] = lok[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
         cbx[v] = a.t.cb[0][xv[v]];
         relx[v] = cbx[v] - xn0;
-        cwx[v] = a.t.cw[0][xv[v]];
         swx[v] = a.t.sw[0][xv[v]];
-        const float4 w = cwx[v];
+        const float4 w = a.t.cw[0][xv[v]];
         cwr[v] = q4 == 0 ? w : q4 == 1 ? make_float4(w.y, w.z, w.w, w.x)
                              : q4 == 2 ? make_float4(w.z, w.w, w.x, w.y) : make_float4(w.w, w.x, w.y, w.z);
     }
@@ -1097,10 +1104,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 float g1p, c2;
                 if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
                 else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
-                if (ex)
-                    exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
-                                 cbx[v], cby, bz, a.t.cw64[0][xv[v]], a.t.cw64[1][y], a.t.cw64[2][z], xv[v], y, z,
-                                 dgx, dgy, dgz, g1p, c2);
+                if (ex) {   // deferred to k_exact_fix (fp64); contributes nothing here
+                    if (lok[v]) {
+                        const int pos = atomicAdd(a.xcount, 1);
+                        if (pos < a.xcap) a.xlist[pos] = ((z - a.mgz0) * g.ny + y) * nx + xv[v];
+                    }
+                    dgx = dgy = dgz = 0.f;
+                }
                 const float d = lok[v] ? g1p * a.invZ * fmaf(c2, At, 2.0f * (Bt - Gt)) : 0.f;
                 const float d0 = d * dgx, d1 = d * dgy, d2 = d * dgz;
 #pragma unroll
@@ -1130,6 +1140,66 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
         const int gzn = zn0 + lz;
         if (c >= g.ndim || gzn >= g.GzExt) continue;
         atomicAdd(a.grad + (((long long)c * g.GzExt + gzn) * g.Gy + (yn0 + gyl)) * g.Gx + (xn0 + gxl), (double)v);
+    }
+}
+
+// The voxels pass 2 deferred (fp32 sample coordinate within rounding of a cell/clamp
+// boundary, or m at the Parzen kink of a non-flat cell): the whole per-voxel derivative
+// in the fp64 definition (exact_sample), its a8 weight dD/dm from the same fp32 alpha,
+// beta, gamma tables and spatial weights (contracted directly over the 64 regions), and
+// its adjoint scattered onto the 64 control nodes with fp64 atomics.  When more voxels
+// were flagged than the list holds, the kernel scans the slab's MG flags instead.
+__global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
+    const Geo &g = a.g;
+    const int cnt = *a.xcount;
+    const bool scan = cnt > a.xcap;
+    const long long slab = (long long)g.nxy * a.mgz1;
+    const long long n = scan ? slab : cnt;
+    const int B = g.B;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        long long idx;
+        if (scan) {
+            if (!(a.MG[i].x < 0.f)) continue;
+            idx = i;
+        } else {
+            idx = a.xlist[i];
+        }
+        const int x = (int)(idx % g.nx);
+        const long long t = idx / g.nx;
+        const int y = (int)(t % g.ny), z = (int)(t / g.ny) + a.mgz0;
+        const int bx = a.t.cb[0][x], by = a.t.cb[1][y], bz = a.t.cb[2][z];
+        const ExactOut e = exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
+                                        a.t.cw64[0], a.t.cw64[1], a.t.cw64[2], bx, by, bz, x, y, z);
+        const float Fv = a.F[(long long)z * g.nxy + (long long)y * g.nx + x];
+        const int a0 = min((int)Fv, g.L - 1);
+        float hlo, hhi;
+        parzen_pair(Fv - (float)a0, hlo, hhi);
+        const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
+        const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
+        float At = 0.f, Bt = 0.f, Gt = 0.f;
+        for (int nn = 0; nn < 4; ++nn)
+            for (int mm = 0; mm < 4; ++mm)
+                for (int l = 0; l < 4; ++l) {
+                    const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+                    if (w == 0.f) continue;
+                    const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+                    At = fmaf(w, a.alpha[r], At);
+                    Bt = fmaf(w, a.beta[r], Bt);
+                    Gt = fmaf(w, fmaf(hlo, a.gamma[r * B + a0], hhi * a.gamma[r * B + a0 + 1]), Gt);
+                }
+        const float d = e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt));
+        const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
+        const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
+        for (int nn = 0; nn < 4; ++nn) {
+            if (bz + nn >= g.GzExt || f4(wz, nn) == 0.f) continue;
+            for (int mm = 0; mm < 4; ++mm)
+                for (int l = 0; l < 4; ++l) {
+                    const float w = f4(wz, nn) * f4(wy, mm) * f4(wx, l);
+                    for (int c = 0; c < g.ndim; ++c)
+                        atomicAdd(a.grad + (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l,
+                                  (double)(w * dc[c]));
+                }
+        }
     }
 }
 

@@ -161,3 +161,25 @@ def test_slab_decomposition_on_one_gpu(P):
     assert rel_l2(gsum, grad1) <= 1e-5
     for r in ranks + [g1]:
         r.close()
+
+
+def test_exact_path_voxels_and_scan_fallback(monkeypatch):
+    """Voxels whose per-voxel derivative is discontinuous within fp32 rounding are
+    deferred by pass 2 to the fp64 k_exact_fix kernel; with the list capacity forced to
+    1 the kernel falls back to scanning the slab's flags.  Both must agree with each
+    other and with the oracle."""
+    g, pb, Fn, Mn, params = problem("C5", 1, params_kind="large")
+    D1, g1 = g.eval(params)
+    st = g.stats()
+    assert st["exact_voxels"] > 1, st
+    g.close()
+    monkeypatch.setenv("SRWCR_XCAP", "1")
+    g2, *_ = problem("C5", 1, params_kind="large")
+    assert g2.stats()["exact_capacity"] == 1
+    D2, g2r = g2.eval(params)
+    assert g2.stats()["exact_voxels"] > 1
+    g2.close()
+    assert rel(D2, D1) <= 2e-7
+    assert rel_l2(g2r, g1) <= 1e-5
+    Do, go = O.eval_moments(pb, Fn, Mn, params)
+    assert rel_l2(g2r, go) <= G_TOL
