@@ -352,6 +352,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     for (int i = 0; i < 2 + !is2d; ++i)
         if (c->delta[i] < 1.2) return fail(c, SRWCR_EINVAL, "control spacing along axis %d is %.3f voxels; >= 1.2 required", i, c->delta[i]);
     g.Gx = (int)G[0]; g.Gy = (int)G[1]; g.GzExt = (int)G[2];
+    g.nxy32 = (int)g.nxy;
+    g.nxm2 = std::max(g.nx - 2, 0); g.nym2 = std::max(g.ny - 2, 0); g.nzm2 = std::max(g.nz - 2, 0);
+    g.dzo = g.nz > 1 ? g.nxy32 : 0;
     g.Gz = is2d ? 4 : (int)G[2];
     g.Kx = c->kcells[0] > 0 ? c->kcells[0] + 3 : 4;
     g.Ky = c->kcells[1] > 0 ? c->kcells[1] + 3 : 4;

@@ -39,6 +39,7 @@ struct Geo {
     int Gx, Gy, Gz;             // internal control grid (Gz padded to 4 in 2-D)
     int Kx, Ky, Kz;             // regions per axis
     int ndim, GzExt;            // external components (2 or 3) and external Gz
+    int nxy32, nxm2, nym2, nzm2, dzo;  // host-precomputed: nx*ny, max(N-2, 0) per axis, z stride (0 in 2-D)
 };
 
 struct Item {
@@ -390,8 +391,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
         Elr[k] = src == 0 ? El[0] : src == 1 ? El[1] : src == 2 ? El[2] : El[3];
     }
     const float cI = it.cI;
-    const int nx = g.nx, nxy = (int)g.nxy, nxm2 = g.nx - 2, nym2 = g.ny - 2, nzm2 = max(g.nz - 2, 0);
-    const int dzo = g.nz > 1 ? nxy : 0;
+    const int nx = g.nx, nxy = g.nxy32, nxm2 = g.nxm2, nym2 = g.nym2, nzm2 = g.nzm2;
+    const int dzo = g.dzo;
     const float *__restrict__ Mv = a.M;
     __syncthreads();
 
