@@ -441,6 +441,32 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             float lo[XV], hi[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
             float amax = 0.f;
+            // gathers first, for all XV voxels of the lane (their latency then overlaps the
+            // fixed-bin work and the other voxel's cell arithmetic)
+            float C[XV][8], T[XV][3];
+            int fl[XV];   // bits: clamp x,y,z (0-2), near-integer coordinate x,y,z (3-5)
+            if (!STATIC) {
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
+                    const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
+                    const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
+                    // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
+                    // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
+                    // The max is over this voxel's own 4x4x4 tap window (k_window_max).
+                    const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
+                    bool clx, cly, clz, nrx, nry, nrz;
+                    const int ccx = axis_fast_fl(xv[v], ux, nxm2, tl.x, T[v][0], clx, nrx);
+                    const int ccy = axis_fast_fl(y, uy, nym2, tl.y, T[v][1], cly, nry);
+                    const int ccz = axis_fast_fl(z, uz, nzm2, tl.z, T[v][2], clz, nrz);
+                    fl[v] = (int)clx | (int)cly << 1 | (int)clz << 2 | (int)nrx << 3 | (int)nry << 4 | (int)nrz << 5;
+                    const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
+                    C[v][0] = __ldg(Mv + o0); C[v][1] = __ldg(Mv + o0 + 1);
+                    C[v][2] = __ldg(Mv + o1); C[v][3] = __ldg(Mv + o1 + 1);
+                    C[v][4] = __ldg(Mv + o2); C[v][5] = __ldg(Mv + o2 + 1);
+                    C[v][6] = __ldg(Mv + o3); C[v][7] = __ldg(Mv + o3 + 1);
+                }
+            }
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 const float Fv = Fcur[v];
@@ -452,22 +478,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     lo[v] = hlo;
                     hi[v] = hhi;
                 } else {
-                    const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
-                    const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
-                    const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
-                    // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
-                    // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
-                    // The max is over this voxel's own 4x4x4 tap window (k_window_max).
-                    const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
-                    const float tlx = tl.x, tly = tl.y, tlz = tl.z;
-                    float tx, ty, tz;
-                    bool clx, cly, clz, nrx, nry, nrz;
-                    const int ccx = axis_fast_fl(xv[v], ux, nxm2, tlx, tx, clx, nrx);
-                    const int ccy = axis_fast_fl(y, uy, nym2, tly, ty, cly, nry);
-                    const int ccz = axis_fast_fl(z, uz, nzm2, tlz, tz, clz, nrz);
-                    const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
-                    const float c000 = __ldg(Mv + o0), c100 = __ldg(Mv + o0 + 1), c010 = __ldg(Mv + o1), c110 = __ldg(Mv + o1 + 1);
-                    const float c001 = __ldg(Mv + o2), c101 = __ldg(Mv + o2 + 1), c011 = __ldg(Mv + o3), c111 = __ldg(Mv + o3 + 1);
+                    const float tx = T[v][0], ty = T[v][1], tz = T[v][2];
+                    const float c000 = C[v][0], c100 = C[v][1], c010 = C[v][2], c110 = C[v][3];
+                    const float c001 = C[v][4], c101 = C[v][5], c011 = C[v][6], c111 = C[v][7];
                     const float e00 = lerpf(c000, c100, tx), e10 = lerpf(c010, c110, tx);
                     const float e01 = lerpf(c001, c101, tx), e11 = lerpf(c011, c111, tx);
                     const float f0 = lerpf(e00, e10, ty);
@@ -483,11 +496,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         float dgx = lerpf(lerpf(c100 - c000, c110 - c010, ty), lerpf(c101 - c001, c111 - c011, ty), tz);
                         float dgy = lerpf(e10 - e00, e11 - e01, tz);
                         float dgz = f1 - f0;
-                        dgx = clx ? 0.f : dgx;
-                        dgy = cly ? 0.f : dgy;
-                        dgz = (clz || dzo == 0) ? 0.f : dgz;
+                        dgx = (fl[v] & 1) ? 0.f : dgx;
+                        dgy = (fl[v] & 2) ? 0.f : dgy;
+                        dgz = ((fl[v] & 4) || dzo == 0) ? 0.f : dgz;
                         const float fm = m - (float)n;
-                        const bool ex = nrx || nry || (nrz && dzo != 0) ||
+                        const bool ex = (fl[v] & 0x18) || ((fl[v] & 0x20) && dzo != 0) ||
                                         ((fm < 5e-5f || fm > 1.0f - 5e-5f) &&
                                          !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 &&
                                            c101 == c000 && c011 == c000 && c111 == c000));
