@@ -406,8 +406,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
         const float *__restrict__ Frow = a.F + y * nx;
         int gzl = a.t.cb[2][it.z0];
         float U[4][XV][3];
+        if (!STATIC) {
 #pragma unroll
-        for (int n = 0; n < 4; ++n) ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+            for (int n = 0; n < 4; ++n) ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
+        }
         float bacc = 0.f;
         unsigned wmask[4] = {0u, 0u, 0u, 0u};
         // F is software-pipelined one slice ahead (its DRAM latency is otherwise exposed:
@@ -415,6 +417,35 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
         float Fnext[XV];
 #pragma unroll
         for (int v = 0; v < XV; ++v) Fnext[v] = ld_stream(Frow + it.z0 * nxy + xv[v]);
+        // The 8 M gathers of every voxel are software-pipelined one slice ahead too: issued
+        // for slice z+1 right after slice z's sample arithmetic, so their latency overlaps
+        // the line-table, fold and binless work of slice z.
+        float C[XV][8], T[XV][3];
+        int fl[XV];   // bits: clamp x,y,z (0-2), near-integer coordinate x,y,z (3-5)
+        auto gather = [&](int zz) {
+            const float4 cw = ZT[zz - it.z0];
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                const float ux = fmaf(cw.w, U[3][v][0], fmaf(cw.z, U[2][v][0], fmaf(cw.y, U[1][v][0], cw.x * U[0][v][0])));
+                const float uy = fmaf(cw.w, U[3][v][1], fmaf(cw.z, U[2][v][1], fmaf(cw.y, U[1][v][1], cw.x * U[0][v][1])));
+                const float uz = fmaf(cw.w, U[3][v][2], fmaf(cw.z, U[2][v][2], fmaf(cw.y, U[1][v][2], cw.x * U[0][v][2])));
+                // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
+                // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
+                // The max is over this voxel's own 4x4x4 tap window (k_window_max).
+                const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
+                bool clx, cly, clz, nrx, nry, nrz;
+                const int ccx = axis_fast_fl(xv[v], ux, nxm2, tl.x, T[v][0], clx, nrx);
+                const int ccy = axis_fast_fl(y, uy, nym2, tl.y, T[v][1], cly, nry);
+                const int ccz = axis_fast_fl(zz, uz, nzm2, tl.z, T[v][2], clz, nrz);
+                fl[v] = (int)clx | (int)cly << 1 | (int)clz << 2 | (int)nrx << 3 | (int)nry << 4 | (int)nrz << 5;
+                const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
+                C[v][0] = __ldg(Mv + o0); C[v][1] = __ldg(Mv + o0 + 1);
+                C[v][2] = __ldg(Mv + o1); C[v][3] = __ldg(Mv + o1 + 1);
+                C[v][4] = __ldg(Mv + o2); C[v][5] = __ldg(Mv + o2 + 1);
+                C[v][6] = __ldg(Mv + o3); C[v][7] = __ldg(Mv + o3 + 1);
+            }
+        };
+        if (!STATIC) gather(it.z0);
 
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
             float Fcur[XV];
@@ -426,47 +457,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     Fnext[v] = ld_stream(Frow + z * nxy + nz1 + xv[v]);
                 }
             }
-            const int bz = a.t.cb[2][z];
-            while (gzl < bz) {                                   // slide the 4-layer window
-#pragma unroll
-                for (int n = 0; n < 3; ++n)
-#pragma unroll
-                    for (int v = 0; v < XV; ++v) { U[n][v][0] = U[n + 1][v][0]; U[n][v][1] = U[n + 1][v][1]; U[n][v][2] = U[n + 1][v][2]; }
-                ++gzl;
-                ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
-            }
-            const float4 cwz = ZT[z - it.z0];
             const float4 wz = ZT[64 + z - it.z0];
             int a0[XV], slot[XV];
             float lo[XV], hi[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
             float amax = 0.f;
-            // gathers first, for all XV voxels of the lane (their latency then overlaps the
-            // fixed-bin work and the other voxel's cell arithmetic)
-            float C[XV][8], T[XV][3];
-            int fl[XV];   // bits: clamp x,y,z (0-2), near-integer coordinate x,y,z (3-5)
-            if (!STATIC) {
-#pragma unroll
-                for (int v = 0; v < XV; ++v) {
-                    const float ux = fmaf(cwz.w, U[3][v][0], fmaf(cwz.z, U[2][v][0], fmaf(cwz.y, U[1][v][0], cwz.x * U[0][v][0])));
-                    const float uy = fmaf(cwz.w, U[3][v][1], fmaf(cwz.z, U[2][v][1], fmaf(cwz.y, U[1][v][1], cwz.x * U[0][v][1])));
-                    const float uz = fmaf(cwz.w, U[3][v][2], fmaf(cwz.z, U[2][v][2], fmaf(cwz.y, U[1][v][2], cwz.x * U[0][v][2])));
-                    // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
-                    // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
-                    // The max is over this voxel's own 4x4x4 tap window (k_window_max).
-                    const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
-                    bool clx, cly, clz, nrx, nry, nrz;
-                    const int ccx = axis_fast_fl(xv[v], ux, nxm2, tl.x, T[v][0], clx, nrx);
-                    const int ccy = axis_fast_fl(y, uy, nym2, tl.y, T[v][1], cly, nry);
-                    const int ccz = axis_fast_fl(z, uz, nzm2, tl.z, T[v][2], clz, nrz);
-                    fl[v] = (int)clx | (int)cly << 1 | (int)clz << 2 | (int)nrx << 3 | (int)nry << 4 | (int)nrz << 5;
-                    const int o0 = ccz * nxy + ccy * nx + ccx, o1 = o0 + nx, o2 = o0 + dzo, o3 = o2 + nx;
-                    C[v][0] = __ldg(Mv + o0); C[v][1] = __ldg(Mv + o0 + 1);
-                    C[v][2] = __ldg(Mv + o1); C[v][3] = __ldg(Mv + o1 + 1);
-                    C[v][4] = __ldg(Mv + o2); C[v][5] = __ldg(Mv + o2 + 1);
-                    C[v][6] = __ldg(Mv + o3); C[v][7] = __ldg(Mv + o3 + 1);
-                }
-            }
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 const float Fv = Fcur[v];
@@ -520,6 +515,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
                     }
                 }
+            }
+            if (!STATIC && z + 1 < it.z0 + it.zlen) {   // next slice: slide the layer window, issue its gathers
+                const int bz1 = a.t.cb[2][z + 1];
+                while (gzl < bz1) {
+#pragma unroll
+                    for (int n = 0; n < 3; ++n)
+#pragma unroll
+                        for (int v = 0; v < XV; ++v) { U[n][v][0] = U[n + 1][v][0]; U[n][v][1] = U[n + 1][v][1]; U[n][v][2] = U[n + 1][v][2]; }
+                    ++gzl;
+                    ffd_layer<XV>(a.phi, g, gzl + 3, cby, cwy, xn0, nxn, relx, cwx, lane, U[3]);
+                }
+                gather(z + 1);
             }
             // ---- binless: warp-reduce (x-tap, channel) and fold the z-taps into bacc
             if (!STATIC) {
