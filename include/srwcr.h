@@ -183,6 +183,33 @@ srwcr_status srwcr_default_lbfgs_config(srwcr_lbfgs_config *cfg);
 srwcr_status srwcr_register(srwcr_ctx *ctx, double *params_inout, const srwcr_lbfgs_config *cfg,
                             srwcr_register_report *report);
 
+/* ---- multi-resolution registration utilities (backward
+ * warping, "the multi-resolution strategy and the concatenation of three isotropic control
+ * grids").  Not on the SRWCR hot path.  Fields are fp32 [3][Nz][Ny][Nx] (component x, y,
+ * z; displacements in voxels of the volume they belong to); volumes fp32 [Nz][Ny][Nx].
+ *
+ * srwcr_field: the dense FFD displacement u(x) at params (Eq 17 taps, the fp32 arithmetic of
+ *   the passes).  params host or device; field host or device (written).  Errors: EINVAL,
+ *   ECUDA, ESTATE.
+ * The context-free functions below take DEVICE pointers only (EINVAL otherwise) and run
+ * on `stream` (a cudaStream_t, NULL = default stream); they return ECUDA on a launch
+ * error and do not synchronise:
+ *   srwcr_resample        out(x) = vol(x + u(x)), trilinear, positions clamped per axis to
+ *                         [0, N-1] (readings c1-c3)
+ *   srwcr_compose         out(x) = u(x) + U(x + u(x)): the backward warp by u followed by U
+ *                         (out must not alias U or u)
+ *   srwcr_downsample2     2x pyramid: out voxel i = mean of voxels 2i, 2i+1 per axis (the
+ *                         last one repeated at an odd edge; a 1-slice z axis stays 1);
+ *                         out dims = ceil(dims / 2)
+ *   srwcr_upsample2_field fine field u_f(x) = 2 u_c((x - 1/2) / 2) (trilinear, clamped)
+ */
+srwcr_status srwcr_field(srwcr_ctx *ctx, const double *params, float *field);
+srwcr_status srwcr_resample(const float *vol, const int64_t dims[3], const float *field, float *out, void *stream);
+srwcr_status srwcr_compose(const float *U, const float *u, const int64_t dims[3], float *out, void *stream);
+srwcr_status srwcr_downsample2(const float *vol, const int64_t dims[3], float *out, void *stream);
+srwcr_status srwcr_upsample2_field(const float *coarse, const int64_t coarse_dims[3], float *fine,
+                                   const int64_t fine_dims[3], void *stream);
+
 /* Debug / parity dumps (copied to host memory `out` of `bytes` bytes).
  *   SRWCR_DUMP_FIXED, _MOVING   normalised volumes, fp32 [Nz][Ny][Nx]
  *   SRWCR_DUMP_A0               fixed-image bin a0 = min(floor F, L-1) per voxel, int16

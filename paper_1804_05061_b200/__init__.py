@@ -19,7 +19,8 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 _LIB = os.path.join(_HERE, "libsrwcr.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("srwcr.cu", "srwcr_kernels.cuh", "srwcr_register.inc")]
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("srwcr.cu", "srwcr_kernels.cuh", "srwcr_register.inc",
+                                                  "srwcr_fields.inc")]
 _HDR = os.path.join(_ROOT, "include", "srwcr.h")
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
@@ -86,7 +87,8 @@ _lib = None
 
 EXPORTS = ["srwcr_default_options", "srwcr_create", "srwcr_num_params", "srwcr_eval", "srwcr_eval_begin",
            "srwcr_stats_buffer", "srwcr_eval_end", "srwcr_plan_slab", "srwcr_default_lbfgs_config",
-           "srwcr_register", "srwcr_bending", "srwcr_debug_size", "srwcr_debug_dump", "srwcr_set_timing", "srwcr_get_stats",
+           "srwcr_register", "srwcr_bending", "srwcr_field", "srwcr_resample", "srwcr_compose",
+           "srwcr_downsample2", "srwcr_upsample2_field", "srwcr_debug_size", "srwcr_debug_dump", "srwcr_set_timing", "srwcr_get_stats",
            "srwcr_stream", "srwcr_last_error", "srwcr_destroy"]
 
 
@@ -118,6 +120,11 @@ def lib():
         L.srwcr_register.argtypes = [vp, vp, P(_LbfgsConfig), P(_Report)]
         L.srwcr_default_lbfgs_config.argtypes = [P(_LbfgsConfig)]
         L.srwcr_bending.argtypes = [vp, vp, P(dbl), vp]
+        L.srwcr_field.argtypes = [vp, vp, vp]
+        L.srwcr_resample.argtypes = [vp, P(i64), vp, vp, vp]
+        L.srwcr_compose.argtypes = [vp, vp, P(i64), vp, vp]
+        L.srwcr_downsample2.argtypes = [vp, P(i64), vp, vp]
+        L.srwcr_upsample2_field.argtypes = [vp, P(i64), vp, P(i64), vp]
         for name in EXPORTS:
             if name not in ("srwcr_last_error", "srwcr_destroy"):
                 getattr(L, name).restype = ctypes.c_int
@@ -266,6 +273,15 @@ class Srwcr:
         out["status_name"] = REGISTER_STATUS.get(rep.status, "?")
         return x, out
 
+    def field(self, params, out=None):
+        """Dense FFD displacement field u(x), float32 [3, Nz, Ny, Nx] (numpy, or `out`)."""
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        if out is None:
+            out = np.empty((3, self.dims[2], self.dims[1], self.dims[0]), dtype=np.float32)
+        op, ok_ = _ptr(out)
+        self._check(lib().srwcr_field(self._ctx, pp, op))
+        return out
+
     def debug_dump(self, what: str) -> np.ndarray:
         code = DUMP[what]
         n = ctypes.c_size_t()
@@ -305,3 +321,61 @@ class Srwcr:
 
     def __exit__(self, *a):
         self.close()
+
+
+# ---------------------------------------------------------------- field utilities (row F4)
+def _dims_arr(shape):
+    nz, ny, nx = (int(s) for s in shape[-3:])
+    return (ctypes.c_int64 * 3)(nx, ny, nz)
+
+
+def _dev(t):
+    if not (hasattr(t, "is_cuda") and t.is_cuda and t.is_contiguous()):
+        raise ValueError("device (CUDA) contiguous tensors required")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream():
+    import torch
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def resample(vol, field, out=None):
+    """out(x) = vol(x + u(x)) (trilinear, clamped); vol [Nz,Ny,Nx], field [3,Nz,Ny,Nx] fp32 CUDA tensors."""
+    import torch
+    out = torch.empty_like(vol) if out is None else out
+    st = lib().srwcr_resample(_dev(vol), _dims_arr(vol.shape), _dev(field), _dev(out), _stream())
+    if st != OK:
+        raise SrwcrError(st, "srwcr_resample")
+    return out
+
+
+def compose(U, u, out=None):
+    """Field of 'warp by u, then by U': out(x) = u(x) + U(x + u(x))."""
+    import torch
+    out = torch.empty_like(u) if out is None else out
+    st = lib().srwcr_compose(_dev(U), _dev(u), _dims_arr(u.shape), _dev(out), _stream())
+    if st != OK:
+        raise SrwcrError(st, "srwcr_compose")
+    return out
+
+
+def downsample2(vol):
+    """2x pyramid level of an fp32 CUDA volume [Nz,Ny,Nx] (a 1-slice z axis stays 1)."""
+    import torch
+    nz, ny, nx = vol.shape
+    out = torch.empty(((nz + 1) // 2 if nz > 1 else 1, (ny + 1) // 2, (nx + 1) // 2), dtype=vol.dtype, device=vol.device)
+    st = lib().srwcr_downsample2(_dev(vol), _dims_arr(vol.shape), _dev(out), _stream())
+    if st != OK:
+        raise SrwcrError(st, "srwcr_downsample2")
+    return out
+
+
+def upsample2_field(coarse, fine_shape):
+    """Fine field [3, *fine_shape] from a coarse one (values doubled: voxel units)."""
+    import torch
+    out = torch.empty((3, *fine_shape), dtype=coarse.dtype, device=coarse.device)
+    st = lib().srwcr_upsample2_field(_dev(coarse), _dims_arr(coarse.shape), _dev(out), _dims_arr(fine_shape), _stream())
+    if st != OK:
+        raise SrwcrError(st, "srwcr_upsample2_field")
+    return out

@@ -952,3 +952,5 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
 
 // ------------------------------------------------------------------ L-BFGS
 #include "srwcr_register.inc"
+// ------------------------------------------- fields / pyramid utilities (row F4)
+#include "srwcr_fields.inc"
