@@ -44,6 +44,7 @@ class _Cfg(ctypes.Structure):
         ("kcells", ctypes.c_int64 * 3),
         ("eps_mass", ctypes.c_double),
         ("eps_sigma", ctypes.c_double),
+        ("orientation", ctypes.c_int32),
     ]
 
 
@@ -82,6 +83,7 @@ def _load():
         lib.orc_grad_moments.argtypes = [c_cfg, vp, vp, vp, vp, vp, vp, ctypes.c_double, i64, i64, vp, vp]
         lib.orc_eval_moments.argtypes = [c_cfg, vp, vp, vp, vp]
         lib.orc_bending.argtypes = [c_cfg, vp, vp]
+        lib.orc_grad_moments_A.argtypes = [c_cfg, vp, vp, vp, vp, vp, vp, ctypes.c_double, i64, i64, vp, vp]
         lib.orc_bending.restype = ctypes.c_double
         lib.orc_eval_moments.restype = ctypes.c_double
         _lib = lib
@@ -107,6 +109,8 @@ class Problem:
     dims: (Nx, Ny, Nz), Nz == 1 means 2-D.  L: maximal bin (bins = L+1).
     delta: control spacing per axis in voxels.  kcells: spatial cells per axis
     (0 = degenerate axis: one real region).  eps_*: retention thresholds (c12).
+    orientation: 0 = moving image as the estimated image B, 1 = moving image as
+    the model image A (Eq 20-21, App. II).
     """
 
     dims: tuple
@@ -116,6 +120,7 @@ class Problem:
     eps_mass: float = 1e-12
     eps_sigma: float = 1e-6
     nthreads: int = 0
+    orientation: int = 0   # 0: moving image = estimated image B; 1: moving = model image A (F2)
 
     def cfg(self) -> _Cfg:
         c = _Cfg()
@@ -127,6 +132,7 @@ class Problem:
         c.nthreads = int(self.nthreads)
         c.eps_mass = float(self.eps_mass)
         c.eps_sigma = float(self.eps_sigma)
+        c.orientation = int(self.orientation)
         return c
 
     @property
@@ -314,6 +320,20 @@ def grad_moments(pb: Problem, F, M, params, alpha, beta_, gamma, Z, z0: int = 0,
     dd = np.zeros((z1 - z0, pb.dims[1], pb.dims[0])) if want_dDdm else None
     _load().orc_grad_moments(ctypes.byref(c), _p(F), _p(M), _p(params), _p(_f64(alpha)), _p(_f64(beta_)),
                              _p(_f64(gamma)), float(Z), int(z0), int(z1), _p(dd), _p(grad))
+    return (grad, dd) if want_dDdm else grad
+
+
+def grad_moments_A(pb: Problem, F, M, params, N, gamma, reg, Z, z0: int = 0, z1: int | None = None,
+                   want_dDdm: bool = False):
+    """Orientation 1 (moving = model image A): per-voxel dD/dm (App. II Eq 31 in moment
+    form, readings c4/c23) + Eq 16-17 over slab [z0, z1).  N, gamma, reg from combine()."""
+    z1 = pb.dims[2] if z1 is None else z1
+    c = pb.cfg()
+    F, M, params = _f32(F), _f32(M), _f64(params)
+    grad = np.zeros(pb.params_shape)
+    dd = np.zeros((z1 - z0, pb.dims[1], pb.dims[0])) if want_dDdm else None
+    _load().orc_grad_moments_A(ctypes.byref(c), _p(F), _p(M), _p(params), _p(_f64(N)), _p(_f64(gamma)),
+                               _p(_f64(reg)), float(Z), int(z0), int(z1), _p(dd), _p(grad))
     return (grad, dd) if want_dDdm else grad
 
 

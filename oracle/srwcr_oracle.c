@@ -19,6 +19,8 @@
  *       statistics Eq 10; the value by the loops of Table I
  *       (P:149-172); dD/dM(y) by Eq 27 as printed; the chain rule of
  *       Eq 16 with the Jacobian of Eq 17.
+ * Both routes take the orientation: the moving image as the
+ * estimated image B (0) or as the model image A (1, Eq 20-21, App. II).
  *   (2) MOMENT route -- the exact algebraic rewrite of SURVEY.md Appendix A
  *       (weighted counts N, Parzen moments S, Q per region and fixed bin), the
  *       combine of SURVEY 8(a) a7 and the per-voxel derivative a8.
@@ -54,6 +56,8 @@ typedef struct {
     int64_t kcells[3];  /* spatial cells per axis (0: degenerate axis) */
     double  eps_mass;   /* region retained iff N_r/Z > eps_mass   (reading c12) */
     double  eps_sigma;  /* ... and sigma_r^2 > eps_sigma (bin^2)  (reading c12) */
+    int32_t orientation;/* 0: moving image is the estimated image B (Eq 18-19);
+                           1: moving image is the model image A (Eq 20-21, App. II) */
 } orc_cfg;
 
 /* ------------------------------------------------------------------ geometry */
@@ -252,7 +256,8 @@ static int nthreads_of(const orc_cfg *c) {
 
 /* ===================================================== (1) LITERAL route === */
 
-/* Eq 3 without the 1/Z factor: P[r][a][b] = sum_x w(r,x) h(a-F(x)) h(b-M(T(x))),
+/* Eq 3 without the 1/Z factor: P[r][a][b] = sum_x w(r,x) h(a-A(x)) h(b-B(x)) with
+ * (A, B) = (F, M(T(x))) in orientation 0 and (M(T(x)), F) in orientation 1,
  * accumulated over the voxels of z-slab [z0, z1).  Dense (L+1)^2 table per region.
  * OpenMP over z with per-thread tables merged in thread order. */
 void orc_joint_hist(const orc_cfg *c, const float *F, const float *M, const double *params,
@@ -281,8 +286,10 @@ void orc_joint_hist(const orc_cfg *c, const float *F, const float *M, const doub
                     p[0] = (double)x + u[0]; p[1] = (double)y + u[1]; p[2] = (double)z + u[2];
                     orc_sample(c, M, p, &m, g);
                     double f = (double)F[(z * ny + y) * nx + x];
-                    for (int a = 0; a < B; ++a) ha[a] = orc_parzen((double)a - f);
-                    for (int b = 0; b < B; ++b) hb[b] = orc_parzen((double)b - m);
+                    /* a: model image A, b: estimated image B */
+                    const double va = c->orientation ? m : f, vb = c->orientation ? f : m;
+                    for (int a = 0; a < B; ++a) ha[a] = orc_parzen((double)a - va);
+                    for (int b = 0; b < B; ++b) hb[b] = orc_parzen((double)b - vb);
                     int64_t sbx, sby, sbz;
                     double wx[4], wy[4], wz[4];
                     spat_taps(c, 0, x, &sbx, wx);
@@ -430,6 +437,63 @@ void orc_dDdm_eq27(const orc_cfg *c, const float *F, const float *M, const doubl
             }
 }
 
+/* dD/dM(y) for the moving image as the model image A: Eq 21 / Eq 31,
+ *   (1/Z) sum_r sum_a sum_b [(2b - mu_r(a)) mu_r(a) / sigma_r^2] w(r,x) h(b - F(x)) h'(a - M(T(x)))
+ * over retained r (sigma_r^2 is F's, static in this orientation).  The a-sum runs over
+ * -1..L+1 (h' is nonzero at |a - m| = 1 only for integer m, reading c4).  Reading c23:
+ * a bin a with p_r(a) = 0 (and the virtual bins -1, L+1) takes mu_r(a) = g1(F(x)) =
+ * sum_b b h(b - F(x)), the limit of mu_r(a) as the voxel's own mass enters the bin, so
+ * the derivative is that of the function D (central differences agree). */
+void orc_dDdm_eq31(const orc_cfg *c, const float *F, const float *M, const double *params, const double *P,
+                   const double *reg, const double *mura, int64_t z0, int64_t z1, double *out) {
+    int64_t G[3], K[3];
+    orc_derived(c, G, K);
+    int L = c->L, B = L + 1;
+    int64_t nx = c->n[0], ny = c->n[1];
+    int nt = nthreads_of(c);
+#pragma omp parallel for schedule(static) num_threads(nt)
+    for (int64_t z = z0; z < z1; ++z)
+        for (int64_t y = 0; y < ny; ++y)
+            for (int64_t x = 0; x < nx; ++x) {
+                double u[3], p[3], m, g[3];
+                orc_displacement(c, params, x, y, z, u);
+                p[0] = (double)x + u[0]; p[1] = (double)y + u[1]; p[2] = (double)z + u[2];
+                orc_sample(c, M, p, &m, g);
+                double f = (double)F[(z * ny + y) * nx + x];
+                double g1f = 0.0;
+                for (int b = 0; b < B; ++b) g1f += (double)b * orc_parzen((double)b - f);
+                int64_t sbx, sby, sbz;
+                double wx[4], wy[4], wz[4];
+                spat_taps(c, 0, x, &sbx, wx);
+                spat_taps(c, 1, y, &sby, wy);
+                spat_taps(c, 2, z, &sbz, wz);
+                double acc = 0.0, Z = reg[5];
+                for (int n = 0; n < 4; ++n)
+                    for (int mm = 0; mm < 4; ++mm)
+                        for (int l = 0; l < 4; ++l) {
+                            double w = wx[l] * wy[mm] * wz[n];
+                            if (w == 0.0) continue;
+                            int64_t r = ((sbz + n) * K[1] + (sby + mm)) * K[0] + (sbx + l);
+                            if (reg[r * 6 + 4] == 0.0) continue;
+                            double sig2 = reg[r * 6 + 1];
+                            for (int a = -1; a <= L + 1; ++a) {
+                                double hp = orc_parzen_deriv((double)a - m);
+                                if (hp == 0.0) continue;
+                                double pa = 0.0;
+                                if (a >= 0 && a <= L)
+                                    for (int b = 0; b < B; ++b) pa += P[(r * B + a) * B + b];
+                                double mua = pa > 0.0 ? mura[r * B + a] : g1f;
+                                for (int b = 0; b < B; ++b) {
+                                    double hb = orc_parzen((double)b - f);
+                                    if (hb == 0.0) continue;
+                                    acc += (2.0 * b - mua) * mua / sig2 * w * hb * hp;
+                                }
+                            }
+                        }
+                out[((z - z0) * ny + y) * nx + x] = acc / Z;
+            }
+}
+
 /* Eq 16 with the Jacobian of Eq 17:
  *   dD/dphi_{s,c} += sum_x dD/dM(y) * d_c M(y) * beta_l(eta) beta_m(gamma) beta_n(tau)
  * over the voxels of z-slab [z0, z1); grad is SoA [ndim][nodes] and is ADDED to. */
@@ -497,7 +561,8 @@ double orc_eval_literal(const orc_cfg *c, const float *F, const float *M, const 
     if (grad) {
         int64_t nodes = G[0] * G[1] * G[2];
         double *dd = (double *)malloc(sizeof(double) * (size_t)nvox);
-        orc_dDdm_eq27(c, F, M, params, reg, mura, 0, c->n[2], dd);
+        if (c->orientation) orc_dDdm_eq31(c, F, M, params, P, reg, mura, 0, c->n[2], dd);
+        else orc_dDdm_eq27(c, F, M, params, reg, mura, 0, c->n[2], dd);
         memset(grad, 0, sizeof(double) * (size_t)(ndim_of(c) * nodes));
         orc_grad_chain(c, M, params, dd, 0, c->n[2], grad);
         free(dd);
@@ -525,9 +590,11 @@ static void bin_split(double v, int L, int *n, double *f) {
     *f = v - (double)k;
 }
 
-/* N[r][a] = sum w_r h_a(F), S[r][a] = sum w_r h_a g1(m), Q[r][a] = sum w_r h_a g2(m)
- * with g1 = n + w1(f) = sum_b b h(b-m), g2 = n^2 + (2n+1) w1(f) = sum_b b^2 h(b-m)
- * (SURVEY Appendix A), over z-slab [z0, z1).  Any of N, S, Q may be NULL. */
+/* N[r][a] = sum w_r h_a(A), S[r][a] = sum w_r h_a(A) g1(B), Q[r][a] = sum w_r h_a(A) g2(B)
+ * with g1 = n + w1(f) = sum_b b h(b-B), g2 = n^2 + (2n+1) w1(f) = sum_b b^2 h(b-B)
+ * (SURVEY Appendix A), over z-slab [z0, z1); (A, B) = (F, M(T)) in orientation 0 and
+ * (M(T), F) in orientation 1 (then N, S are dynamic and sum_a Q[r][a] = Q_r is static).
+ * Any of N, S, Q may be NULL. */
 void orc_moments(const orc_cfg *c, const float *F, const float *M, const double *params,
                  int64_t z0, int64_t z1, double *N, double *S, double *Q) {
     int64_t G[3], K[3];
@@ -552,10 +619,13 @@ void orc_moments(const orc_cfg *c, const float *F, const float *M, const double 
                     orc_displacement(c, params, x, y, z, u);
                     p[0] = (double)x + u[0]; p[1] = (double)y + u[1]; p[2] = (double)z + u[2];
                     orc_sample(c, M, p, &m, g);
+                    /* the model image A gives the bin a0 and its two Parzen weights, the
+                     * estimated image B the moments g1, g2 (orientation: A = F or A = M) */
+                    const double f = (double)F[(z * ny + y) * nx + x];
                     int a0, n;
                     double fa, fm;
-                    bin_split((double)F[(z * ny + y) * nx + x], L, &a0, &fa);
-                    bin_split(m, L, &n, &fm);
+                    bin_split(c->orientation ? m : f, L, &a0, &fa);
+                    bin_split(c->orientation ? f : m, L, &n, &fm);
                     double h1 = w1_of(fa), h0 = 1.0 - h1;
                     double w1m = w1_of(fm);
                     double g1 = (double)n + w1m, g2 = (double)n * (double)n + (2.0 * n + 1.0) * w1m;
@@ -719,6 +789,101 @@ void orc_grad_moments(const orc_cfg *c, const float *F, const float *M, const do
     }
 }
 
+/* Orientation 1 (moving image as the model image A; Eq 20-21, App. II Eq 28-31), moment
+ * form: with mu_ra = S_ra/N_ra and psi_ra(g) = (mu_ra^2 - 2 mu_ra g)/sigma_r^2 (and, reading
+ * c23, psi = -g^2/sigma_r^2 for an empty or virtual bin a), g = g1(F(x)):
+ *   dD/dm = (1/Z) sum_r w_r sum_a (d h_a(m)/dm) psi_ra(g)
+ * with d h_n/dm = -w1'(f), d h_{n+1}/dm = +w1'(f) for fractional m and, at integer m = k,
+ * the two-sided average -0.05 (bin k-1), +0.05 (bin k+1) (reading c4).  gamma and reg as
+ * orc_combine (gamma_ra = mu_ra/sigma_r^2), N for the empty-bin test.  Per voxel of the
+ * slab into out (nullable); if grad != NULL the chain rule of Eq 16-17 is ADDED. */
+void orc_grad_moments_A(const orc_cfg *c, const float *F, const float *M, const double *params,
+                        const double *N, const double *gamma, const double *reg, double Z,
+                        int64_t z0, int64_t z1, double *out, double *grad) {
+    int64_t G[3], K[3];
+    orc_derived(c, G, K);
+    int L = c->L, B = L + 1, nd = ndim_of(c);
+    int64_t nodes = G[0] * G[1] * G[2], nx = c->n[0], ny = c->n[1];
+    int nt = nthreads_of(c);
+    double *priv = grad ? (double *)calloc((size_t)nt * (size_t)(nd * nodes), sizeof(double)) : NULL;
+#pragma omp parallel num_threads(nt)
+    {
+        int tid = 0;
+#ifdef _OPENMP
+        tid = omp_get_thread_num();
+#endif
+        double *T = priv ? priv + (size_t)tid * (size_t)(nd * nodes) : NULL;
+#pragma omp for schedule(static)
+        for (int64_t z = z0; z < z1; ++z)
+            for (int64_t y = 0; y < ny; ++y)
+                for (int64_t x = 0; x < nx; ++x) {
+                    double u[3], p[3], m, g[3];
+                    orc_displacement(c, params, x, y, z, u);
+                    p[0] = (double)x + u[0]; p[1] = (double)y + u[1]; p[2] = (double)z + u[2];
+                    orc_sample(c, M, p, &m, g);
+                    int nF, n;
+                    double fF, fm;
+                    bin_split((double)F[(z * ny + y) * nx + x], L, &nF, &fF);
+                    const double gF = (double)nF + w1_of(fF);
+                    bin_split(m, L, &n, &fm);
+                    int ab[2];
+                    double dh[2];
+                    if (m == floor(m)) { ab[0] = (int)m - 1; ab[1] = (int)m + 1; dh[0] = -0.05; dh[1] = 0.05; }
+                    else { ab[0] = n; ab[1] = n + 1; dh[0] = -w1_deriv(fm); dh[1] = w1_deriv(fm); }
+                    int64_t sbx, sby, sbz;
+                    double wx[4], wy[4], wz[4];
+                    spat_taps(c, 0, x, &sbx, wx);
+                    spat_taps(c, 1, y, &sby, wy);
+                    spat_taps(c, 2, z, &sbz, wz);
+                    double acc = 0.0;
+                    for (int nn = 0; nn < 4; ++nn)
+                        for (int mm = 0; mm < 4; ++mm)
+                            for (int l = 0; l < 4; ++l) {
+                                double w = wx[l] * wy[mm] * wz[nn];
+                                if (w == 0.0) continue;
+                                int64_t r = ((sbz + nn) * K[1] + (sby + mm)) * K[0] + (sbx + l);
+                                if (reg[r * 6 + 4] == 0.0) continue;
+                                const double sig2 = reg[r * 6 + 1];
+                                for (int k = 0; k < 2; ++k) {
+                                    const int a = ab[k];
+                                    double psi;
+                                    if (a < 0 || a > L || N[r * B + a] <= 0.0) psi = -gF * gF / sig2;
+                                    else {
+                                        const double mu = gamma[r * B + a] * sig2;
+                                        psi = (mu * mu - 2.0 * mu * gF) / sig2;
+                                    }
+                                    acc += w * dh[k] * psi;
+                                }
+                            }
+                    const double d = acc / Z;
+                    if (out) out[((z - z0) * ny + y) * nx + x] = d;
+                    if (!T || d == 0.0) continue;
+                    int64_t bx, by, bz;
+                    double cx[4], cy[4], cz[4];
+                    ctrl_taps(c, 0, x, &bx, cx);
+                    ctrl_taps(c, 1, y, &by, cy);
+                    ctrl_taps(c, 2, z, &bz, cz);
+                    for (int nn = 0; nn < 4; ++nn) {
+                        if (cz[nn] == 0.0) continue;
+                        for (int mm = 0; mm < 4; ++mm) {
+                            if (cy[mm] == 0.0) continue;
+                            for (int l = 0; l < 4; ++l) {
+                                if (cx[l] == 0.0) continue;
+                                double jac = cx[l] * cy[mm] * cz[nn];
+                                int64_t s = node_index(G, bx + l, by + mm, bz + nn);
+                                for (int comp = 0; comp < nd; ++comp) T[comp * nodes + s] += d * g[comp] * jac;
+                            }
+                        }
+                    }
+                }
+    }
+    if (grad) {
+        for (int t = 0; t < nt; ++t)
+            for (int64_t i = 0; i < nd * nodes; ++i) grad[i] += priv[(size_t)t * (size_t)(nd * nodes) + i];
+        free(priv);
+    }
+}
+
 /* full moment-route evaluation */
 double orc_eval_moments(const orc_cfg *c, const float *F, const float *M, const double *params,
                         double *grad) {
@@ -731,14 +896,16 @@ double orc_eval_moments(const orc_cfg *c, const float *F, const float *M, const 
     double *Q = (double *)malloc(sizeof(double) * (size_t)(R * B));
     double *al = (double *)malloc(sizeof(double) * (size_t)R), *be = (double *)malloc(sizeof(double) * (size_t)R);
     double *ga = (double *)malloc(sizeof(double) * (size_t)(R * B));
+    double *reg = (double *)malloc(sizeof(double) * (size_t)(R * 6));
     orc_moments(c, F, M, params, 0, c->n[2], N, S, Q);
     double Z;
-    double D = orc_combine(c, N, S, Q, al, be, ga, NULL, &Z);
+    double D = orc_combine(c, N, S, Q, al, be, ga, reg, &Z);
     if (grad) {
         memset(grad, 0, sizeof(double) * (size_t)(nd * nodes));
-        orc_grad_moments(c, F, M, params, al, be, ga, Z, 0, c->n[2], NULL, grad);
+        if (c->orientation) orc_grad_moments_A(c, F, M, params, N, ga, reg, Z, 0, c->n[2], NULL, grad);
+        else orc_grad_moments(c, F, M, params, al, be, ga, Z, 0, c->n[2], NULL, grad);
     }
-    free(N); free(S); free(Q); free(al); free(be); free(ga);
+    free(N); free(S); free(Q); free(al); free(be); free(ga); free(reg);
     return D;
 }
 

@@ -466,3 +466,84 @@ def test_bending_gradient_central_differences(dims, delta):
         assert g.reshape(-1)[i] == pytest.approx(fd, rel=1e-7, abs=1e-12)
     # quadratic form: phi . grad = 2 C_p
     assert float((phi * g).sum()) == pytest.approx(2 * E, rel=1e-12)
+
+
+# ------------------------------------ orientation 1: moving image as model A (F2)
+
+def _swap(pb, o):
+    from dataclasses import replace
+    return replace(pb, orientation=o)
+
+
+@pytest.mark.parametrize("dims,L,delta,kcells", CASES)
+def test_orientation1_at_identity_is_orientation0_with_images_swapped(dims, L, delta, kcells):
+    """At Phi = 0 the warped moving image is M itself, so making M the model image A is
+    the same as swapping the two images (Eq 3 with A and B exchanged)."""
+    pb, F, M, _ = _rand_problem(6, dims, L, delta, kcells)
+    zero = np.zeros(pb.params_shape)
+    P1 = O.joint_hist(_swap(pb, 1), F, M, zero)
+    P0 = O.joint_hist(_swap(pb, 0), M, F, zero)
+    assert np.array_equal(P1, P0)
+    for route in (O.eval_literal, O.eval_moments):
+        D1, _ = route(_swap(pb, 1), F, M, zero, want_grad=False)
+        D0, _ = route(_swap(pb, 0), M, F, zero, want_grad=False)
+        assert D1 == pytest.approx(D0, rel=1e-13, abs=1e-15)
+    # and the orientations differ in general (SRWCR is asymmetric, P:67)
+    Da, _ = O.eval_moments(_swap(pb, 0), F, M, zero, want_grad=False)
+    assert abs(Da - O.eval_moments(_swap(pb, 1), F, M, zero, want_grad=False)[0]) > 1e-6
+
+
+@pytest.mark.parametrize("dims,L,delta,kcells", CASES)
+def test_orientation1_literal_equals_moment_route(dims, L, delta, kcells):
+    pb, F, M, params = _rand_problem(1, dims, L, delta, kcells)
+    pb = _swap(pb, 1)
+    D1, g1 = O.eval_literal(pb, F, M, params)
+    D2, g2 = O.eval_moments(pb, F, M, params)
+    assert D1 == pytest.approx(D2, rel=1e-12)
+    assert 0.0 <= D1 <= 1.0
+    assert np.linalg.norm(g1 - g2) <= 1e-11 * np.linalg.norm(g1)
+
+
+@pytest.mark.parametrize("dims,L,delta,kcells", [((16, 14, 1), 15, (4.0, 3.5, 1.0), (2, 2, 0)),
+                                                 ((10, 9, 8), 15, (3.5, 4.0, 3.0), (2, 2, 2)),
+                                                 ((11, 8, 7), 31, (2.6, 3.0, 2.2), (1, 2, 0))])
+def test_orientation1_gradient_central_differences(dims, L, delta, kcells):
+    """Eq 31 (App. II) with reading c23 is the derivative of D: central differences."""
+    pb, F, M, params = _rand_problem(3, dims, L, delta, kcells)
+    pb = _swap(pb, 1)
+    D, g = O.eval_literal(pb, F, M, params)
+    rng = np.random.default_rng(4)
+    idx = list(np.ndindex(g.shape))
+    sel = [idx[i] for i in rng.choice(len(idx), min(30, len(idx)), replace=False)]
+    sel += [np.unravel_index(i, g.shape) for i in np.argsort(-np.abs(g).ravel())[:10]]
+    h = 1e-6
+    num, ana = [], []
+    for s in sel:
+        pp, pm = params.copy(), params.copy()
+        pp[s] += h
+        pm[s] -= h
+        num.append((O.eval_literal(pb, F, M, pp, False)[0] - O.eval_literal(pb, F, M, pm, False)[0]) / (2 * h))
+        ana.append(g[s])
+    num, ana = np.array(num), np.array(ana)
+    assert np.linalg.norm(num - ana) <= 2e-5 * np.linalg.norm(num)
+
+
+def test_orientation1_identical_images_and_slabs():
+    pb3 = O.Problem(dims=(9, 8, 7), L=15, delta=(3, 3, 3), kcells=(2, 2, 2), orientation=1)
+    I = np.random.default_rng(4).integers(0, 16, size=(7, 8, 9)).astype(np.float32)
+    for route in (O.eval_literal, O.eval_moments):
+        D, _ = route(pb3, I, I, np.zeros(pb3.params_shape), want_grad=False)
+        assert abs(D) < 1e-15
+    # slab partial statistics and gradients sum to the full ones (z-slab decomposition)
+    pb, F, M, params = _rand_problem(5, (12, 10, 11), 15, (3.0, 3.0, 2.5), (2, 2, 2))
+    pb = _swap(pb, 1)
+    N, Sm, Q = O.moments(pb, F, M, params)
+    cuts = [0, 4, 11]
+    parts = [O.moments(pb, F, M, params, a, b) for a, b in zip(cuts[:-1], cuts[1:])]
+    for k, full in enumerate((N, Sm, Q)):
+        assert np.allclose(sum(p[k] for p in parts), full, rtol=1e-13, atol=1e-12)
+    D, al, be, ga, reg, Z = O.combine(pb, N, Sm, Q)
+    g_full = O.grad_moments_A(pb, F, M, params, N, ga, reg, Z)
+    g_parts = sum(O.grad_moments_A(pb, F, M, params, N, ga, reg, Z, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
+    assert np.linalg.norm(g_parts - g_full) <= 1e-13 * np.linalg.norm(g_full)
+    assert np.linalg.norm(g_full - O.eval_moments(pb, F, M, params)[1]) <= 1e-13 * np.linalg.norm(g_full)
