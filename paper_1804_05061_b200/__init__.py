@@ -164,7 +164,7 @@ class Srwcr:
 
     def __init__(self, fixed, moving, spacing_mm, bins, spatial_bins, control_spacing_mm, *,
                  inputs_normalized=False, device=0, nranks=1, rank=0, nccl_id=None, eps_mass=1e-12,
-                 eps_sigma=1e-6, moment_shift=True, use_graph=True):
+                 eps_sigma=1e-6, moment_shift=True, use_graph=True, orientation=0):
         L = lib()
         shape = tuple(int(s) for s in fixed.shape)
         if tuple(moving.shape) != shape or len(shape) != 3:
@@ -173,6 +173,7 @@ class Srwcr:
         opt = _Options()
         L.srwcr_default_options(ctypes.byref(opt))
         opt.inputs_normalized = int(bool(inputs_normalized))
+        opt.orientation = int(orientation)
         opt.device = int(device)
         opt.nranks, opt.rank = int(nranks), int(rank)
         self._nccl_id = None

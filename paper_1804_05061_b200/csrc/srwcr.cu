@@ -84,6 +84,8 @@ struct srwcr_ctx {
     int nitems = 0, nitems_full = 0;
     int W = 16, W2 = 16, XV = 1, S = 1, S2 = 2;       // warps per CTA (pass 1, 2), voxels per lane, slots, bin list
     double *SQ = nullptr, *Qt = nullptr;             // stats: [R][B][2] binned, then [R] binless
+    double *NQ = nullptr;                            // orientation 1: dynamic counts [R][B][2]
+    int gstride = 0;                                 // row stride of the gamma table
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     double *S_out = nullptr;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
@@ -140,6 +142,11 @@ static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
         ncclResult_t r_ = (call);                                                                       \
         if (r_ != ncclSuccess) return fail(c, SRWCR_ENCCL, "%s failed: %s", #call,                      \
                                            nccl().GetErrorString(r_));                                  \
+    } while (0)
+
+#define CK0(call)                                   \
+    do {                                            \
+        if ((call) != cudaSuccess) return SRWCR_ECUDA; \
     } while (0)
 
 #define TRY(x)                                \
@@ -232,6 +239,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     a.MG = c->MG; a.mgz0 = (int)c->z0; a.mgz1 = (int)(c->z1 - c->z0);
     a.xlist = c->xlist; a.xcount = c->xcount; a.xcap = c->xcap;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
+    a.NQ = c->NQ; a.gstride = c->gstride;
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
     a.grad = c->grad64;
@@ -248,13 +256,9 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     if (full) a.MG = nullptr;   // whole-volume create-time passes: no (m, dM/dy) output
     if (n == 0) return SRWCR_OK;
     a.pf = c->pf1;
-    if (c->W > 16) {
-        if (stat) k_pass1<XV, true, 768><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
-        else k_pass1<XV, false, 768><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
-    } else {
-        if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
-        else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
-    }
+    if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);   // fixed-image bins (both orientations)
+    else if (c->opt.orientation) k_pass1<XV, false, 512, 1><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
 }
@@ -271,34 +275,45 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     a.W = c->W2;
     a.pf = c->pf2;
     CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
-    if (c->W2 > 21) k_pass2<XV, 1024><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-    else if (c->W2 > 16) k_pass2<XV, 672><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-    else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-    CKL();
-    k_exact_fix<<<296, 128, 0, c->stream>>>(a);
+    if (c->opt.orientation) {
+        k_pass2<XV, 512, 1><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        CKL();
+        k_exact_fix<1><<<296, 128, 0, c->stream>>>(a);
+    } else {
+        k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        CKL();
+        k_exact_fix<0><<<296, 128, 0, c->stream>>>(a);
+    }
     CKL();
     return SRWCR_OK;
 }
 static srwcr_status launch_pass2(srwcr_ctx *c, double *grad) {
     return c->XV2 == 2 ? launch_pass2_t<2>(c, grad) : launch_pass2_t<1>(c, grad);
 }
+// The dynamic-shared-memory ceiling is a per-kernel (process-wide) attribute: set it to the
+// device's opt-in maximum so that contexts with different table sizes never race on it
+// (each launch still requests exactly its own smem1 / smem2).
 template <int XV>
-static srwcr_status set_smem_t(srwcr_ctx *c) {
-    CK(cudaFuncSetAttribute(k_pass1<XV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass1<XV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass1<XV, false, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass1<XV, true, 768>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem1));
-    CK(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
-    CK(cudaFuncSetAttribute(k_pass2<XV, 672>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
-    CK(cudaFuncSetAttribute(k_pass2<XV, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem2));
+static srwcr_status set_smem_t(int maxsm) {
+    CK0(cudaFuncSetAttribute(k_pass1<XV, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<XV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<XV, false, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass2<XV, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     return SRWCR_OK;
 }
 static srwcr_status set_smem(srwcr_ctx *c) {
-    TRY(c->XV == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c));
-    return c->XV2 == 2 ? set_smem_t<2>(c) : set_smem_t<1>(c);
+    int maxsm = 0;
+    CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
+    if (set_smem_t<1>(maxsm) != SRWCR_OK || set_smem_t<2>(maxsm) != SRWCR_OK)
+        return fail(c, SRWCR_ECUDA, "cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+    return SRWCR_OK;
 }
 
-static size_t stats_count(const srwcr_ctx *c) { return (size_t)c->R * c->g.B * 2 + (size_t)c->R; }
+// [SQ R][B][2] (ORI 1: then the dynamic counts NQ [R][B][2]) then the binless Q [R]
+static size_t stats_count(const srwcr_ctx *c) {
+    return (size_t)c->R * c->g.B * (c->opt.orientation ? 4 : 2) + (size_t)c->R;
+}
 
 static srwcr_status allreduce(srwcr_ctx *c, double *buf, size_t count) {
     if (c->comm) NCK(nccl().AllReduce(buf, buf, count, ncclFloat64, ncclSum, c->comm, c->stream));
@@ -312,8 +327,10 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     ca.eps_mass = c->opt.eps_mass; ca.eps_sigma = c->opt.eps_sigma;
     ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out;
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
+    ca.NQ = c->NQ; ca.gstride = c->gstride;
     const int wpb = 8;
-    k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
+    if (c->opt.orientation) k_combineA<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
+    else k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
     CKL();
     k_reduce_D<<<1, 1024, 0, c->stream>>>(c->dterm, c->reg, (int)c->R, c->Z, c->Dout);
     CKL();
@@ -330,7 +347,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (dims[0] < 2 || dims[1] < 2 || dims[2] < 1) return fail(c, SRWCR_EINVAL, "dims: need Nx >= 2, Ny >= 2, Nz >= 1");
     if (dims[0] > (1 << 20) || dims[1] > (1 << 20) || dims[2] > (1 << 20)) return fail(c, SRWCR_EINVAL, "dims too large");
     if (bins < 2 || bins > 128) return fail(c, SRWCR_EINVAL, "intensity_bins must be in [2, 128], got %d", bins);
-    if (o.orientation != 0) return fail(c, SRWCR_ENOTSUP, "orientation 1 (moving as model image, Eq 20-21) is not supported");
+    if (o.orientation != 0 && o.orientation != 1) return fail(c, SRWCR_EINVAL, "orientation must be 0 or 1");
+    if (o.orientation == 1 && bins > 83)
+        return fail(c, SRWCR_ENOTSUP, "orientation 1 (moving as model image) supports at most 83 intensity bins, got %d", bins);
     if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(c, SRWCR_EINVAL, "rank/nranks out of range");
     for (int i = 0; i < 3; ++i) {
         if (!(sp[i] > 0)) return fail(c, SRWCR_EINVAL, "spacing_mm[%d] must be > 0", i);
@@ -549,7 +568,13 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             Item &it = its[i];
             it.slot_off = (int)slotbins.size();
             int ns = 0;
-            if (!pass2) {   // pass 1: the fixed bins a0 present in the item ("slots")
+            if (o.orientation == 1) {   // model bins come from m: every bin (dense lists)
+                const int cnt = pass2 ? 3 * (g.B + 2) : g.L;      // pass 2: 3 table columns per bin -1..L+1
+                for (int b = 0; b < cnt; ++b) slotbins.push_back(b);
+                ns = cnt;
+                if (pass2) s2max = std::max(s2max, ns);
+                else smax = std::max(smax, 2 * ns);               // two slot groups per bin
+            } else if (!pass2) {   // pass 1: the fixed bins a0 present in the item ("slots")
                 for (int b = 0; b < g.B; ++b)
                     if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
                 smax = std::max(smax, ns);
@@ -620,7 +645,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->grad64, sizeof(double) * c->nparams));
     CK(cudaMalloc(&c->SQ, sizeof(double) * stats_count(c)));
-    c->Qt = c->SQ + RB * 2;
+    const bool ori1 = o.orientation == 1;
+    c->NQ = ori1 ? c->SQ + RB * 2 : nullptr;
+    c->Qt = c->SQ + RB * (ori1 ? 4 : 2);
+    c->gstride = ori1 ? 3 * (g.B + 2) : g.B;
     CK(cudaMalloc(&c->Nlo, sizeof(double) * RB));
     CK(cudaMalloc(&c->Nup, sizeof(double) * RB));
     CK(cudaMalloc(&c->S_out, sizeof(double) * RB));
@@ -630,7 +658,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
     CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
     CK(cudaMalloc(&c->beta, sizeof(float) * c->R));
-    CK(cudaMalloc(&c->gamma, sizeof(float) * RB));
+    CK(cudaMalloc(&c->gamma, sizeof(float) * (size_t)c->R * c->gstride));
     CK(cudaMemset(c->phi, 0, sizeof(float) * c->nint));
     CK(cudaMemset(c->params64, 0, sizeof(double) * c->nparams));
     c->cur_params = c->params64;
@@ -648,7 +676,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
                           sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16 + 2048;
         if (!c->W && W <= w1max && W != 32 && W != 20 && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
         const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (GYS + 1) +
-                          sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192) + ((g.B + 15) & ~15) +
+                          sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192 + (o.orientation ? g.B : 0)) +
+                          (((o.orientation ? 3 * (g.B + 2) : g.B) + 15) & ~15) +
                           sizeof(float) * npmax;
         if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
     }
@@ -692,7 +721,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             TRY(launch_pass1(c, false, true));
             float *tmp = nullptr;
             CK(cudaMalloc(&tmp, sizeof(float) * g.B));
-            k_shift_update<<<(g.B + 127) / 128, 128, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, c->shiftc, tmp, (int)c->R, g.B);
+            if (o.orientation)
+                k_shift_updateA<<<(g.B + 127) / 128, 128, 0, c->stream>>>(c->SQ, c->NQ, c->shiftc, tmp, (int)c->R, g.B);
+            else
+                k_shift_update<<<(g.B + 127) / 128, 128, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, c->shiftc, tmp, (int)c->R, g.B);
             CKL();
             CK(cudaMemcpyAsync(c->shiftc, tmp, sizeof(float) * g.B, cudaMemcpyDeviceToDevice, c->stream));
             CK(cudaStreamSynchronize(c->stream));

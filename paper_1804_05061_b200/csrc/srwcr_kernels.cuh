@@ -62,6 +62,8 @@ struct PassArgs {
     const int *slotbins;        // concatenated per-item slot -> bin lists
     double *SQ;                 // pass 1 out: [R][B][2] shifted binned first moments (lo, hi)
     double *Qt;                 // pass 1 out: [R] binless second moments sum_x w_r g2(m)
+    double *NQ;                 // pass 1 out (ORI 1): [R][B][2] dynamic counts N' (lo, hi halves)
+    int gstride;                // pass 2: row stride of the gamma table (B; ORI 1: 3 (B + 2))
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
     const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 4e-6 max |phi_c| over the tap window (c = x,y,z)
@@ -313,7 +315,12 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
 // line tables) so that the zero pattern of N is exact.
 // Lanes past the item's x-extent sample the item's last column with zero weights, so
 // the voxel loop has no divergent branches.
-template <int XV, bool STATIC, int MAXT = 512>
+// ORI = 1 (moving image as the model image A, Eq 20-21): the bins come from
+// m (dynamic, n = min(floor m, L-1)), the item's slot list is every bin, and each voxel
+// feeds two slot groups: 2*slot(n) the counts N'_{r,n|n+1} = sum w h_{n|n+1}(m) and
+// 2*slot(n)+1 the first moments S'_{r,n|n+1} = sum w h_{n|n+1}(m) (g1(F) - c_n); the
+// second moments of F are static (no binless channel).
+template <int XV, bool STATIC, int MAXT = 512, int ORI = 0>
 __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
@@ -329,12 +336,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = a.items[blockIdx.x];
-    const int ns = it.nslots;
-    const int nwords = (ns + 31) >> 5;
+    const int ns = it.nslots;                       // list entries (ORI 1: every bin)
+    const int nsl = ORI ? 2 * ns : ns;                // slots (ORI 1: two groups per bin)
+    const int nwords = (nsl + 31) >> 5;
 
     for (int i = threadIdx.x; i < ltsz; i += blockDim.x) LT[i] = 0;
     for (int i = threadIdx.x; i < W * S * 32; i += blockDim.x) K[i] = 0.f;
-    for (int i = threadIdx.x; i < ns * 128 + 128; i += blockDim.x) (i < ns * 128 ? CT[i] : CB[i - ns * 128]) = 0.f;
+    for (int i = threadIdx.x; i < nsl * 128 + 128; i += blockDim.x) (i < nsl * 128 ? CT[i] : CB[i - nsl * 128]) = 0.f;
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
         shc[i] = STATIC ? 0.f : a.shiftc[i];
         smap[i] = 0xFF;
@@ -459,9 +467,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
             }
             const float4 wz = ZT[64 + z - it.z0];
             int a0[XV], slot[XV];
-            float lo[XV], hi[XV];
+            float lo[XV], hi[XV], lo2[XV], hi2[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
-            float amax = 0.f;
+            float amax = 0.f, amax2 = 0.f;
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 const float Fv = Fcur[v];
@@ -503,16 +511,27 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                             st_stream4(a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx + xv[v],
                                        make_float4(ex ? -1.0f - m : m, dgx, dgy, dgz));
                     }
-                    const float A = ((float)n - shc[a0[v]]) + w1;      // g1 - c_a0
-                    const float Ab = ((float)n - cI) + w1;            // g1 - cI
-                    const float q = fmaf(Ab, Ab, w1 * w1l);           // sum_b (b - cI)^2 h(b - m)
-                    lo[v] = hlo * A;
-                    hi[v] = hhi * A;
-                    amax = fmaxf(amax, fabsf(A));
+                    if (ORI == 0) {
+                        const float A = ((float)n - shc[a0[v]]) + w1;      // g1 - c_a0
+                        const float Ab = ((float)n - cI) + w1;            // g1 - cI
+                        const float q = fmaf(Ab, Ab, w1 * w1l);           // sum_b (b - cI)^2 h(b - m)
+                        lo[v] = hlo * A;
+                        hi[v] = hhi * A;
+                        amax = fmaxf(amax, fabsf(A));
 #pragma unroll
-                    for (int l = 0; l < 4; ++l) {
-                        bq[l] = fmaf(f4(swx[v], l), q, bq[l]);
-                        ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
+                        for (int l = 0; l < 4; ++l) {
+                            bq[l] = fmaf(f4(swx[v], l), q, bq[l]);
+                            ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
+                        }
+                    } else {   // model bins from m; F gives the moment g1(F) = a0 + w1(F - a0)
+                        slot[v] = 2 * smap[n];
+                        lo[v] = w1l;                                      // N' halves
+                        hi[v] = w1;
+                        const float A = ((float)a0[v] + hhi) - shc[n];   // g1(F) - c_n
+                        lo2[v] = w1l * A;                                 // S' halves
+                        hi2[v] = w1 * A;
+                        amax = fmaxf(amax, fmaxf(w1l, w1));
+                        amax2 = fmaxf(amax2, fabsf(A));
                     }
                 }
             }
@@ -529,12 +548,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 gather(z + 1);
             }
             // ---- binless: warp-reduce (x-tap, channel) and fold the z-taps into bacc
-            if (!STATIC) {
+            if (!STATIC && ORI == 0) {
                 const float bv[8] = {bq[0], ba[0], bq[1], ba[1], bq[2], ba[2], bq[3], ba[3]};
                 const float tot = halving8(bv, lane);          // value (lane>>2) = 2*l + ch
                 bacc = fmaf(f4(wz, lane & 3), tot, bacc);
             }
-            // ---- binned: line table
+            // ---- binned: line table (ORI 1: two slot groups per voxel, each with its own scale)
+            float isc_g[2] = {1.f, 1.f};
+            bool uniform = true;
+#pragma unroll
+            for (int gi = 0; gi < (ORI ? 2 : 1); ++gi) {
+            if (gi == 1) {
+#pragma unroll
+                for (int v = 0; v < XV; ++v) { slot[v] += 1; lo[v] = lo2[v]; hi[v] = hi2[v]; }
+                amax = amax2;
+            }
             float sc[4] = {1.f, 1.f, 1.f, 1.f}, isc_e = 1.f;
             int EA = 0;
             if (!STATIC) {
@@ -543,14 +571,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 for (int l = 0; l < 4; ++l) sc[l] = exp2i(min(274 - El[l] - EA, 120));
                 isc_e = exp2i(-min(274 - El_e - EA, 120));
             }
-            int amx = a0[0];
+            isc_g[gi] = isc_e;
+            int amx = ORI ? slot[0] : a0[0];
 #pragma unroll
-            for (int v = 1; v < XV; ++v) amx = max(amx, a0[v]);
+            for (int v = 1; v < XV; ++v) amx = max(amx, ORI ? slot[v] : a0[v]);
             const int af = (int)__reduce_max_sync(FULL, (unsigned)amx);
             bool same = true;
 #pragma unroll
-            for (int v = 0; v < XV; ++v) same = same && a0[v] == af;
-            const bool uniform = __all_sync(FULL, same);
+            for (int v = 0; v < XV; ++v) same = same && (ORI ? slot[v] : a0[v]) == af;
+            uniform = __all_sync(FULL, same);
             if (uniform) {
                 float vv[8];
 #pragma unroll
@@ -606,11 +635,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                     }
                 }
             }
+            if (ORI && gi == 1) {   // both groups' slots are marked (uniform lines) / folded below
+#pragma unroll
+                for (int v = 0; v < XV; ++v) slot[v] -= 1;
+            }
+            if (uniform && ORI) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (((slot[0] + gi) >> 5) == k) wmask[k] |= 1u << ((slot[0] + gi) & 31);
+            }
+            }
             // ---- fold the line into the warp's column table, 4 slots per instruction:
             //      K[slot][ent][n] += wz_n * LT[slot][ent]
             unsigned bits[4] = {0u, 0u, 0u, 0u};
             int cnt = 0;
-            if (uniform) {
+            if (uniform && !ORI) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
                     if ((slot[0] >> 5) == k) wmask[k] |= 1u << (slot[0] & 31);
@@ -620,7 +659,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 if (k < nwords && !uniform) {
                     unsigned mine = 0u;
 #pragma unroll
-                    for (int v = 0; v < XV; ++v) mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
+                    for (int v = 0; v < XV; ++v) {
+                        mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
+                        if (ORI) mine |= (((slot[v] + 1) >> 5) == k) ? 1u << ((slot[v] + 1) & 31) : 0u;
+                    }
                     bits[k] = __reduce_or_sync(FULL, mine);
                     wmask[k] |= bits[k];
                     cnt += __popc(bits[k]);
@@ -638,7 +680,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         int *lp = LTw + s * LTS + ent;
                         const int iv = *lp;
                         *lp = 0;
-                        const float val = STATIC ? __int_as_float(iv) : (float)iv * isc_e;
+                        const float val = STATIC ? __int_as_float(iv) : (float)iv * isc_g[ORI ? (s & 1) : 0];
                         float4 *kp = reinterpret_cast<float4 *>(Kw + s * 32 + ent * 4);
                         float4 k4 = *kp;
                         k4.x = fmaf(wz.x, val, k4.x);
@@ -674,15 +716,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     }
     __syncthreads();
     // ---- item done: flush to global.  CT entry (s, m, e): e = 8*l + 4*ch + n
-    for (int t = threadIdx.x; t < ns * 128; t += blockDim.x) {
+    for (int t = threadIdx.x; t < nsl * 128; t += blockDim.x) {
         const float val = CT[t];
         if (val == 0.f) continue;
         const int s = t >> 7, mm = (t >> 5) & 3, e = t & 31;
         const int l = e >> 3, ch = (e >> 2) & 1, n = e & 3;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        atomicAdd(a.SQ + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
+        if (ORI)   // slot 2k: counts N' -> NQ, slot 2k+1: first moments S' -> SQ
+            atomicAdd(((s & 1) ? a.SQ : a.NQ) + (r * B + a.slotbins[it.slot_off + (s >> 1)]) * 2 + ch, (double)val);
+        else
+            atomicAdd(a.SQ + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
     }
-    if (!STATIC && threadIdx.x < 64) {
+    if (!STATIC && ORI == 0 && threadIdx.x < 64) {
         // binless: Q_r += Q' + 2 cI S' + cI^2 N  with N = sum of the item's spatial weights
         const int l = threadIdx.x >> 4, mm = (threadIdx.x >> 2) & 3, n = threadIdx.x & 3;
         const double Qp = CB[mm * 32 + (2 * l) * 4 + n], Sp = CB[mm * 32 + (2 * l + 1) * 4 + n];
@@ -715,6 +760,8 @@ struct CombineArgs {
     double *reg;                // [R][6] {p(r), sigma2, mu, 1-CR, retained, Z}
     double *S_out;              // [R][B] unshifted (debug / parity), may be null
     float *alpha, *beta, *gamma;
+    const double *NQ;           // ORI 1: [R][B][2] dynamic counts N' (lo, hi halves)
+    int gstride;                // ORI 1: row stride of gamma = 3 (B + 2)
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -781,6 +828,88 @@ __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
         double N, S;
         bin_NS(a, r, b, N, S);
         a.gamma[(long long)r * B + b] = (ret && N > 0.0) ? (float)((S / N) / sig2) : 0.f;
+    }
+}
+
+
+// ORI 1 (moving image as the model image A; Eq 20-21, App. II in moment form, reading
+// c23), one warp per region: the estimated image is F, so N_r, S_r = sum_a a N^F_ra and
+// Q_r = sum_a a^2 N^F_ra are static (from the fixed-bin counts, exact: g1(F), g2(F) are
+// the Parzen moments); the model bins are m's:
+//   N'_ra = NQ[r][a][0] + NQ[r][a-1][1],  S'_ra unshifted likewise (shift c_a, c_{a-1});
+//   V_r = Q_r - sum_{a: N'_ra > 0} S'_ra^2 / N'_ra,  T_r = Q_r - S_r^2/N_r.
+// Pass 2's table, per region and bin a = -1..L+1 (column 3(a+1) + {0,1,2}), written so
+// that the fp32 derivative has no cancellation: psi_ra(g) = (mu_ra - g)^2/sigma_r^2 - g^2/
+// sigma_r^2 for a populated bin and -g^2/sigma_r^2 for an empty or virtual one (c23); the
+// -g^2 terms cancel exactly in dD/dm (the two bins' dh/dm are opposite), so only
+//   psi'_ra(g) = [populated] (delta^2 + 2 delta (c_a - g) + (c_a - g)^2) / sigma_r^2,
+//   delta = mu_ra - c_a (c_a: the bin's moment shift, near the conditional mean)
+// is needed: columns {1/sigma^2, delta/sigma^2, delta^2/sigma^2} for a populated bin of a
+// retained region, zeros otherwise.
+__device__ __forceinline__ void bin_NS_A(const CombineArgs &a, int r, int b, double &N, double &S) {
+    const int B = a.B;
+    const double *n = a.NQ + ((long long)r * B + b) * 2;
+    const double *q = a.SQ + ((long long)r * B + b) * 2;
+    N = n[0];
+    S = q[0] + (double)a.shiftc[b] * n[0];
+    if (b > 0) {
+        N += (n - 2)[1];
+        S += (q - 2)[1] + (double)a.shiftc[b - 1] * (n - 2)[1];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (r >= a.R) return;
+    const int B = a.B;
+    double Nr = 0, Sr = 0, Qr = 0, s2n = 0;
+    for (int b = lane; b < B; b += 32) {
+        const double nf = a.Nlo[(long long)r * B + b] + (b > 0 ? a.Nup[(long long)r * B + b - 1] : 0.0);
+        Nr += nf;
+        Sr += (double)b * nf;
+        Qr += (double)b * (double)b * nf;
+        double N, S;
+        bin_NS_A(a, r, b, N, S);
+        if (a.S_out) a.S_out[(long long)r * B + b] = S;
+        if (N > 0.0) s2n += S * S / N;
+    }
+    Nr = warp_sum_d(Nr);
+    Sr = warp_sum_d(Sr);
+    Qr = warp_sum_d(Qr);
+    s2n = warp_sum_d(s2n);
+    const double pr = Nr / a.Z;
+    double sig2 = 0, omcr = 0;
+    bool ret = false;
+    if (pr > a.eps_mass) {
+        const double Tr = Qr - Sr * Sr / Nr, Vr = Qr - s2n;
+        sig2 = Tr / Nr;
+        if (sig2 > a.eps_sigma) { ret = true; omcr = Vr / Tr; }
+    }
+    if (lane == 0) {
+        a.dterm[r] = ret ? Nr * omcr : 0.0;
+        a.alpha[r] = 0.f;
+        a.beta[r] = 0.f;
+        double *rg = a.reg + (long long)r * 6;
+        rg[0] = pr; rg[1] = sig2; rg[2] = Nr > 0 ? Sr / Nr : 0.0; rg[3] = omcr; rg[4] = ret ? 1.0 : 0.0; rg[5] = a.Z;
+    }
+    float *row = a.gamma + (long long)r * a.gstride;
+    for (int j = lane; j < B + 2; j += 32) {   // bin a = j - 1
+        const int b = j - 1;
+        float T0 = 0.f, T1 = 0.f, T2 = 0.f;
+        if (ret && b >= 0 && b < B) {
+            double N = 0.0, S = 0.0;
+            bin_NS_A(a, r, b, N, S);
+            if (N > 0.0) {
+                const double dl = S / N - (double)a.shiftc[b];
+                T0 = (float)(1.0 / sig2);
+                T1 = (float)(dl / sig2);
+                T2 = (float)(dl * dl / sig2);
+            }
+        }
+        row[3 * j] = T0;
+        row[3 * j + 1] = T1;
+        row[3 * j + 2] = T2;
     }
 }
 
@@ -903,7 +1032,11 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 // y-taps once per row (GY[bin][xtap] = float4 over the z-taps); per line the bins the
 // line touches are contracted over z cooperatively (GZ[bin] = float4 over the x-taps),
 // so a voxel reads two float4.
-template <int XV, int MAXT = 512>
+// ORI = 1 (moving image as the model image A): dD/dm = (1/Z) sum_r w_r sum_a (dh_a/dm)
+// psi'_ra(g1(F)) (k_combineA's table, 3 columns per bin, bins -1..L+1): bins n, n+1 with
+// -/+ w1'(f), or at integer m = k bins k-1, k+1 with -/+ 0.05 (reading c4); no alpha /
+// beta terms.
+template <int XV, int MAXT = 512, int ORI = 0>
 __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
@@ -926,9 +1059,10 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
     float *gl = reinterpret_cast<float *>(GZ + W * GB);           // [64][GB] gamma of the 64 regions
     int *gbins = reinterpret_cast<int *>(gl + 64 * GB);           // [GB+1] the bin list, count
     unsigned char *gmap = reinterpret_cast<unsigned char *>(gbins + GB + 1);  // [B] bin -> list index
-    float *al = reinterpret_cast<float *>(gmap + ((B + 15) & ~15)); // [64]
+    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [64]
     float *bl = al + 64;                                          // [64]
-    float *RB = bl + 64;                                          // [W][3][64] retiring-layer row buffer
+    float *shc2 = bl + 64;                                        // [B] (ORI 1) the bins' moment shifts
+    float *RB = shc2 + (ORI ? B : 0);                             // [W][3][64] retiring-layer row buffer
     float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
 
     const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
@@ -944,7 +1078,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
         const int reg = i / nb2, k = i - reg * nb2;
         const int l = reg & 3, mm = (reg >> 2) & 3, n = reg >> 4;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        gl[reg * GB + k] = __ldg(a.gamma + r * B + gbins[k]);
+        gl[reg * GB + k] = __ldg(a.gamma + r * a.gstride + gbins[k]);
     }
     for (int i = threadIdx.x; i < 64; i += blockDim.x) {
         const int l = i & 3, mm = (i >> 2) & 3, n = i >> 4;
@@ -952,6 +1086,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
         al[i] = __ldg(a.alpha + r);
         bl[i] = __ldg(a.beta + r);
     }
+    if (ORI)
+        for (int i = threadIdx.x; i < B; i += blockDim.x) shc2[i] = a.shiftc[i];
     const int npsz = nzn * 3 * nyn * nxn;
     for (int i = threadIdx.x; i < npsz; i += blockDim.x) NP[i] = 0.f;
     for (int i = threadIdx.x; i < W * 192; i += blockDim.x) RB[i] = 0.f;
@@ -992,8 +1128,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             reinterpret_cast<float *>(GYw + k * GYS + l)[n] = val;
         }
         // alpha (lanes 0-15) / beta (lanes 16-31) contracted over y: lane = 16*ab + 4*l + n
-        float abY;
-        {
+        float abY = 0.f;
+        if (ORI == 0) {
             const int l = (lane >> 2) & 3, n = lane & 3;
             const float *src = (lane < 16 ? al : bl) + n * 16 + l;
             abY = swy.x * src[0] + swy.y * src[4] + swy.z * src[8] + swy.w * src[12];
@@ -1083,14 +1219,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 mgl[v] = ld_stream4(MGz + xv[v]);
             }
             // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
-            float t = f4(wz, lane & 3) * abY;
-            t += __shfl_xor_sync(FULL, t, 1);
-            t += __shfl_xor_sync(FULL, t, 2);
             float ay[4], by4[4];
+            if (ORI == 0) {
+                float t = f4(wz, lane & 3) * abY;
+                t += __shfl_xor_sync(FULL, t, 1);
+                t += __shfl_xor_sync(FULL, t, 2);
 #pragma unroll
-            for (int l = 0; l < 4; ++l) {
-                ay[l] = __shfl_sync(FULL, t, 4 * l);
-                by4[l] = __shfl_sync(FULL, t, 16 + 4 * l);
+                for (int l = 0; l < 4; ++l) {
+                    ay[l] = __shfl_sync(FULL, t, 4 * l);
+                    by4[l] = __shfl_sync(FULL, t, 16 + 4 * l);
+                }
             }
             // gamma of the item's bins contracted over z for this line: GZw[bin] = float4_l
             for (int i = lane; i < 4 * nb2; i += 32) {
@@ -1114,17 +1252,38 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 float m = mg.x, dgx = mg.y, dgy = mg.z, dgz = mg.w;
                 const bool ex = m < 0.f;
                 m = ex ? -1.0f - m : m;
-                const int gk = gmap[a0[v]];
-                const float4 G0 = GZw[gk], G1 = GZw[gk + 1];
                 const float4 sw = swx[v];
-                const float At = fmaf(sw.w, ay[3], fmaf(sw.z, ay[2], fmaf(sw.y, ay[1], sw.x * ay[0])));
-                const float Bt = fmaf(sw.w, by4[3], fmaf(sw.z, by4[2], fmaf(sw.y, by4[1], sw.x * by4[0])));
-                const float Gt = fmaf(hlo[v], dot4(sw, G0), hhi[v] * dot4(sw, G1));
                 const int n = min(max((int)floorf(m), 0), g.L - 1);
                 const float fm = m - (float)n;
-                float g1p, c2;
-                if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
-                else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
+                float dval;   // dD/dm * Z
+                if (ORI == 0) {
+                    const int gk = gmap[a0[v]];
+                    const float4 G0 = GZw[gk], G1 = GZw[gk + 1];
+                    const float At = fmaf(sw.w, ay[3], fmaf(sw.z, ay[2], fmaf(sw.y, ay[1], sw.x * ay[0])));
+                    const float Bt = fmaf(sw.w, by4[3], fmaf(sw.z, by4[2], fmaf(sw.y, by4[1], sw.x * by4[0])));
+                    const float Gt = fmaf(hlo[v], dot4(sw, G0), hhi[v] * dot4(sw, G1));
+                    float g1p, c2;
+                    if (m == floorf(m)) { g1p = 0.1f; c2 = 2.0f * m; }
+                    else { g1p = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f); c2 = 2.0f * (float)n + 1.0f; }
+                    dval = g1p * fmaf(c2, At, 2.0f * (Bt - Gt));
+                } else {
+                    const float gF = (float)a0[v] + hhi[v];       // g1(F)
+                    int jm, jp;                                     // table columns 3 (bin + 1)
+                    float dm, dp;
+                    if (m == floorf(m)) { const int k = (int)m; jm = 3 * k; jp = 3 * (k + 2); dm = -0.05f; dp = 0.05f; }
+                    else {
+                        jm = 3 * (n + 1); jp = 3 * (n + 2);
+                        dp = fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f);
+                        dm = -dp;
+                    }
+                    const int km = gmap[jm], kp = gmap[jp];
+                    // psi' = T2~ + 2 (c_a - g) T1~ + (c_a - g)^2 T0~ (see k_combineA)
+                    const int am = jm / 3 - 1, ap = jp / 3 - 1;
+                    const float em = (am >= 0 && am < B ? shc2[am] : 0.f) - gF, ep = (ap < B ? shc2[ap] : 0.f) - gF;
+                    const float psm = fmaf(em * em, dot4(sw, GZw[km]), fmaf(2.0f * em, dot4(sw, GZw[km + 1]), dot4(sw, GZw[km + 2])));
+                    const float psp = fmaf(ep * ep, dot4(sw, GZw[kp]), fmaf(2.0f * ep, dot4(sw, GZw[kp + 1]), dot4(sw, GZw[kp + 2])));
+                    dval = fmaf(dm, psm, dp * psp);
+                }
                 if (ex) {   // deferred to k_exact_fix (fp64); contributes nothing here
                     if (lok[v]) {
                         const int pos = atomicAdd(a.xcount, 1);
@@ -1132,7 +1291,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                     }
                     dgx = dgy = dgz = 0.f;
                 }
-                const float d = lok[v] ? g1p * a.invZ * fmaf(c2, At, 2.0f * (Bt - Gt)) : 0.f;
+                const float d = lok[v] ? a.invZ * dval : 0.f;
                 const float d0 = d * dgx, d1 = d * dgy, d2 = d * dgz;
 #pragma unroll
                 for (int n2 = 0; n2 < 4; ++n2) {
@@ -1170,13 +1329,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
 // beta, gamma tables and spatial weights (contracted directly over the 64 regions), and
 // its adjoint scattered onto the 64 control nodes with fp64 atomics.  When more voxels
 // were flagged than the list holds, the kernel scans the slab's MG flags instead.
+template <int ORI = 0>
 __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
     const Geo &g = a.g;
     const int cnt = *a.xcount;
     const bool scan = cnt > a.xcap;
     const long long slab = (long long)g.nxy * a.mgz1;
     const long long n = scan ? slab : cnt;
-    const int B = g.B;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         long long idx;
         if (scan) {
@@ -1197,18 +1356,44 @@ __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
         parzen_pair(Fv - (float)a0, hlo, hhi);
         const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
         const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
-        float At = 0.f, Bt = 0.f, Gt = 0.f;
-        for (int nn = 0; nn < 4; ++nn)
-            for (int mm = 0; mm < 4; ++mm)
-                for (int l = 0; l < 4; ++l) {
-                    const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
-                    if (w == 0.f) continue;
-                    const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-                    At = fmaf(w, a.alpha[r], At);
-                    Bt = fmaf(w, a.beta[r], Bt);
-                    Gt = fmaf(w, fmaf(hlo, a.gamma[r * B + a0], hhi * a.gamma[r * B + a0 + 1]), Gt);
-                }
-        const float d = e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt));
+        float d;
+        if (ORI == 0) {
+            float At = 0.f, Bt = 0.f, Gt = 0.f;
+            for (int nn = 0; nn < 4; ++nn)
+                for (int mm = 0; mm < 4; ++mm)
+                    for (int l = 0; l < 4; ++l) {
+                        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+                        if (w == 0.f) continue;
+                        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+                        At = fmaf(w, a.alpha[r], At);
+                        Bt = fmaf(w, a.beta[r], Bt);
+                        Gt = fmaf(w, fmaf(hlo, a.gamma[r * a.gstride + a0], hhi * a.gamma[r * a.gstride + a0 + 1]), Gt);
+                    }
+            d = e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt));
+        } else {
+            // exact_sample's c2 is 2m at integer m (even) and 2n + 1 otherwise (odd)
+            const int c2i = (int)e.c2;
+            int jm, jp;
+            float dm, dp;
+            if ((c2i & 1) == 0) { const int k = c2i / 2; jm = 3 * k; jp = 3 * (k + 2); dm = -0.05f; dp = 0.05f; }
+            else { const int nb = (c2i - 1) / 2; jm = 3 * (nb + 1); jp = 3 * (nb + 2); dm = -e.g1p; dp = e.g1p; }
+            const float gF = (float)a0 + hhi;
+            const int am = jm / 3 - 1, ap = jp / 3 - 1;
+            const float em = (am >= 0 && am < g.B ? a.shiftc[am] : 0.f) - gF, ep = (ap < g.B ? a.shiftc[ap] : 0.f) - gF;
+            float acc = 0.f;
+            for (int nn = 0; nn < 4; ++nn)
+                for (int mm = 0; mm < 4; ++mm)
+                    for (int l = 0; l < 4; ++l) {
+                        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+                        if (w == 0.f) continue;
+                        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+                        const float *row = a.gamma + r * a.gstride;
+                        const float pm = fmaf(em * em, row[jm], fmaf(2.0f * em, row[jm + 1], row[jm + 2]));
+                        const float pp = fmaf(ep * ep, row[jp], fmaf(2.0f * ep, row[jp + 1], row[jp + 2]));
+                        acc = fmaf(w, fmaf(dm, pm, dp * pp), acc);
+                    }
+            d = a.invZ * acc;
+        }
         const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
         const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
         for (int nn = 0; nn < 4; ++nn) {
@@ -1367,6 +1552,27 @@ __global__ void k_shift_update(const double *SQ, const double *Nlo, const double
             const double nup = Nup[(long long)r * B + b - 1];
             N += nup;
             S += SQ[((long long)r * B + b - 1) * 2 + 1] + cp * nup;
+        }
+    }
+    shift_out[b] = N > 0.0 ? (float)(S / N) : (float)b;
+}
+
+
+// ORI 1: the per-bin shift c_b = conditional mean of g1(F) over the voxels whose m falls in
+// bin b (all regions), from an identity pass with shifts shift_in
+__global__ void k_shift_updateA(const double *SQ, const double *NQ, const float *shift_in, float *shift_out,
+                                int R, int B) {
+    const int b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= B) return;
+    double N = 0, S = 0;
+    const double c = shift_in[b], cp = b > 0 ? shift_in[b - 1] : 0.0;
+    for (int r = 0; r < R; ++r) {
+        const long long i = ((long long)r * B + b) * 2;
+        N += NQ[i];
+        S += SQ[i] + c * NQ[i];
+        if (b > 0) {
+            N += NQ[i - 1];
+            S += SQ[i - 1] + cp * NQ[i - 1];
         }
     }
     shift_out[b] = N > 0.0 ? (float)(S / N) : (float)b;

@@ -17,14 +17,15 @@ REDUCED = {
 }
 
 
-def problem(name, seed=1, dims=None, params_kind="small", pseed=None):
+def problem(name, seed=1, dims=None, params_kind="small", pseed=None, orientation=0, bins=None):
     """(gpu Srwcr, oracle Problem, Fn, Mn, params) for a config at the given dims."""
     cfg = synth.config(name, dims if dims is not None else REDUCED[name])
     F, M = synth.make_pair(name, seed, cfg["dims"])
-    L = cfg["bins"] - 1
+    nb = bins if bins is not None else cfg["bins"]
+    L = nb - 1
     delta = tuple(c / s for c, s in zip(cfg["control_mm"], cfg["spacing"]))
-    pb = O.Problem(dims=cfg["dims"], L=L, delta=delta, kcells=cfg["cells"])
-    g = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    pb = O.Problem(dims=cfg["dims"], L=L, delta=delta, kcells=cfg["cells"], orientation=orientation)
+    g = S.Srwcr(F, M, cfg["spacing"], nb, cfg["cells"], cfg["control_mm"], orientation=orientation)
     assert g.params_shape == pb.params_shape, (g.params_shape, pb.params_shape)
     params = synth.make_params(pb.params_shape, params_kind, seed if pseed is None else pseed)
     Fn, Mn = O.normalize(F, L), O.normalize(M, L)

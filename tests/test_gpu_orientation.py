@@ -1,0 +1,56 @@
+"""GPU parity of SURVEY 8(f) row F2 -- the moving image as the model image A (Eq 20-21,
+App. II Eq 31; readings c4, c23) -- against the fp64 oracle, same gates as orientation 0:
+D relative error <= 1e-5, gradient relative L2 <= 1e-4."""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+import paper_1804_05061_b200 as S
+from gpu_common import problem, rel, rel_l2
+
+pytestmark = pytest.mark.gpu
+
+D_TOL = 1e-5
+G_TOL = 1e-4
+
+
+@pytest.mark.parametrize("name,bins", [("C1", None), ("C2", None), ("C3", None), ("C4", None), ("C5", 64)])
+@pytest.mark.parametrize("kind", ["zero", "small", "large"])
+def test_orientation1_value_and_gradient(name, bins, kind):
+    g, pb, Fn, Mn, params = problem(name, 1, params_kind=kind, orientation=1, bins=bins)
+    D, grad = g.eval(params)
+    if name == "C1":
+        Do, go = O.eval_literal(pb, Fn, Mn, params)
+    else:
+        Do, go = O.eval_moments(pb, Fn, Mn, params)
+    assert rel(D, Do) <= D_TOL, (D, Do)
+    if np.linalg.norm(go) > 0:
+        assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+    g.close()
+
+
+def test_orientation1_swap_identity_at_zero_params():
+    """At Phi = 0, orientation 1 on (F, M) equals orientation 0 on (M, F)."""
+    cfg = synth.config("C3", (70, 66, 34))
+    F, M = synth.make_pair("C3", 1, cfg["dims"])
+    a = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], orientation=1)
+    b = S.Srwcr(M, F, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], orientation=0)
+    z = np.zeros(a.params_shape)
+    Da, _ = a.eval(z, want_grad=False)
+    Db, _ = b.eval(z, want_grad=False)
+    assert rel(Da, Db) <= 2e-6, (Da, Db)
+    a.close()
+    b.close()
+
+
+def test_orientation1_register_reduces_cost_and_too_many_bins_rejected():
+    g, pb, Fn, Mn, _ = problem("C3", 1, orientation=1)
+    x, rep = g.register(None, max_iter=30)
+    assert rep["final_cost"] < rep["initial_cost"] * (1 - 1e-3)
+    g.close()
+    cfg = synth.config("C5", (66, 62, 42))
+    F, M = synth.make_pair("C5", 1, cfg["dims"])
+    with pytest.raises(S.SrwcrError) as e:
+        S.Srwcr(F, M, cfg["spacing"], 128, cfg["cells"], cfg["control_mm"], orientation=1)
+    assert e.value.status == S.ENOTSUP
