@@ -60,7 +60,9 @@ typedef enum {
 typedef struct {
     int32_t struct_size;       /* = sizeof(srwcr_options); set by srwcr_default_options */
     int32_t orientation;       /* 0 = moving image is the estimated image B (Eq 18-19/27).
-                                  1 = moving as model image A (Eq 20-21/31): SRWCR_ENOTSUP */
+                                  1 = moving image is the model image A (Eq 20-21, App. II Eq 31;
+                                  readings c4, c23): at most 83 intensity bins (SRWCR_ENOTSUP
+                                  above); other values SRWCR_EINVAL */
     int32_t inputs_normalized; /* 1: fixed/moving already in [0, L]; 0: min-max normalise */
     int32_t device;            /* CUDA device ordinal */
     int32_t nranks, rank;      /* z-slab decomposition: rank r owns slab srwcr_plan_slab(r) */
@@ -81,8 +83,9 @@ srwcr_status srwcr_default_options(srwcr_options *opt);
 /* Create a context: copies F and M (host or device; the caller may free them on
  * return), normalises them, builds the per-axis B-spline tables (Eq 8, Eq 17),
  * accumulates the static fixed-image counts N[r][a] = sum_x w_r(x) h(a - F(x))
- * (Eq 3; they do not depend on Phi in this orientation) and captures the
- * evaluation graph.
+ * (Eq 3; they do not depend on Phi) and estimates the per-bin moment shifts
+ * with one identity pass.  (options.use_graph is reserved: an evaluation is 9
+ * ordinary launches on the context's stream.)
  *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2
  *   spacing_mm[3]      voxel spacing (> 0)
  *   intensity_bins     L + 1, in [2, 256] (paper: L = 31)
