@@ -73,7 +73,7 @@ typedef struct {
     int32_t moment_shift;      /* 1 (default): per-fixed-bin shift of the accumulated moments
                                   estimated at Phi = 0; 0: shift = bin index.  Exact algebra
                                   either way; it only conditions the fp32 partial sums. */
-    int32_t use_graph;         /* 1 (default): srwcr_eval replays one CUDA graph */
+    int32_t use_graph;         /* reserved (accepted, no effect): srwcr_eval issues ordinary launches */
 } srwcr_options;
 
 /* Fills *opt with defaults: orientation 0, inputs_normalized 0, device 0, nranks 1,
