@@ -66,8 +66,9 @@ typedef struct {
     int32_t inputs_normalized; /* 1: fixed/moving already in [0, L]; 0: min-max normalise */
     int32_t device;            /* CUDA device ordinal */
     int32_t nranks, rank;      /* z-slab decomposition: rank r owns slab srwcr_plan_slab(r) */
-    const void *nccl_id;       /* nranks > 1: 128-byte ncclUniqueId (broadcast by the caller),
-                                  or NULL for caller-driven exchange (srwcr_eval_begin/end) */
+    const void *nccl_id;       /* 128-byte ncclUniqueId (broadcast by the caller): the library
+                                  all-reduces over NCCL (any nranks >= 1); NULL with nranks > 1:
+                                  caller-driven exchange (srwcr_eval_begin/end) */
     double eps_mass;           /* region retained iff p(r) > eps_mass ... (reading c12) */
     double eps_sigma;          /* ... and sigma_r^2 > eps_sigma (bin^2)                  */
     int32_t moment_shift;      /* 1 (default): per-fixed-bin shift of the accumulated moments

@@ -684,8 +684,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (c->W == 0 || c->W2 == 0) return fail(c, SRWCR_EINVAL, "shared memory too small for %d bins / %d slots", g.B, c->S);
     TRY(set_smem(c));
 
-    // NCCL communicator for the z-slab decomposition
-    if (c->nranks > 1) {
+    // NCCL communicator for the z-slab decomposition (also built for nranks = 1 when an id
+    // is given: the same code path, exercised on a single GPU by the tests)
+    if (c->nranks > 1 || o.nccl_id) {
         if (o.nccl_id) {
             if (!nccl().ok) return fail(c, SRWCR_ENCCL, "libnccl.so.2 could not be loaded");
             ncclUniqueId id;

@@ -183,3 +183,28 @@ def test_exact_path_voxels_and_scan_fallback(monkeypatch):
     assert rel_l2(g2r, g1) <= 1e-5
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     assert rel_l2(g2r, go) <= G_TOL
+
+
+def test_nccl_exchange_path_single_rank():
+    """The library-driven exchange (ncclCommInitRank from a caller-broadcast unique id,
+    ncclAllReduce of the statistics and of the gradient on the library stream) with one
+    rank: the NCCL plumbing of the z-slab decomposition runs on the GPU box and leaves the
+    result unchanged (a sum over one rank)."""
+    torch = pytest.importorskip("torch")
+    import synth
+    import paper_1804_05061_b200 as S
+    name = "C3"
+    cfg = synth.config(name, REDUCED[name])
+    F, M = synth.make_pair(name, 1, cfg["dims"])
+    g1 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    params = synth.make_params(g1.params_shape, "small", 1)
+    D1, grad1 = g1.eval(params)
+    uid = torch.cuda.nccl.unique_id()
+    g2 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], nranks=1, rank=0, nccl_id=uid)
+    D2, grad2 = g2.eval(params)
+    x, rep = g2.register(params, max_iter=3)
+    assert rep["iterations"] >= 1
+    assert rel(D2, D1) <= 2e-7
+    assert rel_l2(grad2, grad1) <= 1e-5
+    g1.close()
+    g2.close()
