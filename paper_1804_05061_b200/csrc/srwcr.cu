@@ -667,7 +667,16 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
     const int Wc[8] = {32, 24, 20, 16, 12, 8, 6, 4};
-    int w1max = 16, w2max = 16;
+    // a CTA's warps own whole rows of its item: no more warps than the tallest item has
+    // rows (fine spatial lattices -- small items -- then fit several CTAs per SM)
+    auto wcap = [&](const std::vector<Item> &its) {
+        int ym = 1;
+        for (const Item &it : its) ym = std::max(ym, it.ylen);
+        for (int W : {4, 6, 8, 12, 16})
+            if (W >= ym) return W;
+        return 16;
+    };
+    int w1max = wcap(items), w2max = wcap(items2);
     if (const char *e = getenv("SRWCR_W1")) w1max = atoi(e);
     if (const char *e = getenv("SRWCR_W2")) w2max = atoi(e);
     c->W = c->W2 = 0;

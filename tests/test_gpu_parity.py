@@ -208,3 +208,27 @@ def test_nccl_exchange_path_single_rank():
     assert rel_l2(grad2, grad1) <= 1e-5
     g1.close()
     g2.close()
+
+
+@pytest.mark.parametrize("orientation", [0, 1])
+def test_fine_spatial_lattice(orientation):
+    """SURVEY 8(f) row F3, the paper's own regime: one spatial cell per control
+    cell (here 14 x 13 x 17 cells, 5440 regions) -- the same kernels, work items of one
+    control cell each."""
+    import synth
+    import paper_1804_05061_b200 as S
+    dims = REDUCED["C3"]
+    cfg = synth.config("C3", dims)
+    F, M = synth.make_pair("C3", 1, dims)
+    L = cfg["bins"] - 1
+    delta = tuple(c / s for c, s in zip(cfg["control_mm"], cfg["spacing"]))
+    cells = tuple(int(n // d) for n, d in zip(dims, delta))
+    pb = O.Problem(dims=dims, L=L, delta=delta, kcells=cells, orientation=orientation)
+    g = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cells, cfg["control_mm"], orientation=orientation)
+    params = synth.make_params(g.params_shape, "small", 2)
+    D, grad = g.eval(params)
+    Do, go = O.eval_moments(pb, O.normalize(F, L), O.normalize(M, L), params)
+    assert pb.nregions == 5440
+    assert rel(D, Do) <= D_TOL
+    assert rel_l2(grad, go) <= G_TOL
+    g.close()
