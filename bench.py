@@ -41,6 +41,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=0, help="z-slices of the oracle sample (0 = auto)")
+    ap.add_argument("--no-paper-workloads", action="store_true",
+                    help="skip the context timings of the paper's Table VIII workloads")
     return ap.parse_args()
 
 
@@ -173,6 +175,42 @@ def run_reference(args):
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# Table VIII: one value+derivative iteration on DIR-Lab CT volumes at three
+# sizes, delta = 5 voxels, L = 31 (32 bins), spatial bins = control nodes,
+# GTX 1060.  Measured here on C3-shaped synthetic CT of the same sizes, same settings.
+PAPER_TABLE_VIII = [((64, 64, 24), 21 + 4), ((128, 128, 49), 132 + 32), ((256, 256, 99), 851 + 238)]
+
+
+def paper_workloads(device, steps=10):
+    import torch
+    import paper_1804_05061_b200 as S
+    import synth
+    out = []
+    for dims, paper_ms in PAPER_TABLE_VIII:
+        cfg = synth.config("C3", dims)
+        F, M = synth.make_pair("C3", 1, dims)
+        sp = cfg["spacing"]
+        cells = tuple(max(1, int(n // 5)) for n in dims)
+        g = S.Srwcr(torch.from_numpy(F).cuda(), torch.from_numpy(M).cuda(), sp, 32, cells, tuple(5.0 * x for x in sp),
+                    device=device)
+        p = torch.from_numpy(synth.make_params(g.params_shape, "small", 1)).cuda()
+        gr = torch.empty_like(p)
+        st = torch.cuda.ExternalStream(g.stream_handle())
+        for _ in range(3):
+            g.eval(p, grad=gr)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            g.eval(p, grad=gr)
+        e1.record(st)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        out.append({"dims": list(dims), "bins": 32, "spatial_cells": list(cells), "ms_per_eval": ms,
+                    "paper_gtx1060_ms": paper_ms, "speedup_vs_paper": paper_ms / ms})
+        g.close()
+    return out
 
 
 def main():
@@ -311,6 +349,7 @@ def main():
                                                         "warps_per_cta2", "items2")},
             "clocks": clk.summary(),
             "D": D,
+            "paper_workloads": None if args.no_paper_workloads else paper_workloads(local),
         }
         print(json.dumps(line), flush=True)
     g.close()
