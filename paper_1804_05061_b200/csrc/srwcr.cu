@@ -91,8 +91,6 @@ struct srwcr_ctx {
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
     double Z = 0;
     size_t smem1 = 0, smem2 = 0;
-    int segsteps = 0;
-    int pf1 = 0, pf2 = 0;                            // software L2 prefetch: measured no gain once loads issue early
     ncclComm_t comm = nullptr;
     bool external_exchange = false;
     bool begun = false;
@@ -243,7 +241,6 @@ static PassArgs pass_args(srwcr_ctx *c) {
     a.alpha = c->alpha; a.beta = c->beta; a.gamma = c->gamma;
     a.invZ = (float)(1.0 / c->Z);
     a.grad = c->grad64;
-    a.segsteps = c->segsteps;
     return a;
 }
 
@@ -255,7 +252,6 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     a.itemw = full ? c->itemw_full : c->itemw;
     if (full) a.MG = nullptr;   // whole-volume create-time passes: no (m, dM/dy) output
     if (n == 0) return SRWCR_OK;
-    a.pf = c->pf1;
     if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);   // fixed-image bins (both orientations)
     else if (c->opt.orientation) k_pass1<XV, false, 512, 1><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
@@ -273,7 +269,6 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     a.items = c->items2;
     if (c->nitems2 == 0) return SRWCR_OK;
     a.W = c->W2;
-    a.pf = c->pf2;
     CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
     if (c->opt.orientation) {
         k_pass2<XV, 512, 1><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
@@ -382,8 +377,6 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->nparams = (int64_t)g.ndim * G[0] * G[1] * G[2];
     c->nint = 3LL * g.Gx * g.Gy * g.Gz;
 
-    if (const char *e = getenv("SRWCR_PF1")) c->pf1 = atoi(e);
-    if (const char *e = getenv("SRWCR_PF2")) c->pf2 = atoi(e);
     c->dev = o.device;
     CK(cudaSetDevice(c->dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
@@ -412,17 +405,6 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         CK(cudaMemcpy(c->sw[ax], w.data(), sizeof(float4) * dims[ax], cudaMemcpyHostToDevice));
     }
     // max lanes sharing a control x-base inside a 32-lane chunk -> segmented-reduction steps
-    {
-        int maxrun = 1, run = 1;
-        for (int i = 1; i < g.nx; ++i) {
-            run = (c->h_cb[0][i] == c->h_cb[0][i - 1]) ? run + 1 : 1;
-            maxrun = std::max(maxrun, run);
-        }
-        maxrun = std::min(maxrun, 32);
-        c->segsteps = 0;
-        while ((1 << c->segsteps) < maxrun) ++c->segsteps;
-    }
-
     // volumes: upload (host or device source) and normalise
     const long long nvox = (long long)g.nx * g.ny * g.nz;
     CK(cudaMalloc(&c->F, sizeof(float) * nvox));

@@ -75,8 +75,6 @@ struct PassArgs {
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
     double *grad;               // pass 2 out: [ndim][GzExt][Gy][Gx] (fp64)
-    int segsteps;               // pass 2: shuffle steps of the segmented x-reduction
-    int pf;                     // L2 prefetch of the next slices (per pass, tunable)
 };
 
 __device__ __forceinline__ float f4(const float4 &v, int i) {
@@ -101,8 +99,6 @@ __device__ __forceinline__ float4 ld_stream4(const float4 *p) {
 __device__ __forceinline__ void st_stream4(float4 *p, float4 v) {
     asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
-__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-constexpr int PFD = 4;          // z-slices of look-ahead of the L2 prefetches
 
 // 2^k as a float, k in [-126, 127]
 __device__ __forceinline__ float exp2i(int k) { return __int_as_float((k + 127) << 23); }
