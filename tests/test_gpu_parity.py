@@ -232,3 +232,33 @@ def test_fine_spatial_lattice(orientation):
     assert rel(D, Do) <= D_TOL
     assert rel_l2(grad, go) <= G_TOL
     g.close()
+
+
+EDGE = [((2, 2, 1), 3, (1.5, 1.5, 1.0), (0, 0, 0)),        # smallest legal volume (2-D)
+        ((5, 3, 2), 7, (1.5, 1.25, 1.5), (1, 1, 1)),        # two slices, one cell
+        ((33, 17, 1), 15, (4.0, 3.0, 1.0), (3, 2, 0)),      # 2-D, ragged cells
+        ((37, 29, 23), 31, (3.3, 2.9, 4.1), (5, 0, 3)),     # one degenerate spatial axis
+        ((70, 9, 40), 63, (5.0, 2.0, 6.0), (7, 1, 2))]      # flat rows (9), wide x
+
+
+@pytest.mark.parametrize("orientation", [0, 1])
+@pytest.mark.parametrize("dims,L,delta,kcells", EDGE)
+def test_edge_geometries(dims, L, delta, kcells, orientation):
+    """Degenerate and ragged geometries (tiny volumes, 2-D, degenerate spatial axes,
+    non-integer control spacings) in both orientations against the oracle."""
+    import paper_1804_05061_b200 as S
+    rng = np.random.default_rng(sum(dims) + orientation)
+    sh = dims[::-1]
+    F = rng.uniform(0, 1000, size=sh).astype(np.float32)
+    M = (0.5 * F + rng.uniform(0, 300, size=sh)).astype(np.float32)
+    sp = (1.0, 1.0, 1.0)
+    g = S.Srwcr(F, M, sp, L + 1, kcells, delta, orientation=orientation)
+    pb = O.Problem(dims=dims, L=L, delta=delta, kcells=kcells, orientation=orientation)
+    assert g.params_shape == pb.params_shape
+    params = rng.uniform(-1.0, 1.0, size=pb.params_shape)
+    D, grad = g.eval(params)
+    Do, go = O.eval_literal(pb, O.normalize(F, L), O.normalize(M, L), params)
+    assert rel(D, Do) <= D_TOL, (D, Do)
+    if np.linalg.norm(go) > 1e-12:
+        assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+    g.close()
