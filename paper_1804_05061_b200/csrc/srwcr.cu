@@ -86,6 +86,7 @@ struct srwcr_ctx {
     double *SQ = nullptr, *Qt = nullptr;             // stats: [R][B][2] binned, then [R] binless
     double *NQ = nullptr;                            // orientation 1: dynamic counts [R][B][2]
     int gstride = 0;                                 // row stride of the gamma table
+    int pz0 = 0, pzb1 = 0, pz1 = 0;                  // node layers the slab reads: [pz0, pz1), bases < pzb1
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     double *S_out = nullptr;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
@@ -376,6 +377,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->R = (int64_t)g.Kx * g.Ky * g.Kz;
     c->nparams = (int64_t)g.ndim * G[0] * G[1] * G[2];
     c->nint = 3LL * g.Gx * g.Gy * g.Gz;
+    c->pz0 = 0; c->pzb1 = g.Gz; c->pz1 = g.Gz;   // refined below once the slab and tap tables exist
 
     c->dev = o.device;
     CK(cudaSetDevice(c->dev));
@@ -450,6 +452,11 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->nranks = o.nranks;
     c->rank = o.rank;
     srwcr_plan_slab(g.nz, c->nranks, c->rank, &c->z0, &c->z1);
+    if (c->z1 > c->z0 && !is2d) {   // node layers read by the slab's taps (3 beyond the last base)
+        c->pz0 = c->h_cb[2][c->z0];
+        c->pzb1 = c->h_cb[2][c->z1 - 1] + 1;
+        c->pz1 = std::min(c->h_cb[2][c->z1 - 1] + 4, g.Gz);
+    }
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, c->dev);
     // voxels per lane: 2 when every spatial x-cell is at least 48 voxels wide
@@ -767,16 +774,20 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     }
     c->cur_params = pd;
     if (c->timing) CK(cudaEventRecord(c->ev[4], c->stream));
-    k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g);
+    // only the node layers this rank's slab reads: taps of slices [z0, z1) (all of them on
+    // one rank), converted to fp32, and their tap-window max |phi_c| (x, y into scratch,
+    // z -> float4) for pass 1's rounding bound
+    k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g, c->pz0, c->pz1);
     CKL();
-    {   // tap-window max |phi_c| for pass 1's rounding bound (x, y into scratch, z -> float4)
+    {
         const size_t G = (size_t)c->g.Gx * c->g.Gy * c->g.Gz;
         float *s1 = c->phimax + 4 * G, *s2 = c->phimax + 7 * G;
-        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, s1, c->g);
+        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, s1, c->g, c->pz0, c->pz1);
         CKL();
-        k_window_max<1><<<592, 256, 0, c->stream>>>(s1, s2, c->g);
+        k_window_max<1><<<592, 256, 0, c->stream>>>(s1, s2, c->g, c->pz0, c->pz1);
         CKL();
-        k_window_max_z4<<<592, 256, 0, c->stream>>>(s2, reinterpret_cast<float4 *>(c->phimax), c->g);
+        k_window_max_z4<<<592, 256, 0, c->stream>>>(s2, reinterpret_cast<float4 *>(c->phimax), c->g, c->pz0,
+                                                    c->pzb1, c->pz1);
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));

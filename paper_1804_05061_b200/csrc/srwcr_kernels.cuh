@@ -1409,10 +1409,12 @@ __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
 
 // fp64 external params [ndim][GzExt][Gy][Gx] -> fp32 internal [3][Gz][Gy][Gx] (zeros padded)
 // phi[c][Gz][Gy][Gx] fp32 (internal layout, Gz padded to 4 in 2-D with zeros)
-__global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict__ phi, Geo g) {
+__global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict__ phi, Geo g, int zlo, int zhi) {
+    // node layers [zlo, zhi) only: a rank converts the layers its slab's taps read
     const long long plane = (long long)g.Gx * g.Gy;
-    const long long cs = (long long)g.Gz * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cs; i += (long long)gridDim.x * blockDim.x) {
+    const long long cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
+        const long long i = (long long)zlo * plane + j;
         const long long gz = i / plane, xy = i - gz * plane;
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -1424,18 +1426,19 @@ __global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict_
 }
 
 // max of |phi_c| over the 4 nodes [k, k+3] along axis AX (clipped to the grid), for all
-// 3 components: three passes give the max over each voxel's 4x4x4 tap window keyed by
-// its base node -- the scale of pass 1's rounding bound of u (k_pass1)
+// 3 components, over node layers [zlo, zhi): three passes give the max over each voxel's
+// 4x4x4 tap window keyed by its base node -- the scale of pass 1's rounding bound of u
 template <int AX>
-__global__ void k_window_max(const float *__restrict__ in, float *__restrict__ out, Geo g) {
-    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < 3 * cs; i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i % cs;
+__global__ void k_window_max(const float *__restrict__ in, float *__restrict__ out, Geo g, int zlo, int zhi) {
+    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 3 * span; j += (long long)gridDim.x * blockDim.x) {
+        const long long comp = j / span, r = (long long)zlo * plane + (j - comp * span);
+        const long long i = comp * cs + r;
         int k, G;
         long long st;
         if (AX == 0) { k = (int)(r % g.Gx); G = g.Gx; st = 1; }
         else if (AX == 1) { k = (int)((r / g.Gx) % g.Gy); G = g.Gy; st = g.Gx; }
-        else { k = (int)(r / plane); G = g.Gz; st = plane; }
+        else { k = (int)(r / plane); G = zhi; st = plane; }
         float m = 0.f;
 #pragma unroll
         for (int d = 0; d < 4; ++d)
@@ -1445,17 +1448,18 @@ __global__ void k_window_max(const float *__restrict__ in, float *__restrict__ o
 }
 
 // last (z) pass of the window max, all 3 components of a node into one float4, already
-// scaled to pass 1's tolerance 4e-6 max |phi_c|
-__global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict__ out, Geo g) {
-    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cs; i += (long long)gridDim.x * blockDim.x) {
+// scaled to pass 1's tolerance 4e-6 max |phi_c|; base layers [zlo, zb) reading up to zhi
+__global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict__ out, Geo g, int zlo, int zb, int zhi) {
+    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zb - zlo) * plane;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
+        const long long i = (long long)zlo * plane + j;
         const int k = (int)(i / plane);
         float m[3] = {0.f, 0.f, 0.f};
 #pragma unroll
         for (int c = 0; c < 3; ++c)
 #pragma unroll
             for (int d = 0; d < 4; ++d)
-                if (k + d < g.Gz) m[c] = fmaxf(m[c], fabsf(in[c * cs + i + d * plane]));
+                if (k + d < zhi) m[c] = fmaxf(m[c], fabsf(in[c * cs + i + d * plane]));
         out[i] = make_float4(4e-6f * m[0], 4e-6f * m[1], 4e-6f * m[2], 0.f);
     }
 }
