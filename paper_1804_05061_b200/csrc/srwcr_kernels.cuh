@@ -266,7 +266,8 @@ __device__ __forceinline__ int axis_fast_fl(int i, float u, int nm2, float tol, 
     const float tt = u - fu;
     const bool lo = c < 0, hi = c > nm2;
     t = lo ? 0.f : (hi ? 1.f : tt);
-    cl = lo || (hi && !(c == nm2 + 1 && tt == 0.f));
+    // clamped iff the position c + tt lies outside [0, N-1]: 2c + (tt > 0) outside [0, 2(N-1)]
+    cl = (unsigned)(2 * c + (tt > 0.f ? 1 : 0)) > (unsigned)(2 * nm2 + 2);
     // (far outside the volume the flag may be raised needlessly: harmless, the fp64 path
     // then confirms the clamp)
     near = fabsf(u - rintf(u)) < tol;
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 }
             }
             const float4 wz = ZT[64 + z - it.z0];
+            float4 *MGrow = a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx;
             int a0[XV], slot[XV];
             float lo[XV], hi[XV], lo2[XV], hi2[XV];
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
@@ -499,13 +501,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                         dgy = (fl[v] & 2) ? 0.f : dgy;
                         dgz = ((fl[v] & 4) || dzo == 0) ? 0.f : dgz;
                         const float fm = m - (float)n;
-                        const bool ex = (fl[v] & 0x18) || ((fl[v] & 0x20) && dzo != 0) ||
-                                        ((fm < 5e-5f || fm > 1.0f - 5e-5f) &&
-                                         !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 &&
-                                           c101 == c000 && c011 == c000 && c111 == c000));
+                        bool ex = (fl[v] & 0x18) || ((fl[v] & 0x20) && dzo != 0);
+                        if (!ex && (fm < 5e-5f || fm > 1.0f - 5e-5f))   // rare: the flatness test
+                            ex = !(c100 == c000 && c010 == c000 && c110 == c000 && c001 == c000 &&
+                                   c101 == c000 && c011 == c000 && c111 == c000);
                         if (a.MG && lane + 32 * v < it.xlen)
-                            st_stream4(a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx + xv[v],
-                                       make_float4(ex ? -1.0f - m : m, dgx, dgy, dgz));
+                            st_stream4(MGrow + xv[v], make_float4(ex ? -1.0f - m : m, dgx, dgy, dgz));
                     }
                     if (ORI == 0) {
                         const float A = ((float)n - shc[a0[v]]) + w1;      // g1 - c_a0
