@@ -671,7 +671,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->W = c->W2 = 0;
     for (int W : Wc) {
         const size_t s1 = sizeof(int) * (((size_t)W * c->S * LTS + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * 32 +
-                          sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16 + 2048;
+                          sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16 + 2048 + 256;
         if (!c->W && W <= w1max && W != 32 && W != 20 && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
         const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (GYS + 1) +
                           sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192 + (o.orientation ? g.B : 0)) +

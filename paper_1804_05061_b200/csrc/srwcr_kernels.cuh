@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     float *CT = K + W * S * 32;                                   // [S][4][32]
     float *CB = CT + S * 128;                                     // [4][32] binless cell table
     float4 *ZT = reinterpret_cast<float4 *>(CB + 128);            // [2][64] the item's z-tap tables
-    float *shc = reinterpret_cast<float *>(ZT + 128);             // [B]
+    int *ZB = reinterpret_cast<int *>(ZT + 128);                  // [64] and control-tap bases
+    float *shc = reinterpret_cast<float *>(ZB + 64);              // [B]
     unsigned char *smap = reinterpret_cast<unsigned char *>(shc + B);  // [B] bin -> slot
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
     for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {   // z-tap tables in shared memory
         ZT[i] = a.t.cw[2][it.z0 + i];
         ZT[64 + i] = a.t.sw[2][it.z0 + i];
+        ZB[i] = a.t.cb[2][it.z0 + i];
     }
     __syncthreads();
     for (int s = threadIdx.x; s < ns; s += blockDim.x) smap[a.slotbins[it.slot_off + s]] = (unsigned char)s;
@@ -533,7 +535,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
                 }
             }
             if (!STATIC && z + 1 < it.z0 + it.zlen) {   // next slice: slide the layer window, issue its gathers
-                const int bz1 = a.t.cb[2][z + 1];
+                const int bz1 = ZB[z + 1 - it.z0];
                 while (gzl < bz1) {
 #pragma unroll
                     for (int n = 0; n < 3; ++n)
@@ -1188,8 +1190,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             __syncwarp();
         };
 
+        float4 cwzn = a.t.cw[2][it.z0], wzn = a.t.sw[2][it.z0];
+        int bzn = a.t.cb[2][it.z0];
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
-            const int bz = a.t.cb[2][z];
+            const int bz = bzn;
+            bzn = a.t.cb[2][min(z + 1, it.z0 + it.zlen - 1)];
             while (gzl < bz) {
                 retire(gzl, Ad[0]);
 #pragma unroll
@@ -1202,8 +1207,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
                 for (int v = 0; v < XV; ++v) Ad[3][v][0] = Ad[3][v][1] = Ad[3][v][2] = 0.f;
                 ++gzl;
             }
-            const float4 cwz = a.t.cw[2][z];
-            const float4 wz = a.t.sw[2][z];
+            const float4 cwz = cwzn, wz = wzn;     // this slice's z taps (loaded one slice ahead)
+            {
+                const int z1 = min(z + 1, it.z0 + it.zlen - 1);
+                cwzn = a.t.cw[2][z1];
+                wzn = a.t.sw[2][z1];
+            }
             const float *__restrict__ Fz = Frow + z * nxy;
             const float4 *__restrict__ MGz = a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx;
             // issue this line's streaming loads first: their latency overlaps the per-line
