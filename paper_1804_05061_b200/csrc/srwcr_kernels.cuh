@@ -1192,6 +1192,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
 
         float4 cwzn = a.t.cw[2][it.z0], wzn = a.t.sw[2][it.z0];
         int bzn = a.t.cb[2][it.z0];
+        float Fn[XV];   // F one slice ahead
+#pragma unroll
+        for (int v = 0; v < XV; ++v) Fn[v] = ld_stream(Frow + (long long)it.z0 * nxy + xv[v]);
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
             const int bz = bzn;
             bzn = a.t.cb[2][min(z + 1, it.z0 + it.zlen - 1)];
@@ -1221,7 +1224,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
             float4 mgl[XV];
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
-                Fl[v] = ld_stream(Fz + xv[v]);
+                Fl[v] = Fn[v];
+                Fn[v] = ld_stream(Fz + (z + 1 < it.z0 + it.zlen ? nxy : 0) + xv[v]);
                 mgl[v] = ld_stream4(MGz + xv[v]);
             }
             // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
