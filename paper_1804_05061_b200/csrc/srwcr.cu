@@ -473,6 +473,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     int ymax = 64, zmax = 64;
     const bool yfirst = true;  // pass 1: split rows before z (longer z-marches), measured ~1% on C5
     const bool yfirst2 = true; // pass 2 likewise (C5 pass 2 -7 %)
+    long long ips1 = 6, ips2 = 6;   // minimum items per SM (load balance vs per-item overhead)
+    if (const char *e = getenv("SRWCR_IPS1")) ips1 = std::max(1, atoi(e));
+    if (const char *e = getenv("SRWCR_IPS2")) ips2 = std::max(1, atoi(e));
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
@@ -495,7 +498,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         items.clear();
         npmax = 0;
         build_items((int)c->z0, (int)c->z1, items, xmax);
-        const bool small = (long long)items.size() < 6LL * nsm;
+        const bool small = (long long)items.size() < ips1 * nsm;
         const bool big_np = npmax > 12288;
         if ((small || big_np) && (ymax > 16 || zmax > 4)) {
             if (yfirst && ymax > 16) ymax /= 2;
@@ -515,7 +518,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         items2.clear();
         npmax = 0;
         build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
-        const bool small = (long long)items2.size() < 6LL * nsm;
+        const bool small = (long long)items2.size() < ips2 * nsm;
         if ((small || npmax > 16384) && (ymax > 16 || zmax > 4)) {
             if (yfirst2 && ymax > 16) ymax /= 2;
             else if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;

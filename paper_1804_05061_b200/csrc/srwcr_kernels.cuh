@@ -954,17 +954,28 @@ struct ExactGeo { int nx, ny, nz, L, Gx, Gy, GzExt, ndim; };
 // 1e-4 of an integer (the Parzen kink of c4): there the per-voxel derivative is
 // discontinuous and the side must be decided as the fp64 definition decides it.
 // (returned by value: reference outputs would force the caller's locals into local memory)
+// Called by a whole warp for one voxel: the lanes stage the 64 x ndim control values in
+// the warp's shared buffer sp[3][64] (independent loads in flight together), then every
+// lane sums them in the definition's order (identical result in every lane).
 struct ExactOut { float gx, gy, gz, g1p, c2; };
-__device__ __noinline__ ExactOut exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
-                                              const double4 *__restrict__ cwx64, const double4 *__restrict__ cwy64,
-                                              const double4 *__restrict__ cwz64, int bx, int by, int bz, int x,
-                                              int y, int z) {
+__device__ __forceinline__ ExactOut exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
+                                                 const double4 *__restrict__ cwx64, const double4 *__restrict__ cwy64,
+                                                 const double4 *__restrict__ cwz64, int bx, int by, int bz, int x,
+                                                 int y, int z, double *sp, int lane) {
     const double4 wx = cwx64[x], wy = cwy64[y], wz = cwz64[z];
     ExactOut o;
     const long long plane = (long long)g.Gx * g.Gy, cs = plane * g.GzExt;
     const long long nxy = (long long)g.nx * g.ny;
-    double u[3] = {0.0, 0.0, 0.0};
 #pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int tp = lane + 32 * h, n = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+        const long long s = (long long)(bz + n) * plane + (long long)(by + mm) * g.Gx + bx + l;
+        const bool in = bz + n < g.GzExt;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sp[c * 64 + tp] = (in && c < g.ndim) ? p64[c * cs + s] : 0.0;
+    }
+    __syncwarp();
+    double u[3] = {0.0, 0.0, 0.0};
     for (int n = 0; n < 4; ++n) {
         const double wn = d4(wz, n);
         if (wn == 0.0 || bz + n >= g.GzExt) continue;
@@ -977,10 +988,10 @@ __device__ __noinline__ ExactOut exact_sample(ExactGeo g, const double *__restri
                 const double wl = d4(wx, l);
                 if (wl == 0.0) continue;
                 const double w = wl * wm * wn;
-                const long long s = (long long)(bz + n) * plane + (long long)(by + mm) * g.Gx + bx + l;
-                u[0] += w * p64[s];
-                u[1] += w * p64[cs + s];
-                if (g.ndim == 3) u[2] += w * p64[2 * cs + s];
+                const int tp = n * 16 + mm * 4 + l;
+                u[0] += w * sp[tp];
+                u[1] += w * sp[64 + tp];
+                if (g.ndim == 3) u[2] += w * sp[128 + tp];
             }
         }
     }
@@ -1339,82 +1350,97 @@ __global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
 // beta, gamma tables and spatial weights (contracted directly over the 64 regions), and
 // its adjoint scattered onto the 64 control nodes with fp64 atomics.  When more voxels
 // were flagged than the list holds, the kernel scans the slab's MG flags instead.
+// One warp per deferred voxel: the 64 tap loads of each stage are spread over the lanes
+// (a thread-per-voxel version was a serial chain of ~250 dependent-latency loads, ~120 us).
+template <int ORI>
+__device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx, double *sp, int lane) {
+    const Geo &g = a.g;
+    const int x = (int)(idx % g.nx);
+    const long long t = idx / g.nx;
+    const int y = (int)(t % g.ny), z = (int)(t / g.ny) + a.mgz0;
+    const int bx = a.t.cb[0][x], by = a.t.cb[1][y], bz = a.t.cb[2][z];
+    const ExactOut e = exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
+                                    a.t.cw64[0], a.t.cw64[1], a.t.cw64[2], bx, by, bz, x, y, z, sp, lane);
+    const float Fv = a.F[(long long)z * g.nxy + (long long)y * g.nx + x];
+    const int a0 = min((int)Fv, g.L - 1);
+    float hlo, hhi;
+    parzen_pair(Fv - (float)a0, hlo, hhi);
+    const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
+    const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
+    // ORI 1: exact_sample's c2 is 2m at integer m (even) and 2n + 1 otherwise (odd)
+    int jm = 0, jp = 0;
+    float dm = 0.f, dp = 0.f, em = 0.f, ep = 0.f;
+    if (ORI == 1) {
+        const int c2i = (int)e.c2;
+        if ((c2i & 1) == 0) { const int k = c2i / 2; jm = 3 * k; jp = 3 * (k + 2); dm = -0.05f; dp = 0.05f; }
+        else { const int nb = (c2i - 1) / 2; jm = 3 * (nb + 1); jp = 3 * (nb + 2); dm = -e.g1p; dp = e.g1p; }
+        const float gF = (float)a0 + hhi;
+        const int am = jm / 3 - 1, ap = jp / 3 - 1;
+        em = (am >= 0 && am < g.B ? a.shiftc[am] : 0.f) - gF;
+        ep = (ap < g.B ? a.shiftc[ap] : 0.f) - gF;
+    }
+    float At = 0.f, Bt = 0.f, Gt = 0.f;   // ORI 1 accumulates into At only
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int tp = lane + 32 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+        if (w == 0.f) continue;
+        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        if (ORI == 0) {
+            At = fmaf(w, a.alpha[r], At);
+            Bt = fmaf(w, a.beta[r], Bt);
+            Gt = fmaf(w, fmaf(hlo, a.gamma[r * a.gstride + a0], hhi * a.gamma[r * a.gstride + a0 + 1]), Gt);
+        } else {
+            const float *row = a.gamma + r * a.gstride;
+            const float pm = fmaf(em * em, row[jm], fmaf(2.0f * em, row[jm + 1], row[jm + 2]));
+            const float pp = fmaf(ep * ep, row[jp], fmaf(2.0f * ep, row[jp + 1], row[jp + 2]));
+            At = fmaf(w, fmaf(dm, pm, dp * pp), At);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        At += __shfl_xor_sync(0xffffffffu, At, o);
+        if (ORI == 0) {
+            Bt += __shfl_xor_sync(0xffffffffu, Bt, o);
+            Gt += __shfl_xor_sync(0xffffffffu, Gt, o);
+        }
+    }
+    const float d = ORI == 0 ? e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt)) : a.invZ * At;
+    const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
+    const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int tp = lane + 32 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+        if (bz + nn >= g.GzExt || f4(wz, nn) == 0.f) continue;
+        const float w = f4(wz, nn) * f4(wy, mm) * f4(wx, l);
+        for (int c = 0; c < g.ndim; ++c)
+            atomicAdd(a.grad + (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l,
+                      (double)(w * dc[c]));
+    }
+    __syncwarp();   // sp is reused by the warp's next voxel
+}
+
 template <int ORI = 0>
 __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
+    __shared__ double spb[4][3 * 64];
     const Geo &g = a.g;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    double *sp = spb[wib];
     const int cnt = *a.xcount;
-    const bool scan = cnt > a.xcap;
+    const long long wid = blockIdx.x * 4LL + wib, nw = gridDim.x * 4LL;
+    if (cnt <= a.xcap) {
+        for (long long i = wid; i < cnt; i += nw) exact_fix_voxel<ORI>(a, a.xlist[i], sp, lane);
+        return;
+    }
+    // list overflowed: scan the slab's MG flags, 32 voxels per warp step
     const long long slab = (long long)g.nxy * a.mgz1;
-    const long long n = scan ? slab : cnt;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        long long idx;
-        if (scan) {
-            if (!(a.MG[i].x < 0.f)) continue;
-            idx = i;
-        } else {
-            idx = a.xlist[i];
-        }
-        const int x = (int)(idx % g.nx);
-        const long long t = idx / g.nx;
-        const int y = (int)(t % g.ny), z = (int)(t / g.ny) + a.mgz0;
-        const int bx = a.t.cb[0][x], by = a.t.cb[1][y], bz = a.t.cb[2][z];
-        const ExactOut e = exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
-                                        a.t.cw64[0], a.t.cw64[1], a.t.cw64[2], bx, by, bz, x, y, z);
-        const float Fv = a.F[(long long)z * g.nxy + (long long)y * g.nx + x];
-        const int a0 = min((int)Fv, g.L - 1);
-        float hlo, hhi;
-        parzen_pair(Fv - (float)a0, hlo, hhi);
-        const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
-        const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
-        float d;
-        if (ORI == 0) {
-            float At = 0.f, Bt = 0.f, Gt = 0.f;
-            for (int nn = 0; nn < 4; ++nn)
-                for (int mm = 0; mm < 4; ++mm)
-                    for (int l = 0; l < 4; ++l) {
-                        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
-                        if (w == 0.f) continue;
-                        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-                        At = fmaf(w, a.alpha[r], At);
-                        Bt = fmaf(w, a.beta[r], Bt);
-                        Gt = fmaf(w, fmaf(hlo, a.gamma[r * a.gstride + a0], hhi * a.gamma[r * a.gstride + a0 + 1]), Gt);
-                    }
-            d = e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt));
-        } else {
-            // exact_sample's c2 is 2m at integer m (even) and 2n + 1 otherwise (odd)
-            const int c2i = (int)e.c2;
-            int jm, jp;
-            float dm, dp;
-            if ((c2i & 1) == 0) { const int k = c2i / 2; jm = 3 * k; jp = 3 * (k + 2); dm = -0.05f; dp = 0.05f; }
-            else { const int nb = (c2i - 1) / 2; jm = 3 * (nb + 1); jp = 3 * (nb + 2); dm = -e.g1p; dp = e.g1p; }
-            const float gF = (float)a0 + hhi;
-            const int am = jm / 3 - 1, ap = jp / 3 - 1;
-            const float em = (am >= 0 && am < g.B ? a.shiftc[am] : 0.f) - gF, ep = (ap < g.B ? a.shiftc[ap] : 0.f) - gF;
-            float acc = 0.f;
-            for (int nn = 0; nn < 4; ++nn)
-                for (int mm = 0; mm < 4; ++mm)
-                    for (int l = 0; l < 4; ++l) {
-                        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
-                        if (w == 0.f) continue;
-                        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-                        const float *row = a.gamma + r * a.gstride;
-                        const float pm = fmaf(em * em, row[jm], fmaf(2.0f * em, row[jm + 1], row[jm + 2]));
-                        const float pp = fmaf(ep * ep, row[jp], fmaf(2.0f * ep, row[jp + 1], row[jp + 2]));
-                        acc = fmaf(w, fmaf(dm, pm, dp * pp), acc);
-                    }
-            d = a.invZ * acc;
-        }
-        const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
-        const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
-        for (int nn = 0; nn < 4; ++nn) {
-            if (bz + nn >= g.GzExt || f4(wz, nn) == 0.f) continue;
-            for (int mm = 0; mm < 4; ++mm)
-                for (int l = 0; l < 4; ++l) {
-                    const float w = f4(wz, nn) * f4(wy, mm) * f4(wx, l);
-                    for (int c = 0; c < g.ndim; ++c)
-                        atomicAdd(a.grad + (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l,
-                                  (double)(w * dc[c]));
-                }
+    for (long long b = wid * 32; b < slab; b += nw * 32) {
+        const long long i = b + lane;
+        unsigned fl = __ballot_sync(0xffffffffu, i < slab && a.MG[i].x < 0.f);
+        while (fl) {
+            const int k = __ffs(fl) - 1;
+            fl &= fl - 1;
+            exact_fix_voxel<ORI>(a, b + k, sp, lane);
         }
     }
 }
