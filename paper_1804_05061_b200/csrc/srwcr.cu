@@ -88,6 +88,7 @@ struct srwcr_ctx {
     int gstride = 0;                                 // row stride of the gamma table
     int pz0 = 0, pzb1 = 0, pz1 = 0;                  // node layers the slab reads: [pz0, pz1), bases < pzb1
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
+    unsigned *ticket = nullptr;   // k_combine's last-CTA ticket
     double *S_out = nullptr;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
     double Z = 0;
@@ -324,11 +325,10 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out;
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
     ca.NQ = c->NQ; ca.gstride = c->gstride;
+    ca.ticket = c->ticket; ca.Dout = c->Dout;   // D reduced by the launch's last CTA
     const int wpb = 8;
     if (c->opt.orientation) k_combineA<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
     else k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
-    CKL();
-    k_reduce_D<<<1, 1024, 0, c->stream>>>(c->dterm, c->reg, (int)c->R, c->Z, c->Dout);
     CKL();
     return SRWCR_OK;
 }
@@ -476,6 +476,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     long long ips1 = 6, ips2 = 6;   // minimum items per SM (load balance vs per-item overhead)
     if (const char *e = getenv("SRWCR_IPS1")) ips1 = std::max(1, atoi(e));
     if (const char *e = getenv("SRWCR_IPS2")) ips2 = std::max(1, atoi(e));
+    int zmin = 20;
+    if (const char *e = getenv("SRWCR_ZMIN")) zmin = atoi(e);
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
@@ -500,6 +502,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         build_items((int)c->z0, (int)c->z1, items, xmax);
         const bool small = (long long)items.size() < ips1 * nsm;
         const bool big_np = npmax > 12288;
+        // z-marches shorter than ~20 slices re-load the 4-layer FFD window too often: accept
+        // 3 items per SM rather than split z below that (C5 on 8 ranks: -14 % per rank)
+        if (!big_np && ymax <= 16 && zmax / 2 < zmin && (long long)items.size() >= 3LL * nsm) break;
         if ((small || big_np) && (ymax > 16 || zmax > 4)) {
             if (yfirst && ymax > 16) ymax /= 2;
             else if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
@@ -519,6 +524,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         npmax = 0;
         build_items((int)c->z0, (int)c->z1, items2, 32 * c->XV2);
         const bool small = (long long)items2.size() < ips2 * nsm;
+        if (npmax <= 16384 && ymax <= 16 && zmax / 2 < zmin && (long long)items2.size() >= 3LL * nsm) break;
         if ((small || npmax > 16384) && (ymax > 16 || zmax > 4)) {
             if (yfirst2 && ymax > 16) ymax /= 2;
             else if (zmax >= ymax / 2 && zmax > 4) zmax /= 2;
@@ -647,6 +653,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->dterm, sizeof(double) * c->R));
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
     CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
+    CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
+    CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
     CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
     CK(cudaMalloc(&c->beta, sizeof(float) * c->R));
@@ -733,7 +741,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             cudaFree(tmp);
         }
     }
-    c->launches_per_eval = 9;  // params->f32, 3 window-max, pass 1, combine, reduce_D, pass 2, exact fix
+    c->launches_per_eval = 6;  // prep (phi + x-max, y/z-max), pass 1, combine (+ D), pass 2, exact fix
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -780,17 +788,13 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
     // only the node layers this rank's slab reads: taps of slices [z0, z1) (all of them on
     // one rank), converted to fp32, and their tap-window max |phi_c| (x, y into scratch,
     // z -> float4) for pass 1's rounding bound
-    k_params_to_f32<<<592, 256, 0, c->stream>>>(pd, c->phi, c->g, c->pz0, c->pz1);
-    CKL();
     {
         const size_t G = (size_t)c->g.Gx * c->g.Gy * c->g.Gz;
-        float *s1 = c->phimax + 4 * G, *s2 = c->phimax + 7 * G;
-        k_window_max<0><<<592, 256, 0, c->stream>>>(c->phi, s1, c->g, c->pz0, c->pz1);
+        float *s1 = c->phimax + 4 * G;
+        k_prep_phi_wx<<<592, 256, 0, c->stream>>>(pd, c->phi, s1, c->g, c->pz0, c->pz1);
         CKL();
-        k_window_max<1><<<592, 256, 0, c->stream>>>(s1, s2, c->g, c->pz0, c->pz1);
-        CKL();
-        k_window_max_z4<<<592, 256, 0, c->stream>>>(s2, reinterpret_cast<float4 *>(c->phimax), c->g, c->pz0,
-                                                    c->pzb1, c->pz1);
+        k_prep_tol<<<592, 256, 0, c->stream>>>(s1, reinterpret_cast<float4 *>(c->phimax), c->g, c->pz0, c->pzb1,
+                                               c->pz1);
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));

@@ -761,12 +761,39 @@ struct CombineArgs {
     float *alpha, *beta, *gamma;
     const double *NQ;           // ORI 1: [R][B][2] dynamic counts N' (lo, hi halves)
     int gstride;                // ORI 1: row stride of gamma = 3 (B + 2)
+    unsigned *ticket;           // last-CTA ticket (0 between launches)
+    double *Dout;               // [2] D, #retained regions
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
     return v;
+}
+
+// The last CTA of a combine launch (atomic ticket) reduces D = (1/Z) sum_r dterm[r] in a
+// fixed order (deterministic): out[0] = D, out[1] = #retained; it re-arms the ticket.
+__device__ __forceinline__ void combine_tail(const CombineArgs &a) {
+    __shared__ bool last;
+    __shared__ double sd[256], sc[256];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    double s = 0, c = 0;
+    for (int r = threadIdx.x; r < a.R; r += blockDim.x) { s += __ldcg(a.dterm + r); c += __ldcg(a.reg + (long long)r * 6 + 4); }
+    sd[threadIdx.x] = s;
+    sc[threadIdx.x] = c;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) { sd[threadIdx.x] += sd[threadIdx.x + o]; sc[threadIdx.x] += sc[threadIdx.x + o]; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) { a.Dout[0] = sd[0] / a.Z; a.Dout[1] = sc[0]; *a.ticket = 0u; }
 }
 
 __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, double &N, double &S) {
@@ -782,7 +809,7 @@ __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, doubl
     }
 }
 
-__global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
+__device__ __forceinline__ void combine_region(const CombineArgs &a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= a.R) return;
@@ -857,7 +884,7 @@ __device__ __forceinline__ void bin_NS_A(const CombineArgs &a, int r, int b, dou
     }
 }
 
-__global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
+__device__ __forceinline__ void combineA_region(const CombineArgs &a) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     if (r >= a.R) return;
@@ -910,6 +937,15 @@ __global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
         row[3 * j + 1] = T1;
         row[3 * j + 2] = T2;
     }
+}
+
+__global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
+    combine_region(a);
+    combine_tail(a);
+}
+__global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
+    combineA_region(a);
+    combine_tail(a);
 }
 
 // D = (1/Z) sum_r dterm[r] in a fixed order (deterministic); out[0] = D, out[1] = #retained
@@ -1484,6 +1520,54 @@ __global__ void k_window_max(const float *__restrict__ in, float *__restrict__ o
         for (int d = 0; d < 4; ++d)
             if (k + d < G) m = fmaxf(m, fabsf(in[i + d * st]));
         out[i] = m;
+    }
+}
+
+// Fused prep, step 1: fp64 params -> fp32 phi (as k_params_to_f32) and, per node, the
+// max |phi_c| over the 4 nodes [k, k+3] along x (k_window_max<0>), node layers [zlo, zhi)
+__global__ void k_prep_phi_wx(const double *__restrict__ p, float *__restrict__ phi, float *__restrict__ wx, Geo g,
+                              int zlo, int zhi) {
+    const long long plane = (long long)g.Gx * g.Gy;
+    const long long cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
+        const long long i = (long long)zlo * plane + j;
+        const long long gz = i / plane, xy = i - gz * plane;
+        const int gx = (int)(xy % g.Gx);
+        const bool live = gz < g.GzExt;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const double *q = p + (c * g.GzExt + gz) * plane + xy;
+            float v = 0.f, m = 0.f;
+            if (c < g.ndim && live) {
+                v = (float)q[0];
+                m = fabsf(v);
+#pragma unroll
+                for (int d = 1; d < 4; ++d)
+                    if (gx + d < g.Gx) m = fmaxf(m, fabsf((float)q[d]));
+            }
+            phi[c * cs + i] = v;
+            wx[c * cs + i] = m;
+        }
+    }
+}
+
+// Fused prep, step 2: the y and z window max of step 1's x-max (k_window_max<1> and
+// k_window_max_z4 in one pass), base layers [zlo, zb) reading node layers up to zhi
+__global__ void k_prep_tol(const float *__restrict__ wx, float4 *__restrict__ out, Geo g, int zlo, int zb, int zhi) {
+    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zb - zlo) * plane;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
+        const long long i = (long long)zlo * plane + j;
+        const int k = (int)(i / plane), gy = (int)((i - (long long)k * plane) / g.Gx);
+        float m[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int dz = 0; dz < 4; ++dz)
+#pragma unroll
+                for (int dy = 0; dy < 4; ++dy)
+                    if (k + dz < zhi && gy + dy < g.Gy)
+                        m[c] = fmaxf(m[c], __ldg(wx + c * cs + i + dz * plane + dy * g.Gx));
+        out[i] = make_float4(4e-6f * m[0], 4e-6f * m[1], 4e-6f * m[2], 0.f);
     }
 }
 
