@@ -256,6 +256,7 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     if (n == 0) return SRWCR_OK;
     if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);   // fixed-image bins (both orientations)
     else if (c->opt.orientation) k_pass1<XV, false, 512, 1><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    else if (XV == 1 && c->W <= 6 && !getenv("SRWCR_NOSMALL")) k_pass1<1, false, 192><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     CKL();
     return SRWCR_OK;
@@ -277,7 +278,8 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
         CKL();
         k_exact_fix<1><<<296, 128, 0, c->stream>>>(a);
     } else {
-        k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
         k_exact_fix<0><<<296, 128, 0, c->stream>>>(a);
     }
@@ -296,6 +298,8 @@ static srwcr_status set_smem_t(int maxsm) {
     CK0(cudaFuncSetAttribute(k_pass1<XV, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass1<XV, false, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<1, false, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass2<1, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass2<XV, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     return SRWCR_OK;
 }

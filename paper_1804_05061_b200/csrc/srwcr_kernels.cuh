@@ -317,8 +317,11 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
 // feeds two slot groups: 2*slot(n) the counts N'_{r,n|n+1} = sum w h_{n|n+1}(m) and
 // 2*slot(n)+1 the first moments S'_{r,n|n+1} = sum w h_{n|n+1}(m) (g1(F) - c_n); the
 // second moments of F are static (no binless channel).
+// MAXT <= 256 (small items of fine spatial lattices, few warps per CTA): register budget for
+// 4 resident CTAs per SM -- their latency is otherwise exposed at 2 CTAs (Table VIII
+// 256x256x99: 4.1 -> 2.9 ms per evaluation with pass 2 at 5 CTAs)
 template <int XV, bool STATIC, int MAXT = 512, int ORI = 0>
-__global__ void __launch_bounds__(MAXT, 1) k_pass1(PassArgs a) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
     const int B = g.B, W = a.W, S = a.S;
@@ -1083,7 +1086,7 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 // -/+ w1'(f), or at integer m = k bins k-1, k+1 with -/+ 0.05 (reading c4); no alpha /
 // beta terms.
 template <int XV, int MAXT = 512, int ORI = 0>
-__global__ void __launch_bounds__(MAXT, 1) k_pass2(PassArgs a) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Geo &g = a.g;
     const int B = g.B, W = a.W;
