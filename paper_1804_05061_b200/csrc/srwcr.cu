@@ -89,6 +89,7 @@ struct srwcr_ctx {
     int pz0 = 0, pzb1 = 0, pz1 = 0;                  // node layers the slab reads: [pz0, pz1), bases < pzb1
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     unsigned *ticket = nullptr;   // k_combine's last-CTA ticket
+    double *dpart = nullptr;      // k_combine's per-CTA partial sums
     double *S_out = nullptr;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
     double Z = 0;
@@ -329,7 +330,7 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out;
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
     ca.NQ = c->NQ; ca.gstride = c->gstride;
-    ca.ticket = c->ticket; ca.Dout = c->Dout;   // D reduced by the launch's last CTA
+    ca.ticket = c->ticket; ca.Dout = c->Dout; ca.part = c->dpart;   // D reduced by the launch's last CTA
     const int wpb = 8;
     if (c->opt.orientation) k_combineA<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
     else k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
@@ -658,6 +659,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
     CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
     CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
+    CK(cudaMalloc(&c->dpart, sizeof(double) * 2 * (size_t)((c->R + 7) / 8)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
     CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
@@ -976,7 +978,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
-                    c->beta, c->gamma};
+                    c->beta, c->gamma, c->ticket, c->dpart};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

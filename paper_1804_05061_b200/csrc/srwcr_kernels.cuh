@@ -765,6 +765,7 @@ struct CombineArgs {
     const double *NQ;           // ORI 1: [R][B][2] dynamic counts N' (lo, hi halves)
     int gstride;                // ORI 1: row stride of gamma = 3 (B + 2)
     unsigned *ticket;           // last-CTA ticket (0 between launches)
+    double *part;               // [2 * gridDim] per-CTA partial sums of dterm, retained
     double *Dout;               // [2] D, #retained regions
 };
 
@@ -774,13 +775,20 @@ __device__ __forceinline__ double warp_sum_d(double v) {
     return v;
 }
 
-// The last CTA of a combine launch (atomic ticket) reduces D = (1/Z) sum_r dterm[r] in a
-// fixed order (deterministic): out[0] = D, out[1] = #retained; it re-arms the ticket.
-__device__ __forceinline__ void combine_tail(const CombineArgs &a) {
+// D = (1/Z) sum_r dterm[r], deterministic: each CTA sums its regions' dterm and retained
+// flags in warp order into part[2*blockIdx]; the last CTA (atomic ticket) sums the
+// partials in block order into Dout = {D, #retained} and re-arms the ticket.
+__device__ __forceinline__ void combine_tail(const CombineArgs &a, double dt, double rt) {
     __shared__ bool last;
     __shared__ double sd[256], sc[256];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) { sd[warp] = dt; sc[warp] = rt; }
     __syncthreads();
     if (threadIdx.x == 0) {
+        double s = 0, c = 0;
+        for (int w = 0; w < nw; ++w) { s += sd[w]; c += sc[w]; }
+        a.part[2 * blockIdx.x] = s;
+        a.part[2 * blockIdx.x + 1] = c;
         __threadfence();
         last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     }
@@ -788,7 +796,7 @@ __device__ __forceinline__ void combine_tail(const CombineArgs &a) {
     if (!last) return;
     __threadfence();
     double s = 0, c = 0;
-    for (int r = threadIdx.x; r < a.R; r += blockDim.x) { s += __ldcg(a.dterm + r); c += __ldcg(a.reg + (long long)r * 6 + 4); }
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) { s += __ldcg(a.part + 2 * i); c += __ldcg(a.part + 2 * i + 1); }
     sd[threadIdx.x] = s;
     sc[threadIdx.x] = c;
     __syncthreads();
@@ -812,31 +820,36 @@ __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, doubl
     }
 }
 
-__device__ __forceinline__ void combine_region(const CombineArgs &a) {
+// returns (in dt, rt; lane 0 of the region's warp) the region's dterm and retained flag
+__device__ __forceinline__ void combine_region(const CombineArgs &a, double &dt, double &rt) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    dt = rt = 0.0;
     if (r >= a.R) return;
     const int B = a.B;
+    double Nv[4], Sv[4];    // this lane's bins b = lane + 32 k (B <= 128)
     double Nr = 0, Sr = 0;
-    for (int b = lane; b < B; b += 32) {
-        double N, S;
-        bin_NS(a, r, b, N, S);
-        if (a.S_out) a.S_out[(long long)r * B + b] = S;
-        Nr += N;
-        Sr += S;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int b = lane + 32 * k;
+        Nv[k] = Sv[k] = 0.0;
+        if (b < B) {
+            bin_NS(a, r, b, Nv[k], Sv[k]);
+            if (a.S_out) a.S_out[(long long)r * B + b] = Sv[k];
+        }
+        Nr += Nv[k];
+        Sr += Sv[k];
     }
     Nr = warp_sum_d(Nr);
     Sr = warp_sum_d(Sr);
     const double mu = Nr > 0 ? Sr / Nr : 0.0;
     double btw = 0;
-    for (int b = lane; b < B; b += 32) {
-        double N, S;
-        bin_NS(a, r, b, N, S);
-        if (N > 0.0) {
-            const double d = S / N - mu;
-            btw += N * d * d;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+        if (Nv[k] > 0.0) {
+            const double d = Sv[k] / Nv[k] - mu;
+            btw += Nv[k] * d * d;
         }
-    }
     btw = warp_sum_d(btw);
     const double pr = Nr / a.Z;
     double sig2 = 0, omcr = 0;
@@ -847,16 +860,19 @@ __device__ __forceinline__ void combine_region(const CombineArgs &a) {
         if (sig2 > a.eps_sigma) { ret = true; omcr = Vr / Tr; }
     }
     if (lane == 0) {
-        a.dterm[r] = ret ? Nr * omcr : 0.0;
+        dt = ret ? Nr * omcr : 0.0;
+        rt = ret ? 1.0 : 0.0;
+        a.dterm[r] = dt;
         a.alpha[r] = ret ? (float)((1.0 - omcr) / sig2) : 0.f;
         a.beta[r] = ret ? (float)(omcr * mu / sig2) : 0.f;
         double *rg = a.reg + (long long)r * 6;
-        rg[0] = pr; rg[1] = sig2; rg[2] = mu; rg[3] = omcr; rg[4] = ret ? 1.0 : 0.0; rg[5] = a.Z;
+        rg[0] = pr; rg[1] = sig2; rg[2] = mu; rg[3] = omcr; rg[4] = rt; rg[5] = a.Z;
     }
-    for (int b = lane; b < B; b += 32) {
-        double N, S;
-        bin_NS(a, r, b, N, S);
-        a.gamma[(long long)r * B + b] = (ret && N > 0.0) ? (float)((S / N) / sig2) : 0.f;
+    const double is2 = ret ? 1.0 / sig2 : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const int b = lane + 32 * k;
+        if (b < B) a.gamma[(long long)r * B + b] = (ret && Nv[k] > 0.0) ? (float)((Sv[k] / Nv[k]) * is2) : 0.f;
     }
 }
 
@@ -887,9 +903,10 @@ __device__ __forceinline__ void bin_NS_A(const CombineArgs &a, int r, int b, dou
     }
 }
 
-__device__ __forceinline__ void combineA_region(const CombineArgs &a) {
+__device__ __forceinline__ void combineA_region(const CombineArgs &a, double &dt, double &rt) {
     const int lane = threadIdx.x & 31;
     const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    dt = rt = 0.0;
     if (r >= a.R) return;
     const int B = a.B;
     double Nr = 0, Sr = 0, Qr = 0, s2n = 0;
@@ -916,7 +933,9 @@ __device__ __forceinline__ void combineA_region(const CombineArgs &a) {
         if (sig2 > a.eps_sigma) { ret = true; omcr = Vr / Tr; }
     }
     if (lane == 0) {
-        a.dterm[r] = ret ? Nr * omcr : 0.0;
+        dt = ret ? Nr * omcr : 0.0;
+        rt = ret ? 1.0 : 0.0;
+        a.dterm[r] = dt;
         a.alpha[r] = 0.f;
         a.beta[r] = 0.f;
         double *rg = a.reg + (long long)r * 6;
@@ -943,12 +962,14 @@ __device__ __forceinline__ void combineA_region(const CombineArgs &a) {
 }
 
 __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
-    combine_region(a);
-    combine_tail(a);
+    double dt, rt;
+    combine_region(a, dt, rt);
+    combine_tail(a, dt, rt);
 }
 __global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
-    combineA_region(a);
-    combine_tail(a);
+    double dt, rt;
+    combineA_region(a, dt, rt);
+    combine_tail(a, dt, rt);
 }
 
 // D = (1/Z) sum_r dterm[r] in a fixed order (deterministic); out[0] = D, out[1] = #retained
