@@ -277,12 +277,12 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
     if (c->opt.orientation) {
         k_pass2<XV, 512, 1><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
-        k_exact_fix<1><<<296, 128, 0, c->stream>>>(a);
+        k_exact_fix<1><<<1184, 128, 0, c->stream>>>(a);
     } else {
         if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
-        k_exact_fix<0><<<296, 128, 0, c->stream>>>(a);
+        k_exact_fix<0><<<1184, 128, 0, c->stream>>>(a);
     }
     CKL();
     return SRWCR_OK;
