@@ -79,6 +79,7 @@ struct srwcr_ctx {
     Item *items = nullptr, *items_full = nullptr;  // this rank's slab / whole volume
     Item *items2 = nullptr;                          // pass 2 (its own x-chunking)
     int nitems2 = 0, XV2 = 1;
+    bool MC = false;   // multi-cell items (fine spatial lattices): several x-cells per item
     ItemW *itemw = nullptr, *itemw_full = nullptr;
     int *slotbins = nullptr;                         // slot lists of both item lists
     int nitems = 0, nitems_full = 0;
@@ -255,7 +256,14 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     a.itemw = full ? c->itemw_full : c->itemw;
     if (full) a.MG = nullptr;   // whole-volume create-time passes: no (m, dM/dy) output
     if (n == 0) return SRWCR_OK;
-    if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);   // fixed-image bins (both orientations)
+    if (XV == 1 && c->MC) {   // fine lattices: multi-cell items
+        const bool small = c->W <= 6;
+        if (stat && small) k_pass1<1, true, 192, 0, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+        else if (stat) k_pass1<1, true, 512, 0, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+        else if (small) k_pass1<1, false, 192, 0, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+        else k_pass1<1, false, 512, 0, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
+    }
+    else if (stat) k_pass1<XV, true><<<n, 32 * c->W, c->smem1, c->stream>>>(a);   // fixed-image bins (both orientations)
     else if (c->opt.orientation) k_pass1<XV, false, 512, 1><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     else if (XV == 1 && c->W <= 6 && !getenv("SRWCR_NOSMALL")) k_pass1<1, false, 192><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
     else k_pass1<XV, false><<<n, 32 * c->W, c->smem1, c->stream>>>(a);
@@ -279,7 +287,9 @@ static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
         CKL();
         k_exact_fix<1><<<1184, 128, 0, c->stream>>>(a);
     } else {
-        if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        if (XV == 1 && c->MC && c->W2 <= 6) k_pass2<1, 192, 0, true><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else if (XV == 1 && c->MC) k_pass2<1, 512, 0, true><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
         k_exact_fix<0><<<1184, 128, 0, c->stream>>>(a);
@@ -301,6 +311,12 @@ static srwcr_status set_smem_t(int maxsm) {
     CK0(cudaFuncSetAttribute(k_pass2<XV>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass1<1, false, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass2<1, 192>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<1, true, 192, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<1, true, 512, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<1, false, 192, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass1<1, false, 512, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass2<1, 192, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
+    CK0(cudaFuncSetAttribute(k_pass2<1, 512, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     CK0(cudaFuncSetAttribute(k_pass2<XV, 512, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
     return SRWCR_OK;
 }
@@ -473,6 +489,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         if (const char *e = getenv("SRWCR_XV")) c->XV = std::min(c->XV, std::max(1, atoi(e)));
         c->XV2 = c->XV;  // pass 2 amortises its per-line gamma/alpha/beta contractions over XV2 x 32 voxels
         if (const char *e = getenv("SRWCR_XV2")) c->XV2 = std::min(c->XV, std::max(1, atoi(e)));
+        // fine spatial lattices: pack whole x-cells into one 32-voxel item when at least two fit
+        int maxw = 0;
+        for (auto &r : xr) maxw = std::max(maxw, r.second);
+        c->MC = o.orientation == 0 && c->XV == 1 && c->XV2 == 1 && 2 * maxw <= 32 && !getenv("SRWCR_NOMC");
     }
     const int xmax = 32 * c->XV;
     int ymax = 64, zmax = 64;
@@ -485,8 +505,21 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (const char *e = getenv("SRWCR_ZMIN")) zmin = atoi(e);
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
+    // MC: consecutive whole x-cells, at most MC_CELLS of them and xm voxels per item
+    auto xruns_mc = [&](int xm) {
+        std::vector<std::pair<int, int>> out;
+        auto cells = runs(c->h_sb[0], 0, g.nx, 1 << 30);
+        size_t i = 0;
+        while (i < cells.size()) {
+            int x0 = cells[i].first, w = cells[i].second, k = 1;
+            while (i + k < cells.size() && k < MC_XRN - 3 && w + cells[i + k].second <= xm) w += cells[i + k++].second;
+            out.push_back({x0, w});
+            i += k;
+        }
+        return out;
+    };
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
-        auto xr = runs(c->h_sb[0], 0, g.nx, xm);
+        auto xr = c->MC ? xruns_mc(xm) : runs(c->h_sb[0], 0, g.nx, xm);
         auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
         auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
         for (auto &zz : zr)
@@ -595,13 +628,16 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             it.nslots = ns;
             it.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
             ItemW &iw = w[i];
-            for (int l = 0; l < 4; ++l) iw.sx[l] = iw.sy[l] = iw.sz[l] = 0.0;
+            for (int l = 0; l < 8; ++l) iw.sx[l] = 0.0;
+            for (int l = 0; l < 4; ++l) iw.sy[l] = iw.sz[l] = 0.0;
             const int lo[3] = {it.x0, it.y0, it.z0}, len[3] = {it.xlen, it.ylen, it.zlen};
             double *dst[3] = {iw.sx, iw.sy, iw.sz};
             for (int ax = 0; ax < 3; ++ax)
                 for (int k = lo[ax]; k < lo[ax] + len[ax]; ++k) {
                     const float4 q = c->h_sw[ax][k];
-                    dst[ax][0] += q.x; dst[ax][1] += q.y; dst[ax][2] += q.z; dst[ax][3] += q.w;
+                    // x: per relative x-region (the voxel's cell offset in a multi-cell item)
+                    const int off = ax == 0 ? c->h_sb[0][k] - c->h_sb[0][it.x0] : 0;
+                    dst[ax][off + 0] += q.x; dst[ax][off + 1] += q.y; dst[ax][off + 2] += q.z; dst[ax][off + 3] += q.w;
                 }
         }
         CK(cudaMalloc(dw, sizeof(ItemW) * n));
@@ -615,7 +651,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         TRY(scan_items(items2, &tmpw, true));
         if (tmpw) cudaFree(tmpw);
     }
-    c->S = smax;
+    c->S = smax + (c->MC ? 1 : 0);   // MC: + the binless slot
     c->S2 = s2max;
     CK(cudaMalloc(&c->slotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
     CK(cudaMemcpy(c->slotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
@@ -687,11 +723,13 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (const char *e = getenv("SRWCR_W2")) w2max = atoi(e);
     c->W = c->W2 = 0;
     for (int W : Wc) {
-        const size_t s1 = sizeof(int) * (((size_t)W * c->S * LTS + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * 32 +
-                          sizeof(float) * ((size_t)c->S * 128 + 128 + g.B) + (size_t)g.B + 16 + 2048 + 256;
+        const size_t ltsv = c->MC ? 2 * MC_XRN + 1 : LTS, ks = c->MC ? 8 * MC_XRN : 32;
+        const size_t s1 = sizeof(int) * (((size_t)W * c->S * ltsv + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * ks +
+                          sizeof(float) * ((size_t)c->S * 4 * ks + 128 + g.B) + (size_t)g.B + 16 + 2048 + 256;
         if (!c->W && W <= w1max && W != 32 && W != 20 && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
-        const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (GYS + 1) +
-                          sizeof(float) * (64 * (size_t)c->S2 + (c->S2 + 1) + 128 + W * 192 + (o.orientation ? g.B : 0)) +
+        const size_t xrn = c->MC ? MC_XRN : 4, gys = c->MC ? MC_XRN + 1 : GYS;
+        const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (gys + xrn / 4) +
+                          sizeof(float) * (16 * xrn * (size_t)c->S2 + (c->S2 + 1) + 32 * xrn + W * 192 + (o.orientation ? g.B : 0)) +
                           (((o.orientation ? 3 * (g.B + 2) : g.B) + 15) & ~15) +
                           sizeof(float) * npmax;
         if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }

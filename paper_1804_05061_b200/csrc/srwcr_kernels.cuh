@@ -23,6 +23,7 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int LTS = 9;          // line-table slot stride: 8 entries (4 x-taps x {lo, hi}) + 1 pad
 constexpr int GYS = 5;          // pass-2 per-warp gamma table: float4 per (bin, x-tap), 4 + 1 pad per bin
 constexpr int MAXW = 16;        // max warps per CTA
+constexpr int MC_XRN = 8;       // multi-cell items: x-regions per item (<= 5 spatial x-cells)
 
 struct Tables {                 // per-axis B-spline taps, index = voxel coordinate on that axis
     const int *cb[3];           // control lattice: tap base floor(i/delta)          (Eq 17)
@@ -48,7 +49,8 @@ struct Item {
     float cI;                   // binless moment shift of the item (mean of M over the box)
     int pad;
 };
-struct ItemW { double sx[4], sy[4], sz[4]; };  // per-item sums of the fp32 spatial weights
+// per-item sums of the fp32 spatial weights: sx per relative x-region (MC items span cells)
+struct ItemW { double sx[8], sy[4], sz[4]; };
 
 struct PassArgs {
     Geo g;
@@ -320,16 +322,25 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
 // MAXT <= 256 (small items of fine spatial lattices, few warps per CTA): register budget for
 // 4 resident CTAs per SM -- their latency is otherwise exposed at 2 CTAs (Table VIII
 // 256x256x99: 4.1 -> 2.9 ms per evaluation with pass 2 at 5 CTAs)
-template <int XV, bool STATIC, int MAXT = 512, int ORI = 0>
+// MC (multi-cell items, fine spatial lattices, ORI 0): an item spans up to MC_CELLS
+// spatial x-cells; every lane keeps its own cell offset lcx, the tables are indexed by the
+// relative x-region xr = lcx + l (XRN = 8 of them: 16 entries per slot), the warp-uniform
+// halving path is off, and the binless channels (q', g1 - cI) are one more slot of the
+// line tables (index ns) with their own fixed-point exponents.
+template <int XV, bool STATIC, int MAXT = 512, int ORI = 0, bool MC = false>
 __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int XRN = MC ? MC_XRN : 4;      // x-regions per item
+    constexpr int E = 2 * XRN;                // line-table entries per slot
+    constexpr int LTSV = MC ? 2 * MC_XRN + 1 : LTS;
+    constexpr int KS = 4 * E;                 // column-table floats per slot (entry*4 + n)
     const Geo &g = a.g;
     const int B = g.B, W = a.W, S = a.S;
-    const int ltsz = (W * S * LTS + 3) & ~3;                      // keep K 16-byte aligned
-    int *LT = reinterpret_cast<int *>(smem);                      // [W][S][LTS]
-    float *K = reinterpret_cast<float *>(LT + ltsz);              // [W][S][32]  (entry*4 + n)
-    float *CT = K + W * S * 32;                                   // [S][4][32]
-    float *CB = CT + S * 128;                                     // [4][32] binless cell table
+    const int ltsz = (W * S * LTSV + 3) & ~3;                     // keep K 16-byte aligned
+    int *LT = reinterpret_cast<int *>(smem);                      // [W][S][LTSV]
+    float *K = reinterpret_cast<float *>(LT + ltsz);              // [W][S][KS]
+    float *CT = K + W * S * KS;                                   // [S][4][KS]
+    float *CB = CT + S * 4 * KS;                                  // [4][32] binless cell table (!MC)
     float4 *ZT = reinterpret_cast<float4 *>(CB + 128);            // [2][64] the item's z-tap tables
     int *ZB = reinterpret_cast<int *>(ZT + 128);                  // [64] and control-tap bases
     float *shc = reinterpret_cast<float *>(ZB + 64);              // [B]
@@ -338,12 +349,12 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const Item it = a.items[blockIdx.x];
     const int ns = it.nslots;                       // list entries (ORI 1: every bin)
-    const int nsl = ORI ? 2 * ns : ns;                // slots (ORI 1: two groups per bin)
+    const int nsl = ORI ? 2 * ns : ns + (MC ? 1 : 0); // slots (ORI 1: two groups per bin; MC: + binless)
     const int nwords = (nsl + 31) >> 5;
 
     for (int i = threadIdx.x; i < ltsz; i += blockDim.x) LT[i] = 0;
-    for (int i = threadIdx.x; i < W * S * 32; i += blockDim.x) K[i] = 0.f;
-    for (int i = threadIdx.x; i < nsl * 128 + 128; i += blockDim.x) (i < nsl * 128 ? CT[i] : CB[i - nsl * 128]) = 0.f;
+    for (int i = threadIdx.x; i < W * S * KS; i += blockDim.x) K[i] = 0.f;
+    for (int i = threadIdx.x; i < nsl * 4 * KS + 128; i += blockDim.x) (i < nsl * 4 * KS ? CT[i] : CB[i - nsl * 4 * KS]) = 0.f;
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
         shc[i] = STATIC ? 0.f : a.shiftc[i];
         smap[i] = 0xFF;
@@ -359,12 +370,13 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
     const int xn0 = a.t.cb[0][it.x0];
     const int nxn = a.t.cb[0][it.x0 + it.xlen - 1] + 4 - xn0;
-    int xv[XV], relx[XV];
+    int xv[XV], relx[XV], lcx[XV];
     float4 cwx[XV], swx[XV];
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
         const bool ok = lane + 32 * v < it.xlen;
         xv[v] = ok ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+        lcx[v] = MC ? a.t.sb[0][xv[v]] - cx : 0;
         relx[v] = a.t.cb[0][xv[v]] - xn0;
         cwx[v] = a.t.cw[0][xv[v]];
         swx[v] = ok ? a.t.sw[0][xv[v]] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -380,6 +392,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
 #pragma unroll
         for (int v = 0; v < XV; ++v) mx = fmaxf(mx, f4(swx[v], l));
         El[l] = (int)(__reduce_max_sync(FULL, __float_as_uint(mx)) >> 23);
+    }
+    if (MC) {   // one exponent for all x-taps: an entry mixes lanes of different cells (taps)
+        const int em = max(max(El[0], El[1]), max(El[2], El[3]));
+#pragma unroll
+        for (int l = 0; l < 4; ++l) El[l] = em;
     }
     const int le = (lane & 7) >> 1;                               // fold lane's x-tap
     const int El_e = le == 0 ? El[0] : le == 1 ? El[1] : le == 2 ? El[2] : El[3];
@@ -406,8 +423,8 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     const float *__restrict__ Mv = a.M;
     __syncthreads();
 
-    int *LTw = LT + warp * S * LTS;
-    float *Kw = K + warp * S * 32;
+    int *LTw = LT + warp * S * LTSV;
+    float *Kw = K + warp * S * KS;
 
     for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
         const int cby = a.t.cb[1][y];
@@ -471,6 +488,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             float4 *MGrow = a.MG + ((long long)(z - a.mgz0) * g.ny + y) * nx;
             int a0[XV], slot[XV];
             float lo[XV], hi[XV], lo2[XV], hi2[XV];
+            float qv[XV], abv[XV];   // MC: binless channels per voxel
             float bq[4] = {0.f, 0.f, 0.f, 0.f}, ba[4] = {0.f, 0.f, 0.f, 0.f};
             float amax = 0.f, amax2 = 0.f;
 #pragma unroll
@@ -520,10 +538,15 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                         lo[v] = hlo * A;
                         hi[v] = hhi * A;
                         amax = fmaxf(amax, fabsf(A));
+                        if (MC) {
+                            qv[v] = q;
+                            abv[v] = Ab;
+                        } else {
 #pragma unroll
-                        for (int l = 0; l < 4; ++l) {
-                            bq[l] = fmaf(f4(swx[v], l), q, bq[l]);
-                            ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
+                            for (int l = 0; l < 4; ++l) {
+                                bq[l] = fmaf(f4(swx[v], l), q, bq[l]);
+                                ba[l] = fmaf(f4(swx[v], l), Ab, ba[l]);
+                            }
                         }
                     } else {   // model bins from m; F gives the moment g1(F) = a0 + w1(F - a0)
                         slot[v] = 2 * smap[n];
@@ -550,7 +573,31 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                 gather(z + 1);
             }
             // ---- binless: warp-reduce (x-tap, channel) and fold the z-taps into bacc
-            if (!STATIC && ORI == 0) {
+            float iscQ = 1.f, iscB = 1.f;
+            if (!STATIC && ORI == 0 && MC) {   // binless slot ns: entry 2 xr + {0: q', 1: g1 - cI}
+                float mq = 0.f, mb = 0.f;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) { mq = fmaxf(mq, qv[v]); mb = fmaxf(mb, fabsf(abv[v])); }
+                const int EQ = (int)(__reduce_max_sync(FULL, __float_as_uint(mq)) >> 23);
+                const int EB = (int)(__reduce_max_sync(FULL, __float_as_uint(mb)) >> 23);
+                const float scQ = exp2i(min(274 - El[0] - EQ, 120)), scB = exp2i(min(274 - El[0] - EB, 120));
+                iscQ = exp2i(-min(274 - El[0] - EQ, 120));
+                iscB = exp2i(-min(274 - El[0] - EB, 120));
+                const int chA = (lane >> 2) & 1;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    int *row = LTw + ns * LTSV + 2 * lcx[v] + chA;
+                    const float va = chA ? abv[v] * scB : qv[v] * scQ, vb = chA ? qv[v] * scQ : abv[v] * scB;
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        const int lr = (l + q4) & 3;
+                        const float w = f4(swr[v], l);
+                        atomicAdd(row + 2 * lr, __float_as_int(fmaf(va, w, 12582912.f)) - 0x4B400000);
+                        atomicAdd(row + 2 * lr + 1 - 2 * chA, __float_as_int(fmaf(vb, w, 12582912.f)) - 0x4B400000);
+                    }
+                }
+            }
+            if (!STATIC && ORI == 0 && !MC) {
                 const float bv[8] = {bq[0], ba[0], bq[1], ba[1], bq[2], ba[2], bq[3], ba[3]};
                 const float tot = halving8(bv, lane);          // value (lane>>2) = 2*l + ch
                 bacc = fmaf(f4(wz, lane & 3), tot, bacc);
@@ -581,7 +628,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             bool same = true;
 #pragma unroll
             for (int v = 0; v < XV; ++v) same = same && (ORI ? slot[v] : a0[v]) == af;
-            uniform = __all_sync(FULL, same);
+            uniform = !MC && __all_sync(FULL, same);
             if (uniform) {
                 float vv[8];
 #pragma unroll
@@ -598,7 +645,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                 const float tot = halving8(vv, lane);
                 if ((lane & 3) == 0) {   // one bin: straight into the column table (no line table, no fold)
                     const int ent = lane >> 2;
-                    float4 *kp = reinterpret_cast<float4 *>(Kw + slot[0] * 32 + ent * 4);
+                    float4 *kp = reinterpret_cast<float4 *>(Kw + slot[0] * KS + ent * 4);
                     float4 k4 = *kp;
                     k4.x = fmaf(wz.x, tot, k4.x);
                     k4.y = fmaf(wz.y, tot, k4.y);
@@ -609,7 +656,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             } else if (STATIC) {
 #pragma unroll
                 for (int v = 0; v < XV; ++v) {
-                    float *row = reinterpret_cast<float *>(LTw + slot[v] * LTS);
+                    float *row = reinterpret_cast<float *>(LTw + slot[v] * LTSV + 2 * lcx[v]);
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
                         const int lr = (l + q4) & 3;
@@ -626,7 +673,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                 const int chA = (lane >> 2) & 1;
 #pragma unroll
                 for (int v = 0; v < XV; ++v) {
-                    int *row = LTw + slot[v] * LTS + chA;
+                    int *row = LTw + slot[v] * LTSV + 2 * lcx[v] + chA;
                     const float va = chA ? hi[v] : lo[v], vb = chA ? lo[v] : hi[v];
 #pragma unroll
                     for (int l = 0; l < 4; ++l) {
@@ -651,6 +698,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             //      K[slot][ent][n] += wz_n * LT[slot][ent]
             unsigned bits[4] = {0u, 0u, 0u, 0u};
             int cnt = 0;
+            if (MC && !STATIC) {   // the binless slot is touched by every line
+                bits[ns >> 5] |= 1u << (ns & 31);
+                wmask[ns >> 5] |= 1u << (ns & 31);
+                cnt = 1;
+            }
             if (uniform && !ORI) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k)
@@ -665,25 +717,32 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                         mine |= ((slot[v] >> 5) == k) ? 1u << (slot[v] & 31) : 0u;
                         if (ORI) mine |= (((slot[v] + 1) >> 5) == k) ? 1u << ((slot[v] + 1) & 31) : 0u;
                     }
-                    bits[k] = __reduce_or_sync(FULL, mine);
+                    bits[k] |= __reduce_or_sync(FULL, mine);
                     wmask[k] |= bits[k];
-                    cnt += __popc(bits[k]);
                 }
             }
+            if (!uniform) {
+                cnt = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) cnt += __popc(bits[k]);
+            }
+            const int nwf = MC ? max(nwords, (ns >> 5) + 1) : nwords;
             __syncwarp();
-            const int ent = lane & 7;
+            const int ent = lane & (E - 1);
             for (int c0 = 0; c0 < cnt; c0 += 32) {
-                const int myslot = mask_select(bits, nwords, c0 + lane);
+                const int myslot = mask_select(bits, nwf, c0 + lane);
                 const int rmax = min(cnt - c0, 32);
-                for (int r = 0; r < rmax; r += 4) {
-                    const int idx = r + (lane >> 3);
+                for (int r = 0; r < rmax; r += 32 / E) {
+                    const int idx = r + lane / E;
                     const int s = __shfl_sync(FULL, myslot, idx & 31);
                     if (idx < rmax) {
-                        int *lp = LTw + s * LTS + ent;
+                        int *lp = LTw + s * LTSV + ent;
                         const int iv = *lp;
                         *lp = 0;
-                        const float val = STATIC ? __int_as_float(iv) : (float)iv * isc_g[ORI ? (s & 1) : 0];
-                        float4 *kp = reinterpret_cast<float4 *>(Kw + s * 32 + ent * 4);
+                        float isc = isc_g[ORI ? (s & 1) : 0];
+                        if (MC && s == ns) isc = (ent & 1) ? iscB : iscQ;
+                        const float val = STATIC ? __int_as_float(iv) : (float)iv * isc;
+                        float4 *kp = reinterpret_cast<float4 *>(Kw + s * KS + ent * 4);
                         float4 k4 = *kp;
                         k4.x = fmaf(wz.x, val, k4.x);
                         k4.y = fmaf(wz.y, val, k4.y);
@@ -702,15 +761,18 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             while (bw) {
                 const int s = 32 * k + __ffs(bw) - 1;
                 bw &= bw - 1;
-                const float val = Kw[s * 32 + lane];
-                Kw[s * 32 + lane] = 0.f;
-                if (val != 0.f) {
 #pragma unroll
-                    for (int mm = 0; mm < 4; ++mm) atomicAdd(CT + (s * 4 + mm) * 32 + lane, f4(swy, mm) * val);
+                for (int j = lane; j < KS; j += 32) {
+                    const float val = Kw[s * KS + j];
+                    Kw[s * KS + j] = 0.f;
+                    if (val != 0.f) {
+#pragma unroll
+                        for (int mm = 0; mm < 4; ++mm) atomicAdd(CT + (s * 4 + mm) * KS + j, f4(swy, mm) * val);
+                    }
                 }
             }
         }
-        if (!STATIC && bacc != 0.f) {
+        if (!STATIC && !MC && bacc != 0.f) {
 #pragma unroll
             for (int mm = 0; mm < 4; ++mm) atomicAdd(CB + mm * 32 + lane, f4(swy, mm) * bacc);
         }
@@ -718,18 +780,29 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     }
     __syncthreads();
     // ---- item done: flush to global.  CT entry (s, m, e): e = 8*l + 4*ch + n
-    for (int t = threadIdx.x; t < nsl * 128; t += blockDim.x) {
+    for (int t = threadIdx.x; t < nsl * 4 * KS; t += blockDim.x) {
         const float val = CT[t];
-        if (val == 0.f) continue;
-        const int s = t >> 7, mm = (t >> 5) & 3, e = t & 31;
-        const int l = e >> 3, ch = (e >> 2) & 1, n = e & 3;
+        const int s = t / (4 * KS), mm = (t / KS) & 3, e = t % KS;
+        const int l = e >> 3, ch = (e >> 2) & 1, n = e & 3;   // l: relative x-region
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        if (MC && !STATIC && s == ns) {   // binless: Q_r += Q' + 2 cI S' + cI^2 N
+            if (ch == 0) {
+                const ItemW &iw = a.itemw[blockIdx.x];
+                const double N = iw.sx[l] * iw.sy[mm] * iw.sz[n];
+                if (N > 0.0) {
+                    const double c = cI;
+                    atomicAdd(a.Qt + r, (double)val + 2.0 * c * (double)CT[t + 4] + c * c * N);
+                }
+            }
+            continue;
+        }
+        if (val == 0.f) continue;
         if (ORI)   // slot 2k: counts N' -> NQ, slot 2k+1: first moments S' -> SQ
             atomicAdd(((s & 1) ? a.SQ : a.NQ) + (r * B + a.slotbins[it.slot_off + (s >> 1)]) * 2 + ch, (double)val);
         else
             atomicAdd(a.SQ + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
     }
-    if (!STATIC && ORI == 0 && threadIdx.x < 64) {
+    if (!STATIC && ORI == 0 && !MC && threadIdx.x < 64) {
         // binless: Q_r += Q' + 2 cI S' + cI^2 N  with N = sum of the item's spatial weights
         const int l = threadIdx.x >> 4, mm = (threadIdx.x >> 2) & 3, n = threadIdx.x & 3;
         const double Qp = CB[mm * 32 + (2 * l) * 4 + n], Sp = CB[mm * 32 + (2 * l + 1) * 4 + n];
@@ -1106,9 +1179,14 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 // psi'_ra(g1(F)) (k_combineA's table, 3 columns per bin, bins -1..L+1): bins n, n+1 with
 // -/+ w1'(f), or at integer m = k bins k-1, k+1 with -/+ 0.05 (reading c4); no alpha /
 // beta terms.
-template <int XV, int MAXT = 512, int ORI = 0>
+// MC (multi-cell items, ORI 0): the region tables are indexed (n, m, xr) with XRN
+// relative x-regions; per line the item's bins are contracted over z per x-region
+// (GZs[bin][xr]) and each voxel sums its own 4 x-regions lcx..lcx+3.
+template <int XV, int MAXT = 512, int ORI = 0, bool MC = false>
 __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int XRN = MC ? MC_XRN : 4;
+    constexpr int GYSV = MC ? MC_XRN + 1 : GYS;
     const Geo &g = a.g;
     const int B = g.B, W = a.W;
     const Item it = a.items[blockIdx.x];
@@ -1124,14 +1202,14 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
     // gamma tables are indexed by the item's bin list (a0 and a0+1 of every slot,
     // sorted, so bin a0+1 always sits right after a0): capacity GB = a.S2
     const int GB = a.S2;
-    float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][GB][GYS]
-    float4 *GZ = GY + W * GB * GYS;                               // [W][GB]
-    float *gl = reinterpret_cast<float *>(GZ + W * GB);           // [64][GB] gamma of the 64 regions
-    int *gbins = reinterpret_cast<int *>(gl + 64 * GB);           // [GB+1] the bin list, count
+    float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][GB][GYSV]
+    float4 *GZ = GY + W * GB * GYSV;                              // [W][GB] (MC: [W][GB][XRN] floats)
+    float *gl = reinterpret_cast<float *>(GZ + W * GB * (XRN / 4)); // [16 XRN][GB] gamma of the regions
+    int *gbins = reinterpret_cast<int *>(gl + 16 * XRN * GB);     // [GB+1] the bin list, count
     unsigned char *gmap = reinterpret_cast<unsigned char *>(gbins + GB + 1);  // [B] bin -> list index
-    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [64]
-    float *bl = al + 64;                                          // [64]
-    float *shc2 = bl + 64;                                        // [B] (ORI 1) the bins' moment shifts
+    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [16 XRN]
+    float *bl = al + 16 * XRN;                                    // [16 XRN]
+    float *shc2 = bl + 16 * XRN;                                  // [B] (ORI 1) the bins' moment shifts
     float *RB = shc2 + (ORI ? B : 0);                             // [W][3][64] retiring-layer row buffer
     float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
 
@@ -1144,17 +1222,18 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
         gmap[b] = (unsigned char)i;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < 64 * nb2; i += blockDim.x) {
+    // region (n, m, l) of the item (l: relative x-region) at index (n * 4 + m) * XRN + l
+    for (int i = threadIdx.x; i < 16 * XRN * nb2; i += blockDim.x) {
         const int reg = i / nb2, k = i - reg * nb2;
-        const int l = reg & 3, mm = (reg >> 2) & 3, n = reg >> 4;
+        const int l = reg % XRN, mm = (reg / XRN) & 3, n = reg / (4 * XRN);
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        gl[reg * GB + k] = __ldg(a.gamma + r * a.gstride + gbins[k]);
+        gl[reg * GB + k] = cx + l < g.Kx ? __ldg(a.gamma + r * a.gstride + gbins[k]) : 0.f;
     }
-    for (int i = threadIdx.x; i < 64; i += blockDim.x) {
-        const int l = i & 3, mm = (i >> 2) & 3, n = i >> 4;
+    for (int i = threadIdx.x; i < 16 * XRN; i += blockDim.x) {
+        const int l = i % XRN, mm = (i / XRN) & 3, n = i / (4 * XRN);
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        al[i] = __ldg(a.alpha + r);
-        bl[i] = __ldg(a.beta + r);
+        al[i] = cx + l < g.Kx ? __ldg(a.alpha + r) : 0.f;
+        bl[i] = cx + l < g.Kx ? __ldg(a.beta + r) : 0.f;
     }
     if (ORI)
         for (int i = threadIdx.x; i < B; i += blockDim.x) shc2[i] = a.shiftc[i];
@@ -1163,7 +1242,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
     for (int i = threadIdx.x; i < W * 192; i += blockDim.x) RB[i] = 0.f;
 
     bool lok[XV];
-    int xv[XV], relx[XV], cbx[XV];
+    int xv[XV], relx[XV], cbx[XV], lcx[XV];
     float4 swx[XV], cwr[XV];
     const int q4 = lane & 3;
 #pragma unroll
@@ -1172,6 +1251,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
         xv[v] = lok[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
         cbx[v] = a.t.cb[0][xv[v]];
         relx[v] = cbx[v] - xn0;
+        lcx[v] = MC ? a.t.sb[0][xv[v]] - cx : 0;
         swx[v] = a.t.sw[0][xv[v]];
         const float4 w = a.t.cw[0][xv[v]];
         cwr[v] = q4 == 0 ? w : q4 == 1 ? make_float4(w.y, w.z, w.w, w.x)
@@ -1179,8 +1259,9 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
     }
     const int nx = g.nx, nxy = (int)g.nxy;
     float *rbw = RB + warp * 192;
-    float4 *GYw = GY + warp * GB * GYS;
-    float4 *GZw = GZ + warp * GB;
+    float4 *GYw = GY + warp * GB * GYSV;
+    float4 *GZw = GZ + warp * GB * (XRN / 4);
+    float *GZs = reinterpret_cast<float *>(GZw);   // MC: [GB][XRN]
     __syncthreads();
 
     for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
@@ -1191,18 +1272,24 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
 
         // gamma of the item's bins contracted over the y-taps:
         // GYw[k][l] = float4_n( sum_m wy_m gamma[(n, m, l)][bin k] )
-        for (int i = lane; i < nb2 * 16; i += 32) {
-            const int k = i >> 4, l = (i >> 2) & 3, n = i & 3;
-            const float *src = gl + (n * 16 + l) * GB + k;       // region (n, m, l): index n*16 + m*4 + l
-            const float val = swy.x * src[0] + swy.y * src[4 * GB] + swy.z * src[8 * GB] + swy.w * src[12 * GB];
-            reinterpret_cast<float *>(GYw + k * GYS + l)[n] = val;
+        for (int i = lane; i < nb2 * 4 * XRN; i += 32) {
+            const int k = i / (4 * XRN), l = (i >> 2) % XRN, n = i & 3;
+            const float *src = gl + (n * 4 * XRN + l) * GB + k;  // region (n, m, l): (n*4 + m)*XRN + l
+            const float val = swy.x * src[0] + swy.y * src[XRN * GB] + swy.z * src[2 * XRN * GB] + swy.w * src[3 * XRN * GB];
+            reinterpret_cast<float *>(GYw + k * GYSV + l)[n] = val;
         }
         // alpha (lanes 0-15) / beta (lanes 16-31) contracted over y: lane = 16*ab + 4*l + n
-        float abY = 0.f;
-        if (ORI == 0) {
+        // (MC: alpha in abY, beta in abY2, lane = 4*xr + n)
+        float abY = 0.f, abY2 = 0.f;
+        if (ORI == 0 && !MC) {
             const int l = (lane >> 2) & 3, n = lane & 3;
             const float *src = (lane < 16 ? al : bl) + n * 16 + l;
             abY = swy.x * src[0] + swy.y * src[4] + swy.z * src[8] + swy.w * src[12];
+        } else if (ORI == 0) {
+            const int l = lane >> 2, n = lane & 3;
+            const float *sa = al + n * 4 * XRN + l, *sb2 = bl + n * 4 * XRN + l;
+            abY = swy.x * sa[0] + swy.y * sa[XRN] + swy.z * sa[2 * XRN] + swy.w * sa[3 * XRN];
+            abY2 = swy.x * sb2[0] + swy.y * sb2[XRN] + swy.z * sb2[2 * XRN] + swy.w * sb2[3 * XRN];
         }
         __syncwarp();
 
@@ -1301,7 +1388,8 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
             }
             // alpha~/beta~ of this line: reduce lane values over the z-taps, then broadcast
             float ay[4], by4[4];
-            if (ORI == 0) {
+            float tA = 0.f, tB = 0.f;   // MC: lane 4 xr holds alpha~ / beta~ of x-region xr
+            if (ORI == 0 && !MC) {
                 float t = f4(wz, lane & 3) * abY;
                 t += __shfl_xor_sync(FULL, t, 1);
                 t += __shfl_xor_sync(FULL, t, 2);
@@ -1310,11 +1398,20 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
                     ay[l] = __shfl_sync(FULL, t, 4 * l);
                     by4[l] = __shfl_sync(FULL, t, 16 + 4 * l);
                 }
+            } else if (ORI == 0) {
+                tA = f4(wz, lane & 3) * abY;
+                tB = f4(wz, lane & 3) * abY2;
+                tA += __shfl_xor_sync(FULL, tA, 1);
+                tB += __shfl_xor_sync(FULL, tB, 1);
+                tA += __shfl_xor_sync(FULL, tA, 2);
+                tB += __shfl_xor_sync(FULL, tB, 2);
             }
             // gamma of the item's bins contracted over z for this line: GZw[bin] = float4_l
-            for (int i = lane; i < 4 * nb2; i += 32) {
-                const int k = i >> 2, l = i & 3;
-                reinterpret_cast<float *>(GZw + k)[l] = dot4(wz, GYw[k * GYS + l]);
+            // (MC: GZs[bin][xr])
+            for (int i = lane; i < XRN * nb2; i += 32) {
+                const int k = i / XRN, l = i % XRN;
+                if (MC) GZs[i] = dot4(wz, GYw[k * GYSV + l]);
+                else reinterpret_cast<float *>(GZw + k)[l] = dot4(wz, GYw[k * GYSV + l]);
             }
             int a0[XV];
             float hlo[XV], hhi[XV];
@@ -1339,7 +1436,20 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
                 float dval;   // dD/dm * Z
                 if (ORI == 0) {
                     const int gk = gmap[a0[v]];
-                    const float4 G0 = GZw[gk], G1 = GZw[gk + 1];
+                    float4 G0, G1;
+                    if (MC) {
+                        const float *g0 = GZs + gk * XRN + lcx[v];
+                        G0 = make_float4(g0[0], g0[1], g0[2], g0[3]);
+                        G1 = make_float4(g0[XRN], g0[XRN + 1], g0[XRN + 2], g0[XRN + 3]);
+#pragma unroll
+                        for (int l = 0; l < 4; ++l) {
+                            ay[l] = __shfl_sync(FULL, tA, 4 * (lcx[v] + l));
+                            by4[l] = __shfl_sync(FULL, tB, 4 * (lcx[v] + l));
+                        }
+                    } else {
+                        G0 = GZw[gk];
+                        G1 = GZw[gk + 1];
+                    }
                     const float At = fmaf(sw.w, ay[3], fmaf(sw.z, ay[2], fmaf(sw.y, ay[1], sw.x * ay[0])));
                     const float Bt = fmaf(sw.w, by4[3], fmaf(sw.z, by4[2], fmaf(sw.y, by4[1], sw.x * by4[0])));
                     const float Gt = fmaf(hlo[v], dot4(sw, G0), hhi[v] * dot4(sw, G1));
