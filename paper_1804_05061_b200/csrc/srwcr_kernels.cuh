@@ -1428,8 +1428,14 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
                 // voxels whose per-voxel derivative is decided by the fp64 definition
                 const float4 mg = mgl[v];
                 float m = mg.x, dgx = mg.y, dgy = mg.z, dgz = mg.w;
-                const bool ex = m < 0.f;
+                bool ex = m < 0.f;
                 m = ex ? -1.0f - m : m;
+                if (ex) {   // rare: a tap window at rest (u = 0 exactly in fp32 and fp64: t = 0, m = the
+                            // voxel's own value on both sides) cannot have flagged a coordinate, and
+                            // its Parzen-kink side is decided identically -- no fp64 recompute needed
+                    const float4 tl = __ldg(a.tolw + ((long long)bz * g.Gy + cby) * g.Gx + cbx[v]);
+                    ex = !(tl.x == 0.f && tl.y == 0.f && tl.z == 0.f);
+                }
                 const float4 sw = swx[v];
                 const int n = min(max((int)floorf(m), 0), g.L - 1);
                 const float fm = m - (float)n;
