@@ -74,7 +74,10 @@ typedef struct {
     int32_t moment_shift;      /* 1 (default): per-fixed-bin shift of the accumulated moments
                                   estimated at Phi = 0; 0: shift = bin index.  Exact algebra
                                   either way; it only conditions the fp32 partial sums. */
-    int32_t use_graph;         /* reserved (accepted, no effect): srwcr_eval issues ordinary launches */
+    int32_t use_graph;         /* 1 (default): srwcr_eval with device params (and device or NULL
+                                  grad) on one rank replays a CUDA graph of the
+                                  evaluation captured on first use for that pointer pair
+                                  (re-captured when a pointer changes); 0: ordinary launches */
 } srwcr_options;
 
 /* Fills *opt with defaults: orientation 0, inputs_normalized 0, device 0, nranks 1,
@@ -85,11 +88,11 @@ srwcr_status srwcr_default_options(srwcr_options *opt);
  * return), normalises them, builds the per-axis B-spline tables (Eq 8, Eq 17),
  * accumulates the static fixed-image counts N[r][a] = sum_x w_r(x) h(a - F(x))
  * (Eq 3; they do not depend on Phi) and estimates the per-bin moment shifts
- * with one identity pass.  (options.use_graph is reserved: an evaluation is 9
- * ordinary launches on the context's stream.)
+ * with one identity pass.  (An evaluation is 6 kernels on the context's stream,
+ * replayed as one CUDA graph when options.use_graph applies.)
  *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2
  *   spacing_mm[3]      voxel spacing (> 0)
- *   intensity_bins     L + 1, in [2, 256] (paper: L = 31)
+ *   intensity_bins     L + 1, in [2, 128] (paper: L = 31); orientation 1: <= 83
  *   spatial_bins[3]    k cells per axis (>= 0; 0 = one region on that axis)
  *   control_spacing_mm[3]  control-node spacing (> 0); paper: delta = [5,5,5]
  *   opt                NULL = defaults

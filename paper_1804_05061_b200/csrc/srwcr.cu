@@ -100,6 +100,11 @@ struct srwcr_ctx {
     bool begun = false;
     // stats
     int64_t launches = 0;
+    cudaGraphExec_t gexec = nullptr;            // captured evaluation (options.use_graph)
+    const double *g_params = nullptr;           //   for these params / grad pointers
+    const double *g_grad = nullptr;
+    int64_t g_kernels = 0;                      //   kernels per replay
+    bool g_timing = false;                      //   with the per-pass event records
     int launches_per_eval = 0;
     bool timing = false;
     cudaEvent_t ev[5]{};  // pass1 start, pass1 end, combine end, pass2 end, prep start
@@ -818,17 +823,17 @@ extern "C" srwcr_status srwcr_num_params(const srwcr_ctx *c, int64_t *n, int64_t
     return SRWCR_OK;
 }
 
-static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
+static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev = -1) {
     if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned by an earlier CUDA error");
     if (!params) return fail(c, SRWCR_EINVAL, "params is NULL");
     CK(cudaSetDevice(c->dev));
     const double *pd = params;
-    if (!is_device_ptr(params)) {
+    if (!(pdev < 0 ? is_device_ptr(params) : pdev != 0)) {
         CK(cudaMemcpyAsync(c->params64, params, sizeof(double) * c->nparams, cudaMemcpyHostToDevice, c->stream));
         pd = c->params64;
     }
     c->cur_params = pd;
-    if (c->timing) CK(cudaEventRecord(c->ev[4], c->stream));
+    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[4], c->stream, cudaEventRecordExternal));
     // only the node layers this rank's slab reads: taps of slices [z0, z1) (all of them on
     // one rank), converted to fp32, and their tap-window max |phi_c| (x, y into scratch,
     // z -> float4) for pass 1's rounding bound
@@ -842,27 +847,33 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params) {
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
-    if (c->timing) CK(cudaEventRecord(c->ev[0], c->stream));
+    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
     TRY(launch_pass1(c, false));
-    if (c->timing) CK(cudaEventRecord(c->ev[1], c->stream));
+    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[1], c->stream, cudaEventRecordExternal));
     return SRWCR_OK;
 }
 
-static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, bool reduce_grad) {
+// combine, pass 2 and the result copies (stream-ordered, no host synchronisation:
+// also the body of the captured evaluation graph)
+static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_grad, int gdev = -1) {
     TRY(run_combine(c));
-    if (c->timing) CK(cudaEventRecord(c->ev[2], c->stream));
+    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[2], c->stream, cudaEventRecordExternal));
     double *gd = nullptr;
-    bool grad_dev = grad && is_device_ptr(grad);
+    const bool grad_dev = grad && (gdev < 0 ? is_device_ptr(grad) : gdev != 0);
     if (grad) {
         gd = grad_dev ? grad : c->grad64;
         CK(cudaMemsetAsync(gd, 0, sizeof(double) * c->nparams, c->stream));
         TRY(launch_pass2(c, gd));
         if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
     }
-    if (c->timing) CK(cudaEventRecord(c->ev[3], c->stream));
+    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal));
     CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (grad) CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (grad && !grad_dev) CK(cudaMemcpyAsync(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost, c->stream));
+    return SRWCR_OK;
+}
+
+static srwcr_status eval_finish(srwcr_ctx *c, double *value) {
     CK(cudaStreamSynchronize(c->stream));
     if (c->timing) {
         cudaEventElapsedTime(&c->ms[0], c->ev[0], c->ev[1]);
@@ -879,9 +890,53 @@ static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, boo
     return SRWCR_OK;
 }
 
+static srwcr_status eval_end_impl(srwcr_ctx *c, double *value, double *grad, bool reduce_grad) {
+    TRY(eval_end_enqueue(c, grad, reduce_grad));
+    return eval_finish(c, value);
+}
+
+// One evaluation as a CUDA graph (options.use_graph, single rank, device params and
+// gradient): the 6 kernels, 3 memsets, 2 result copies (and, with timing on, the per-pass
+// event records) are captured once per (params, grad, timing) and replayed with one
+// cudaGraphLaunch.
+static srwcr_status eval_graph(srwcr_ctx *c, const double *params, double *value, double *grad) {
+    CK(cudaSetDevice(c->dev));
+    if (!c->gexec || c->g_params != params || c->g_grad != grad || c->g_timing != c->timing) {
+        if (c->gexec) cudaGraphExecDestroy(c->gexec);
+        c->gexec = nullptr;
+        const int64_t l0 = c->launches;
+        CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+        srwcr_status st = eval_begin_impl(c, params, 1);
+        if (st == SRWCR_OK) st = eval_end_enqueue(c, grad, false, 1);
+        cudaGraph_t gr = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+        c->g_kernels = c->launches - l0;
+        c->launches = l0;
+        if (st != SRWCR_OK || e != cudaSuccess) {
+            if (gr) cudaGraphDestroy(gr);
+            return st != SRWCR_OK ? st : fail(c, SRWCR_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
+        }
+        const cudaError_t e2 = cudaGraphInstantiate(&c->gexec, gr, 0);
+        cudaGraphDestroy(gr);
+        if (e2 != cudaSuccess) {
+            c->gexec = nullptr;
+            return fail(c, SRWCR_ECUDA, "cudaGraphInstantiate: %s", cudaGetErrorString(e2));
+        }
+        c->g_params = params;
+        c->g_grad = grad;
+        c->g_timing = c->timing;
+    }
+    CK(cudaGraphLaunch(c->gexec, c->stream));
+    c->launches += c->g_kernels;
+    return eval_finish(c, value);
+}
+
 extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
     if (!c) return SRWCR_EINVAL;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
+    if (c->opt.use_graph && !c->comm && !c->poisoned && params && is_device_ptr(params) &&
+        (!grad || is_device_ptr(grad)))
+        return eval_graph(c, params, value, grad);
     TRY(eval_begin_impl(c, params));
     TRY(allreduce(c, c->SQ, stats_count(c)));
     return eval_end_impl(c, value, grad, true);
@@ -1014,6 +1069,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     cudaSetDevice(c->dev);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
+    if (c->gexec) cudaGraphExecDestroy(c->gexec);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma, c->ticket, c->dpart};

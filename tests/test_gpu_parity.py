@@ -262,3 +262,40 @@ def test_edge_geometries(dims, L, delta, kcells, orientation):
     if np.linalg.norm(go) > 1e-12:
         assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
     g.close()
+
+
+def test_graph_replay_matches_eager_launches():
+    """options.use_graph: srwcr_eval with device buffers replays a captured CUDA graph
+    (re-captured when a pointer changes); it must give the eager launches' result, follow
+    new parameter values written into the same buffer, and count its kernels."""
+    torch = pytest.importorskip("torch")
+    import synth
+    import paper_1804_05061_b200 as S
+    name = "C3"
+    cfg = synth.config(name, REDUCED[name])
+    F, M = synth.make_pair(name, 1, cfg["dims"])
+    ge = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], use_graph=False)
+    gg = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], use_graph=True)
+    p1 = synth.make_params(ge.params_shape, "small", 1)
+    p2 = synth.make_params(ge.params_shape, "large", 2)
+    pt = torch.from_numpy(p1).cuda()
+    gt = torch.empty_like(pt)
+    n0 = gg.stats()["launches_total"]
+    for p in (p1, p2, p1):
+        pt.copy_(torch.from_numpy(p))
+        Dg, _ = gg.eval(pt, grad=gt)
+        De, ge_grad = ge.eval(p)
+        assert rel(Dg, De) <= 2e-7
+        assert rel_l2(gt.cpu().numpy(), ge_grad) <= 1e-5
+    st = gg.stats()
+    assert st["launches_total"] - n0 == 3 * st["launches_per_eval"]
+    gt2 = torch.empty_like(pt)   # new gradient buffer: re-capture
+    Dg2, _ = gg.eval(pt, grad=gt2)
+    assert rel(Dg2, Dg) <= 2e-7 and rel_l2(gt2.cpu().numpy(), gt.cpu().numpy()) <= 1e-5
+    gg.set_timing(True)          # per-pass event records captured into the graph
+    gg.eval(pt, grad=gt2)
+    gg.eval(pt, grad=gt2)
+    st = gg.stats()
+    assert st["ms_pass1"] > 0 and st["ms_pass2"] > 0 and st["ms_total"] >= st["ms_pass1"] + st["ms_pass2"]
+    ge.close()
+    gg.close()
