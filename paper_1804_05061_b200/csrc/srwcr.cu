@@ -80,6 +80,7 @@ struct srwcr_ctx {
     Item *items2 = nullptr;                          // pass 2 (its own x-chunking)
     int nitems2 = 0, XV2 = 1;
     bool MC = false;   // multi-cell items (fine spatial lattices): several x-cells per item
+    int zrn = 4;       //   and their z-regions (z-cells per item + 3)
     ItemW *itemw = nullptr, *itemw_full = nullptr;
     int *slotbins = nullptr;                         // slot lists of both item lists
     int nitems = 0, nitems_full = 0;
@@ -244,6 +245,7 @@ static PassArgs pass_args(srwcr_ctx *c) {
     a.F = c->F; a.M = c->M; a.phi = c->phi; a.shiftc = c->shiftc; a.items = c->items; a.itemw = c->itemw;
     a.tolw = reinterpret_cast<const float4 *>(c->phimax);
     a.MG = c->MG; a.mgz0 = (int)c->z0; a.mgz1 = (int)(c->z1 - c->z0);
+    a.zrn = c->zrn;
     a.xlist = c->xlist; a.xcount = c->xcount; a.xcap = c->xcap;
     a.slotbins = c->slotbins; a.SQ = c->SQ; a.Qt = c->Qt; a.W = c->W; a.S = c->S; a.S2 = c->S2;
     a.NQ = c->NQ; a.gstride = c->gstride;
@@ -510,23 +512,30 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (const char *e = getenv("SRWCR_ZMIN")) zmin = atoi(e);
     std::vector<Item> items, items_full, items2;
     size_t npmax = 0;
-    // MC: consecutive whole x-cells, at most MC_CELLS of them and xm voxels per item
-    auto xruns_mc = [&](int xm) {
+    // MC: consecutive whole cells along an axis, at most XRN - 3 of them and len voxels per item
+    auto cruns_mc = [&](const std::vector<int> &sb, int lo, int hi, int len, int maxcells) {
         std::vector<std::pair<int, int>> out;
-        auto cells = runs(c->h_sb[0], 0, g.nx, 1 << 30);
+        auto cells = runs(sb, lo, hi, 1 << 30);
         size_t i = 0;
         while (i < cells.size()) {
             int x0 = cells[i].first, w = cells[i].second, k = 1;
-            while (i + k < cells.size() && k < MC_XRN - 3 && w + cells[i + k].second <= xm) w += cells[i + k++].second;
-            out.push_back({x0, w});
+            while (i + k < cells.size() && k < maxcells && w + cells[i + k].second <= len) w += cells[i + k++].second;
+            if (w > len) {   // one cell longer than len: split it
+                for (auto &r : runs(sb, x0, x0 + w, len)) out.push_back(r);
+            } else {
+                out.push_back({x0, w});
+            }
             i += k;
         }
         return out;
     };
+    int mcz = 3;   // MC: z-cells per item (tables grow with it; measured best 3-5)
+    if (const char *e = getenv("SRWCR_MCZ")) mcz = std::min(MC_ZRN - 3, std::max(1, atoi(e)));
+    c->zrn = mcz + 3;
     auto build_items = [&](int zlo, int zhi, std::vector<Item> &out, int xm) {
-        auto xr = c->MC ? xruns_mc(xm) : runs(c->h_sb[0], 0, g.nx, xm);
+        auto xr = c->MC ? cruns_mc(c->h_sb[0], 0, g.nx, xm, MC_XRN - 3) : runs(c->h_sb[0], 0, g.nx, xm);
         auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
-        auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
+        auto zr = c->MC ? cruns_mc(c->h_sb[2], zlo, zhi, std::min(zmax, 64), mcz) : runs(c->h_sb[2], zlo, zhi, zmax);
         for (auto &zz : zr)
             for (auto &yy : yr)
                 for (auto &xx : xr) {
@@ -633,15 +642,15 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
             it.nslots = ns;
             it.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
             ItemW &iw = w[i];
-            for (int l = 0; l < 8; ++l) iw.sx[l] = 0.0;
-            for (int l = 0; l < 4; ++l) iw.sy[l] = iw.sz[l] = 0.0;
+            for (int l = 0; l < 8; ++l) iw.sx[l] = iw.sz[l] = 0.0;
+            for (int l = 0; l < 4; ++l) iw.sy[l] = 0.0;
             const int lo[3] = {it.x0, it.y0, it.z0}, len[3] = {it.xlen, it.ylen, it.zlen};
             double *dst[3] = {iw.sx, iw.sy, iw.sz};
             for (int ax = 0; ax < 3; ++ax)
                 for (int k = lo[ax]; k < lo[ax] + len[ax]; ++k) {
                     const float4 q = c->h_sw[ax][k];
-                    // x: per relative x-region (the voxel's cell offset in a multi-cell item)
-                    const int off = ax == 0 ? c->h_sb[0][k] - c->h_sb[0][it.x0] : 0;
+                    // x, z: per relative region (the voxel's cell offset in a multi-cell item)
+                    const int off = ax == 1 ? 0 : c->h_sb[ax][k] - c->h_sb[ax][lo[ax]];
                     dst[ax][off + 0] += q.x; dst[ax][off + 1] += q.y; dst[ax][off + 2] += q.z; dst[ax][off + 3] += q.w;
                 }
         }
@@ -729,12 +738,13 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->W = c->W2 = 0;
     for (int W : Wc) {
         const size_t ltsv = c->MC ? 2 * MC_XRN + 1 : LTS, ks = c->MC ? 8 * MC_XRN : 32;
+        const size_t cts = c->MC ? 4 * (size_t)c->zrn * 2 * MC_XRN : 4 * ks;
         const size_t s1 = sizeof(int) * (((size_t)W * c->S * ltsv + 3) & ~(size_t)3) + sizeof(float) * (size_t)W * c->S * ks +
-                          sizeof(float) * ((size_t)c->S * 4 * ks + 128 + g.B) + (size_t)g.B + 16 + 2048 + 256;
+                          sizeof(float) * ((size_t)c->S * cts + 128 + g.B) + (size_t)g.B + 16 + 2048 + 256;
         if (!c->W && W <= w1max && W != 32 && W != 20 && (int)s1 <= maxsm) { c->W = W; c->smem1 = s1; }
-        const size_t xrn = c->MC ? MC_XRN : 4, gys = c->MC ? MC_XRN + 1 : GYS;
+        const size_t xrn = c->MC ? MC_XRN : 4, zrn = c->MC ? c->zrn : 4, gys = c->MC ? MC_XRN + 1 : GYS;
         const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (gys + xrn / 4) +
-                          sizeof(float) * (16 * xrn * (size_t)c->S2 + (c->S2 + 1) + 32 * xrn + W * 192 + (o.orientation ? g.B : 0)) +
+                          sizeof(float) * (4 * zrn * xrn * (size_t)c->S2 + (c->S2 + 1) + 8 * zrn * xrn + W * 192 + (o.orientation ? g.B : 0)) +
                           (((o.orientation ? 3 * (g.B + 2) : g.B) + 15) & ~15) +
                           sizeof(float) * npmax;
         if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }

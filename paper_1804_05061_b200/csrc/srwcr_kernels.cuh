@@ -24,6 +24,7 @@ constexpr int LTS = 9;          // line-table slot stride: 8 entries (4 x-taps x
 constexpr int GYS = 5;          // pass-2 per-warp gamma table: float4 per (bin, x-tap), 4 + 1 pad per bin
 constexpr int MAXW = 16;        // max warps per CTA
 constexpr int MC_XRN = 8;       // multi-cell items: x-regions per item (<= 5 spatial x-cells)
+constexpr int MC_ZRN = 8;       //                   z-regions per item (<= 5 spatial z-cells)
 
 struct Tables {                 // per-axis B-spline taps, index = voxel coordinate on that axis
     const int *cb[3];           // control lattice: tap base floor(i/delta)          (Eq 17)
@@ -50,7 +51,7 @@ struct Item {
     int pad;
 };
 // per-item sums of the fp32 spatial weights: sx per relative x-region (MC items span cells)
-struct ItemW { double sx[8], sy[4], sz[4]; };
+struct ItemW { double sx[8], sy[4], sz[8]; };
 
 struct PassArgs {
     Geo g;
@@ -72,6 +73,7 @@ struct PassArgs {
     int *xlist, *xcount;        // pass 2: slab-linear indices of the voxels deferred to k_exact_fix
     int xcap;                   //         capacity of xlist
     int mgz1;                   //         slab slices (k_exact_fix scan fallback)
+    int zrn;                    // multi-cell items: z-regions per item (z-cells + 3, <= MC_ZRN)
     float4 *MG;                 // pass 1 out / pass 2 in: per slab voxel (m, dM/dy) -- m < 0
     int mgz0;                   //   encodes -1 - m for voxels that need the fp64 exact path
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
@@ -328,21 +330,23 @@ __device__ __forceinline__ int axis_fast_cl(int i, float u, int nm2, float tol, 
 // halving path is off, and the binless channels (q', g1 - cI) are one more slot of the
 // line tables (index ns) with their own fixed-point exponents.
 template <int XV, bool STATIC, int MAXT = 512, int ORI = 0, bool MC = false>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int XRN = MC ? MC_XRN : 4;      // x-regions per item
     constexpr int E = 2 * XRN;                // line-table entries per slot
     constexpr int LTSV = MC ? 2 * MC_XRN + 1 : LTS;
     constexpr int KS = 4 * E;                 // column-table floats per slot (entry*4 + n)
+    const int ZR = MC ? a.zrn : 4;            // z-regions of the item's cell table
+    const int CTS = MC ? 4 * ZR * E : 4 * KS; // cell-table floats per slot
     const Geo &g = a.g;
     const int B = g.B, W = a.W, S = a.S;
     const int ltsz = (W * S * LTSV + 3) & ~3;                     // keep K 16-byte aligned
     int *LT = reinterpret_cast<int *>(smem);                      // [W][S][LTSV]
     float *K = reinterpret_cast<float *>(LT + ltsz);              // [W][S][KS]
-    float *CT = K + W * S * KS;                                   // [S][4][KS]
-    float *CB = CT + S * 4 * KS;                                  // [4][32] binless cell table (!MC)
+    float *CT = K + W * S * KS;                                   // [S][4][KS]  (MC: [S][4 m][ZRN zr][E])
+    float *CB = CT + S * CTS;                                     // [4][32] binless cell table (!MC)
     float4 *ZT = reinterpret_cast<float4 *>(CB + 128);            // [2][64] the item's z-tap tables
-    int *ZB = reinterpret_cast<int *>(ZT + 128);                  // [64] and control-tap bases
+    int *ZB = reinterpret_cast<int *>(ZT + 128);                  // [64] control-tap bases, MC: | z-cell offset << 20
     float *shc = reinterpret_cast<float *>(ZB + 64);              // [B]
     unsigned char *smap = reinterpret_cast<unsigned char *>(shc + B);  // [B] bin -> slot
 
@@ -354,7 +358,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
 
     for (int i = threadIdx.x; i < ltsz; i += blockDim.x) LT[i] = 0;
     for (int i = threadIdx.x; i < W * S * KS; i += blockDim.x) K[i] = 0.f;
-    for (int i = threadIdx.x; i < nsl * 4 * KS + 128; i += blockDim.x) (i < nsl * 4 * KS ? CT[i] : CB[i - nsl * 4 * KS]) = 0.f;
+    for (int i = threadIdx.x; i < nsl * CTS + 128; i += blockDim.x) (i < nsl * CTS ? CT[i] : CB[i - nsl * CTS]) = 0.f;
     for (int i = threadIdx.x; i < B; i += blockDim.x) {
         shc[i] = STATIC ? 0.f : a.shiftc[i];
         smap[i] = 0xFF;
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {   // z-tap tables in shared memory
         ZT[i] = a.t.cw[2][it.z0 + i];
         ZT[64 + i] = a.t.sw[2][it.z0 + i];
-        ZB[i] = a.t.cb[2][it.z0 + i];
+        ZB[i] = a.t.cb[2][it.z0 + i] | (MC ? (a.t.sb[2][it.z0 + i] - a.t.sb[2][it.z0]) << 20 : 0);
     }
     __syncthreads();
     for (int s = threadIdx.x; s < ns; s += blockDim.x) smap[a.slotbins[it.slot_off + s]] = (unsigned char)s;
@@ -439,6 +443,36 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
         }
         float bacc = 0.f;
         unsigned wmask[4] = {0u, 0u, 0u, 0u};
+        // fold the column table with the row's y-weights into the cell table (MC: at z-region
+        // offset lcz -- called at every crossed z-cell of a multi-cell item and at row end)
+        // (MC only: a by-reference lambda in the coarse kernel costs it registers)
+        auto foldK = [&](int lcz) {
+          if constexpr (MC) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                unsigned bw = k < nwords ? wmask[k] : 0u;
+                wmask[k] = 0u;
+                while (bw) {
+                    const int s = 32 * k + __ffs(bw) - 1;
+                    bw &= bw - 1;
+#pragma unroll
+                    for (int jj = lane; jj < KS; jj += 32) {
+                        // lane -> (z-tap n, entry) with the 16 entries of one z-tap on
+                        // consecutive lanes: the cell-table atomics hit 32 distinct banks
+                        const int j = (jj & 15) * 4 + (jj >> 4);
+                        const float val = Kw[s * KS + j];
+                        Kw[s * KS + j] = 0.f;
+                        if (val != 0.f) {
+                            float *ct = CT + s * CTS + (lcz + (j & 3)) * E + (j >> 2);
+#pragma unroll
+                            for (int mm = 0; mm < 4; ++mm) atomicAdd(ct + mm * ZR * E, f4(swy, mm) * val);
+                        }
+                    }
+                }
+            }
+          }
+        };
+        int lczr = 0;   // MC: z-cell offset of the column table's contents
         // F is software-pipelined one slice ahead (its DRAM latency is otherwise exposed:
         // the bin a0 it decides gates the whole line's accumulation)
         float Fnext[XV];
@@ -475,6 +509,15 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
         if (!STATIC) gather(it.z0);
 
         for (int z = it.z0; z < it.z0 + it.zlen; ++z) {
+            if (MC) {   // crossed into the next z-cell: its z-taps are other regions
+                const int lz = ZB[z - it.z0] >> 20;
+                if (lz != lczr) {
+                    __syncwarp();
+                    foldK(lczr);
+                    __syncwarp();
+                    lczr = lz;
+                }
+            }
             float Fcur[XV];
             {
                 const int nz1 = z + 1 < it.z0 + it.zlen ? nxy : 0;
@@ -561,7 +604,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                 }
             }
             if (!STATIC && z + 1 < it.z0 + it.zlen) {   // next slice: slide the layer window, issue its gathers
-                const int bz1 = ZB[z + 1 - it.z0];
+                const int bz1 = MC ? ZB[z + 1 - it.z0] & 0xFFFFF : ZB[z + 1 - it.z0];
                 while (gzl < bz1) {
 #pragma unroll
                     for (int n = 0; n < 3; ++n)
@@ -755,19 +798,24 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
             __syncwarp();
         }
         // ---- row done: fold the column table with the row's y-weights into the cell table
+        if constexpr (MC) {
+            __syncwarp();
+            foldK(lczr);
+        } else {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            unsigned bw = k < nwords ? wmask[k] : 0u;
-            while (bw) {
-                const int s = 32 * k + __ffs(bw) - 1;
-                bw &= bw - 1;
+            for (int k = 0; k < 4; ++k) {
+                unsigned bw = k < nwords ? wmask[k] : 0u;
+                while (bw) {
+                    const int s = 32 * k + __ffs(bw) - 1;
+                    bw &= bw - 1;
 #pragma unroll
-                for (int j = lane; j < KS; j += 32) {
-                    const float val = Kw[s * KS + j];
-                    Kw[s * KS + j] = 0.f;
-                    if (val != 0.f) {
+                    for (int j = lane; j < KS; j += 32) {
+                        const float val = Kw[s * KS + j];
+                        Kw[s * KS + j] = 0.f;
+                        if (val != 0.f) {
 #pragma unroll
-                        for (int mm = 0; mm < 4; ++mm) atomicAdd(CT + (s * 4 + mm) * KS + j, f4(swy, mm) * val);
+                            for (int mm = 0; mm < 4; ++mm) atomicAdd(CT + (s * 4 + mm) * KS + j, f4(swy, mm) * val);
+                        }
                     }
                 }
             }
@@ -780,10 +828,23 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
     }
     __syncthreads();
     // ---- item done: flush to global.  CT entry (s, m, e): e = 8*l + 4*ch + n
-    for (int t = threadIdx.x; t < nsl * 4 * KS; t += blockDim.x) {
+    for (int t = threadIdx.x; t < nsl * CTS; t += blockDim.x) {
         const float val = CT[t];
-        const int s = t / (4 * KS), mm = (t / KS) & 3, e = t % KS;
-        const int l = e >> 3, ch = (e >> 2) & 1, n = e & 3;   // l: relative x-region
+        const int s = t / CTS;
+        int mm, l, ch, n;
+        if (MC) {   // [s][m][zr][E], entry = 2 xr + ch
+            const int rem = t - s * CTS;
+            mm = rem / (ZR * E);
+            n = (rem / E) % ZR;
+            l = (rem % E) >> 1;
+            ch = rem & 1;
+        } else {    // [s][m][8 l + 4 ch + n]
+            const int e = t % KS;
+            mm = (t / KS) & 3;
+            l = e >> 3;
+            ch = (e >> 2) & 1;
+            n = e & 3;
+        }
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
         if (MC && !STATIC && s == ns) {   // binless: Q_r += Q' + 2 cI S' + cI^2 N
             if (ch == 0) {
@@ -791,7 +852,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 4 : 1) k_pass1(PassArgs a)
                 const double N = iw.sx[l] * iw.sy[mm] * iw.sz[n];
                 if (N > 0.0) {
                     const double c = cI;
-                    atomicAdd(a.Qt + r, (double)val + 2.0 * c * (double)CT[t + 4] + c * c * N);
+                    atomicAdd(a.Qt + r, (double)val + 2.0 * c * (double)CT[t + 1] + c * c * N);
                 }
             }
             continue;
@@ -1183,9 +1244,10 @@ __device__ __forceinline__ bool near_integer(float v, float tol) { return fabsf(
 // relative x-regions; per line the item's bins are contracted over z per x-region
 // (GZs[bin][xr]) and each voxel sums its own 4 x-regions lcx..lcx+3.
 template <int XV, int MAXT = 512, int ORI = 0, bool MC = false>
-__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a) {
+__global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 5) : 1) k_pass2(PassArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int XRN = MC ? MC_XRN : 4;
+    const int ZRN = MC ? a.zrn : 4;           // z-regions per item
     constexpr int GYSV = MC ? MC_XRN + 1 : GYS;
     const Geo &g = a.g;
     const int B = g.B, W = a.W;
@@ -1204,12 +1266,12 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
     const int GB = a.S2;
     float4 *GY = reinterpret_cast<float4 *>(smem);                // [W][GB][GYSV]
     float4 *GZ = GY + W * GB * GYSV;                              // [W][GB] (MC: [W][GB][XRN] floats)
-    float *gl = reinterpret_cast<float *>(GZ + W * GB * (XRN / 4)); // [16 XRN][GB] gamma of the regions
-    int *gbins = reinterpret_cast<int *>(gl + 16 * XRN * GB);     // [GB+1] the bin list, count
+    float *gl = reinterpret_cast<float *>(GZ + W * GB * (XRN / 4)); // [4 ZRN XRN][GB] gamma of the regions
+    int *gbins = reinterpret_cast<int *>(gl + 4 * ZRN * XRN * GB); // [GB+1] the bin list, count
     unsigned char *gmap = reinterpret_cast<unsigned char *>(gbins + GB + 1);  // [B] bin -> list index
-    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [16 XRN]
-    float *bl = al + 16 * XRN;                                    // [16 XRN]
-    float *shc2 = bl + 16 * XRN;                                  // [B] (ORI 1) the bins' moment shifts
+    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [4 ZRN XRN]
+    float *bl = al + 4 * ZRN * XRN;                               // [4 ZRN XRN]
+    float *shc2 = bl + 4 * ZRN * XRN;                             // [B] (ORI 1) the bins' moment shifts
     float *RB = shc2 + (ORI ? B : 0);                             // [W][3][64] retiring-layer row buffer
     float *NP = RB + W * 192;                                     // [nzn][3][nyn][nxn] node window
 
@@ -1222,18 +1284,19 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
         gmap[b] = (unsigned char)i;
     }
     __syncthreads();
-    // region (n, m, l) of the item (l: relative x-region) at index (n * 4 + m) * XRN + l
-    for (int i = threadIdx.x; i < 16 * XRN * nb2; i += blockDim.x) {
+    // region (n, m, l) of the item (l, n: relative x-, z-regions) at index (n * 4 + m) * XRN + l
+    for (int i = threadIdx.x; i < 4 * ZRN * XRN * nb2; i += blockDim.x) {
         const int reg = i / nb2, k = i - reg * nb2;
         const int l = reg % XRN, mm = (reg / XRN) & 3, n = reg / (4 * XRN);
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        gl[reg * GB + k] = cx + l < g.Kx ? __ldg(a.gamma + r * a.gstride + gbins[k]) : 0.f;
+        gl[reg * GB + k] = cx + l < g.Kx && cz + n < g.Kz ? __ldg(a.gamma + r * a.gstride + gbins[k]) : 0.f;
     }
-    for (int i = threadIdx.x; i < 16 * XRN; i += blockDim.x) {
+    for (int i = threadIdx.x; i < 4 * ZRN * XRN; i += blockDim.x) {
         const int l = i % XRN, mm = (i / XRN) & 3, n = i / (4 * XRN);
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        al[i] = cx + l < g.Kx ? __ldg(a.alpha + r) : 0.f;
-        bl[i] = cx + l < g.Kx ? __ldg(a.beta + r) : 0.f;
+        const bool in = cx + l < g.Kx && cz + n < g.Kz;
+        al[i] = in ? __ldg(a.alpha + r) : 0.f;
+        bl[i] = in ? __ldg(a.beta + r) : 0.f;
     }
     if (ORI)
         for (int i = threadIdx.x; i < B; i += blockDim.x) shc2[i] = a.shiftc[i];
@@ -1270,27 +1333,31 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
         const float4 swy = a.t.sw[1][y];
         const float *__restrict__ Frow = a.F + y * nx;
 
-        // gamma of the item's bins contracted over the y-taps:
-        // GYw[k][l] = float4_n( sum_m wy_m gamma[(n, m, l)][bin k] )
-        for (int i = lane; i < nb2 * 4 * XRN; i += 32) {
-            const int k = i / (4 * XRN), l = (i >> 2) % XRN, n = i & 3;
-            const float *src = gl + (n * 4 * XRN + l) * GB + k;  // region (n, m, l): (n*4 + m)*XRN + l
-            const float val = swy.x * src[0] + swy.y * src[XRN * GB] + swy.z * src[2 * XRN * GB] + swy.w * src[3 * XRN * GB];
-            reinterpret_cast<float *>(GYw + k * GYSV + l)[n] = val;
-        }
+        // gamma of the item's bins contracted over the y-taps, for the z-cell at offset lcz:
+        // GYw[k][l] = float4_n( sum_m wy_m gamma[(lcz + n, m, l)][bin k] )
         // alpha (lanes 0-15) / beta (lanes 16-31) contracted over y: lane = 16*ab + 4*l + n
         // (MC: alpha in abY, beta in abY2, lane = 4*xr + n)
         float abY = 0.f, abY2 = 0.f;
-        if (ORI == 0 && !MC) {
-            const int l = (lane >> 2) & 3, n = lane & 3;
-            const float *src = (lane < 16 ? al : bl) + n * 16 + l;
-            abY = swy.x * src[0] + swy.y * src[4] + swy.z * src[8] + swy.w * src[12];
-        } else if (ORI == 0) {
-            const int l = lane >> 2, n = lane & 3;
-            const float *sa = al + n * 4 * XRN + l, *sb2 = bl + n * 4 * XRN + l;
-            abY = swy.x * sa[0] + swy.y * sa[XRN] + swy.z * sa[2 * XRN] + swy.w * sa[3 * XRN];
-            abY2 = swy.x * sb2[0] + swy.y * sb2[XRN] + swy.z * sb2[2 * XRN] + swy.w * sb2[3 * XRN];
-        }
+        auto rowTables = [&](int lcz) {
+            for (int i = lane; i < nb2 * 4 * XRN; i += 32) {
+                const int k = i / (4 * XRN), l = (i >> 2) % XRN, n = i & 3;
+                const float *src = gl + ((lcz + n) * 4 * XRN + l) * GB + k;   // region (n, m, l): (n*4 + m)*XRN + l
+                const float val = swy.x * src[0] + swy.y * src[XRN * GB] + swy.z * src[2 * XRN * GB] + swy.w * src[3 * XRN * GB];
+                reinterpret_cast<float *>(GYw + k * GYSV + l)[n] = val;
+            }
+            if (ORI == 0 && !MC) {
+                const int l = (lane >> 2) & 3, n = lane & 3;
+                const float *src = (lane < 16 ? al : bl) + n * 16 + l;
+                abY = swy.x * src[0] + swy.y * src[4] + swy.z * src[8] + swy.w * src[12];
+            } else if (ORI == 0) {
+                const int l = lane >> 2, n = lane & 3;
+                const float *sa = al + (lcz + n) * 4 * XRN + l, *sb2 = bl + (lcz + n) * 4 * XRN + l;
+                abY = swy.x * sa[0] + swy.y * sa[XRN] + swy.z * sa[2 * XRN] + swy.w * sa[3 * XRN];
+                abY2 = swy.x * sb2[0] + swy.y * sb2[XRN] + swy.z * sb2[2 * XRN] + swy.w * sb2[3 * XRN];
+            }
+        };
+        rowTables(0);
+        int lczr = 0;   // MC: z-cell offset the row tables are built for
         __syncwarp();
 
         int gzl = zn0;
@@ -1367,6 +1434,15 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? 5 : 1) k_pass2(PassArgs a)
 #pragma unroll
                 for (int v = 0; v < XV; ++v) Ad[3][v][0] = Ad[3][v][1] = Ad[3][v][2] = 0.f;
                 ++gzl;
+            }
+            if (MC) {   // crossed into the next z-cell: rebuild the row tables for its z-regions
+                const int lz = a.t.sb[2][z] - cz;
+                if (lz != lczr) {
+                    __syncwarp();
+                    rowTables(lz);
+                    __syncwarp();
+                    lczr = lz;
+                }
             }
             const float4 cwz = cwzn, wz = wzn;     // this slice's z taps (loaded one slice ahead)
             {
