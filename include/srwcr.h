@@ -250,6 +250,10 @@ typedef struct {
     int32_t warps_per_cta2, items2;  /* pass 2's decomposition */
     int32_t exact_voxels;       /* voxels of the last eval's pass 2 decided in fp64 (k_exact_fix) */
     int32_t exact_capacity;     /* list capacity; more fall back to a scan of the slab */
+    int32_t pipe_items1;        /* host-buffer srwcr_eval: pass-1 items started after the first
+                                   part of the params upload (0: not pipelined) */
+    int32_t pipe_items2;        /* pass-2 items after which the final gradient layers go back
+                                   while the rest run (0: not pipelined) */
 } srwcr_stats;
 srwcr_status srwcr_set_timing(srwcr_ctx *ctx, int32_t enable);
 srwcr_status srwcr_get_stats(const srwcr_ctx *ctx, srwcr_stats *out);

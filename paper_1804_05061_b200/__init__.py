@@ -63,7 +63,8 @@ class _Stats(ctypes.Structure):
                 ("ms_total", ctypes.c_float), ("warps_per_cta", ctypes.c_int32), ("slot_capacity", ctypes.c_int32),
                 ("voxels_per_lane", ctypes.c_int32), ("items", ctypes.c_int32), ("ms_prep", ctypes.c_float),
                 ("warps_per_cta2", ctypes.c_int32), ("items2", ctypes.c_int32),
-                ("exact_voxels", ctypes.c_int32), ("exact_capacity", ctypes.c_int32)]
+                ("exact_voxels", ctypes.c_int32), ("exact_capacity", ctypes.c_int32),
+                ("pipe_items1", ctypes.c_int32), ("pipe_items2", ctypes.c_int32)]
 
 
 class _LbfgsConfig(ctypes.Structure):

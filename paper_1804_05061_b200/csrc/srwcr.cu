@@ -109,6 +109,15 @@ struct srwcr_ctx {
     int launches_per_eval = 0;
     bool timing = false;
     cudaEvent_t ev[5]{};  // pass1 start, pass1 end, combine end, pass2 end, prep start
+    // pipelined host-buffer evaluation (one rank): params H2D overlapped with pass 1, the
+    // gradient D2H with pass 2, on a second stream
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t pev[4]{};
+    int *xbeg = nullptr;
+    // pass 1 in parts: items [p1_b[j], p1_b[j+1]) need params layers [0, p1_l[j]); pass 2 in
+    // parts: after items [0, p2_b[j+1]) the gradient layers [0, p2_l[j]) are final
+    std::vector<int> p1_b, p1_l, p2_b, p2_l;
+    int p1_split = 0, p2_split = 0;    // first part boundaries (stats; 0: not pipelined)
     float ms[5]{};
     double *pinned = nullptr;  // 2 doubles
     // bending energy / L-BFGS (srwcr_register.inc)
@@ -256,11 +265,12 @@ static PassArgs pass_args(srwcr_ctx *c) {
 }
 
 template <int XV>
-static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
+static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full, int i0, int cnt) {
     PassArgs a = pass_args(c);
-    const int n = full ? c->nitems_full : c->nitems;
-    a.items = full ? c->items_full : c->items;
-    a.itemw = full ? c->itemw_full : c->itemw;
+    int n = full ? c->nitems_full : c->nitems;
+    a.items = (full ? c->items_full : c->items) + i0;
+    a.itemw = (full ? c->itemw_full : c->itemw) + i0;
+    n = cnt >= 0 ? cnt : n - i0;
     if (full) a.MG = nullptr;   // whole-volume create-time passes: no (m, dM/dy) output
     if (n == 0) return SRWCR_OK;
     if (XV == 1 && c->MC) {   // fine lattices: multi-cell items
@@ -278,34 +288,43 @@ static srwcr_status launch_pass1_t(srwcr_ctx *c, bool stat, bool full) {
     return SRWCR_OK;
 }
 // full = true: whole volume (create-time static passes, identical on every rank)
-static srwcr_status launch_pass1(srwcr_ctx *c, bool stat, bool full = false) {
-    return c->XV == 2 ? launch_pass1_t<2>(c, stat, full) : launch_pass1_t<1>(c, stat, full);
+static srwcr_status launch_pass1(srwcr_ctx *c, bool stat, bool full = false, int i0 = 0, int cnt = -1) {
+    return c->XV == 2 ? launch_pass1_t<2>(c, stat, full, i0, cnt) : launch_pass1_t<1>(c, stat, full, i0, cnt);
 }
+// pass 2 over items2 [i0, i0 + cnt) (cnt < 0: to the end), then k_exact_fix over the list
+// entries from *xbeg (xmode as in PassArgs); reset = zero the deferred-voxel count first
 template <int XV>
-static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad) {
+static srwcr_status launch_pass2_t(srwcr_ctx *c, double *grad, int i0, int cnt, bool reset, const int *xbeg,
+                                   int xmode) {
     PassArgs a = pass_args(c);
     a.grad = grad;
-    a.items = c->items2;
-    if (c->nitems2 == 0) return SRWCR_OK;
+    a.items = c->items2 + i0;
+    a.xbeg = xbeg;
+    a.xmode = xmode;
+    const int n = cnt >= 0 ? cnt : c->nitems2 - i0;
+    if (n <= 0) return SRWCR_OK;
     a.W = c->W2;
-    CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
+    if (reset) CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
+    const int nitems2 = n;
     if (c->opt.orientation) {
-        k_pass2<XV, 512, 1><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        k_pass2<XV, 512, 1><<<nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
         k_exact_fix<1><<<1184, 128, 0, c->stream>>>(a);
     } else {
-        if (XV == 1 && c->MC && c->W2 <= 6) k_pass2<1, 192, 0, true><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-        else if (XV == 1 && c->MC) k_pass2<1, 512, 0, true><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-        else if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
-        else k_pass2<XV><<<c->nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        if (XV == 1 && c->MC && c->W2 <= 6) k_pass2<1, 192, 0, true><<<nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else if (XV == 1 && c->MC) k_pass2<1, 512, 0, true><<<nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else if (XV == 1 && c->W2 <= 6 && !getenv("SRWCR_NOSMALL")) k_pass2<1, 192><<<nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
+        else k_pass2<XV><<<nitems2, 32 * c->W2, c->smem2, c->stream>>>(a);
         CKL();
         k_exact_fix<0><<<1184, 128, 0, c->stream>>>(a);
     }
     CKL();
     return SRWCR_OK;
 }
-static srwcr_status launch_pass2(srwcr_ctx *c, double *grad) {
-    return c->XV2 == 2 ? launch_pass2_t<2>(c, grad) : launch_pass2_t<1>(c, grad);
+static srwcr_status launch_pass2(srwcr_ctx *c, double *grad, int i0 = 0, int cnt = -1, bool reset = true,
+                                 const int *xbeg = nullptr, int xmode = 0) {
+    return c->XV2 == 2 ? launch_pass2_t<2>(c, grad, i0, cnt, reset, xbeg, xmode)
+                       : launch_pass2_t<1>(c, grad, i0, cnt, reset, xbeg, xmode);
 }
 // The dynamic-shared-memory ceiling is a per-kernel (process-wide) attribute: set it to the
 // device's opt-in maximum so that contexts with different table sizes never race on it
@@ -412,6 +431,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&c->ev[i]));
     CK(cudaMallocHost(&c->pinned, 4 * sizeof(double)));
+    CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+    for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->pev[i], cudaEventDisableTiming));
+    CK(cudaMalloc(&c->xbeg, sizeof(int)));
     memset(c->pinned, 0, 4 * sizeof(double));
 
     // per-axis tables (fp64 on host -> device), control and spatial lattices
@@ -590,6 +612,38 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->nitems = (int)items.size();
     c->nitems_full = (int)items_full.size();
     c->nitems2 = (int)items2.size();
+    // pipelined host-buffer evaluation (one rank, 3-D): pass 1's first two waves of items
+    // start once their params layers have arrived; the gradient layers no item of pass 2's
+    // last two waves touches go back to the host while those run
+    if (c->nranks == 1 && !is2d && !getenv("SRWCR_NOPIPE")) {
+        int wave = nsm;
+        if (const char *e = getenv("SRWCR_PIPE_WAVE")) wave = std::max(1, atoi(e));   // tests: small volumes
+        // parts are whole waves (a part boundary at a z-run start instead needs fewer layers
+        // but adds a partial wave: measured slower on C5)
+        // pass 1: one wave, one wave, the rest (the first upload part is as small as one
+        // wave's layers; later parts arrive while earlier waves run)
+        if (c->nitems >= 4 * wave) {
+            std::vector<int> b = {0, wave, 2 * wave, c->nitems}, l;
+            for (size_t j = 0; j + 1 < b.size(); ++j) {
+                int hi = 0;
+                for (int i = 0; i < b[j + 1]; ++i) hi = std::max(hi, c->h_cb[2][items[i].z0 + items[i].zlen - 1] + 4);
+                l.push_back(std::min(hi, g.GzExt));
+            }
+            if (l[0] < g.GzExt) { c->p1_b = b; c->p1_l = l; c->p1_split = b[1]; }
+        }
+        // pass 2: all but three waves, then one wave at a time (the gradient layers final
+        // after each part go back while the next runs)
+        if (c->nitems2 >= 5 * wave) {
+            const int n = c->nitems2;
+            std::vector<int> b = {0, n - 3 * wave, n - 2 * wave, n - wave, n}, l;
+            for (size_t j = 0; j + 1 < b.size(); ++j) {
+                int lo = g.GzExt;
+                for (int i = b[j + 1]; i < n; ++i) lo = std::min(lo, c->h_cb[2][items2[i].z0]);
+                l.push_back(lo);
+            }
+            if (l[0] > 0) { c->p2_b = b; c->p2_l = l; c->p2_split = b[1]; }
+        }
+    }
 
     // per item: fixed bins present (slot lists), binless shift cI, spatial weight sums
     std::vector<int> slotbins;
@@ -750,6 +804,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
     }
     if (c->W == 0 || c->W2 == 0) return fail(c, SRWCR_EINVAL, "shared memory too small for %d bins / %d slots", g.B, c->S);
+    // the pipelined parts are whole waves of one resident CTA per SM (16 warps x 128
+    // registers fill the register file); with several resident CTAs they would not be
+    if (c->W != 16 && !getenv("SRWCR_PIPE_WAVE")) { c->p1_b.clear(); c->p1_l.clear(); c->p1_split = 0; }
+    if (c->W2 != 16 && !getenv("SRWCR_PIPE_WAVE")) { c->p2_b.clear(); c->p2_l.clear(); c->p2_split = 0; }
     TRY(set_smem(c));
 
     // NCCL communicator for the z-slab decomposition (also built for nranks = 1 when an id
@@ -941,12 +999,107 @@ static srwcr_status eval_graph(srwcr_ctx *c, const double *params, double *value
     return eval_finish(c, value);
 }
 
+// Host params and host gradient on one rank: the H2D of the params runs on a second
+// stream in two parts -- the layers the first two waves of pass-1 items read, then the
+// rest -- and the prep + pass 1 of those items start after the first part; pass 2 runs in
+// two parts too, and the gradient layers final after the first part (all but the layers
+// the last two waves of items touch; their deferred exact voxels fixed first) are copied
+// back while the second part runs.  Same kernels, same results as srwcr_eval's plain path.
+static srwcr_status eval_host_pipelined(srwcr_ctx *c, const double *params, double *value, double *grad) {
+    if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned by an earlier CUDA error");
+    CK(cudaSetDevice(c->dev));
+    const Geo &g = c->g;
+    const size_t plane = (size_t)g.Gx * g.Gy, cs = plane * g.GzExt;
+    auto copy_layers = [&](double *dst, const double *src, int l0, int l1, cudaMemcpyKind kind, cudaStream_t st) {
+        for (int k = 0; k < g.ndim; ++k)
+            if (l1 > l0)
+                CK(cudaMemcpyAsync(dst + k * cs + l0 * plane, src + k * cs + l0 * plane, sizeof(double) * plane * (l1 - l0),
+                                   kind, st));
+        return SRWCR_OK;
+    };
+    const size_t G = (size_t)g.Gx * g.Gy * g.Gz;
+    float *s1 = c->phimax + 4 * G;
+    auto prep = [&](int l0, int l1, int b0, int b1) {
+        if (l1 > l0) {
+            k_prep_phi_wx<<<592, 256, 0, c->stream>>>(c->params64, c->phi, s1, g, l0, l1);
+            CKL();
+        }
+        if (b1 > b0) {
+            k_prep_tol<<<592, 256, 0, c->stream>>>(s1, reinterpret_cast<float4 *>(c->phimax), g, b0, b1, c->pz1);
+            CKL();
+        }
+        return SRWCR_OK;
+    };
+    // ---- params upload in parts (copy stream), each followed by its prep and pass-1 items
+    CK(cudaEventRecord(c->pev[3], c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->pev[3], 0));
+    std::vector<int> b1 = c->p1_b, l1 = c->p1_l;
+    if (b1.empty()) { b1 = {0, c->nitems}; l1 = {g.GzExt}; }
+    l1.back() = g.GzExt;
+    const int np1 = (int)l1.size();
+    c->cur_params = c->params64;
+    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
+    int lo_l = 0, lo_b = c->pz0;
+    for (int j = 0; j < np1; ++j) {
+        TRY(copy_layers(c->params64, params, lo_l, l1[j], cudaMemcpyHostToDevice, c->cstream));
+        CK(cudaEventRecord(c->pev[0], c->cstream));
+        CK(cudaStreamWaitEvent(c->stream, c->pev[0], 0));
+        // fp32 phi of the new layers; tolerance of the base layers whose 4-layer window is here
+        const int hi_b = j + 1 == np1 ? c->pzb1 : std::min(c->pzb1, std::max(lo_b, l1[j] - 3));
+        TRY(prep(std::max(lo_l, c->pz0), j + 1 == np1 ? c->pz1 : l1[j], lo_b, hi_b));
+        TRY(launch_pass1(c, false, false, b1[j], b1[j + 1] - b1[j]));
+        lo_l = l1[j];
+        lo_b = hi_b;
+    }
+    TRY(run_combine(c));
+    CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    bool parts2 = false;
+    if (grad) {
+        CK(cudaMemsetAsync(c->grad64, 0, sizeof(double) * c->nparams, c->stream));
+        if (!c->p2_b.empty()) {
+            // ---- pass 2 in parts: the layers final after a part go back during the next
+            parts2 = true;
+            CK(cudaMemsetAsync(c->xbeg, 0, sizeof(int), c->stream));
+            const int np2 = (int)c->p2_l.size();
+            int done = 0;
+            for (int j = 0; j < np2; ++j) {
+                const bool last = j + 1 == np2;
+                TRY(launch_pass2(c, c->grad64, c->p2_b[j], c->p2_b[j + 1] - c->p2_b[j], j == 0, c->xbeg, last ? 0 : 1));
+                if (last) {
+                    TRY(copy_layers(grad, c->grad64, done, g.GzExt, cudaMemcpyDeviceToHost, c->stream));
+                } else {
+                    CK(cudaMemcpyAsync(c->xbeg, c->xcount, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+                    CK(cudaEventRecord(c->pev[2], c->stream));
+                    CK(cudaStreamWaitEvent(c->cstream, c->pev[2], 0));
+                    TRY(copy_layers(grad, c->grad64, done, c->p2_l[j], cudaMemcpyDeviceToHost, c->cstream));
+                    done = std::max(done, c->p2_l[j]);
+                }
+            }
+        } else {
+            TRY(launch_pass2(c, c->grad64));
+            TRY(copy_layers(grad, c->grad64, 0, g.GzExt, cudaMemcpyDeviceToHost, c->stream));
+        }
+        CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->cstream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (parts2) {   // list overflow: the last launch scanned the whole slab, after the early
+        int xc = 0;   // gradient layers had gone back -- copy the whole gradient again
+        memcpy(&xc, c->pinned + 2, sizeof(int));
+        if (xc > c->xcap) CK(cudaMemcpy(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost));
+    }
+    return eval_finish(c, value);
+}
+
 extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
     if (!c) return SRWCR_EINVAL;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
     if (c->opt.use_graph && !c->comm && !c->poisoned && params && is_device_ptr(params) &&
         (!grad || is_device_ptr(grad)))
         return eval_graph(c, params, value, grad);
+    if (!c->comm && !c->timing && !c->poisoned && params && (c->p1_split > 0 || c->p2_split > 0) &&
+        !is_device_ptr(params) && (!grad || !is_device_ptr(grad)))
+        return eval_host_pipelined(c, params, value, grad);
     TRY(eval_begin_impl(c, params));
     TRY(allreduce(c, c->SQ, stats_count(c)));
     return eval_end_impl(c, value, grad, true);
@@ -1064,6 +1217,8 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->warps_per_cta2 = c->W2;
     out->items2 = c->nitems2;
     out->exact_capacity = c->xcap;
+    out->pipe_items1 = c->p1_split;
+    out->pipe_items2 = c->p2_split;
     out->exact_voxels = c->pinned ? reinterpret_cast<const int *>(c->pinned + 2)[0] : 0;
     return SRWCR_OK;
 }
@@ -1080,9 +1235,13 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
+    if (c->cstream) cudaStreamSynchronize(c->cstream);
+    for (int i = 0; i < 4; ++i)
+        if (c->pev[i]) cudaEventDestroy(c->pev[i]);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
-                    c->beta, c->gamma, c->ticket, c->dpart};
+                    c->beta, c->gamma, c->ticket, c->dpart, c->xbeg};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

@@ -71,6 +71,8 @@ struct PassArgs {
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
     const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 4e-6 max |phi_c| over the tap window (c = x,y,z)
     int *xlist, *xcount;        // pass 2: slab-linear indices of the voxels deferred to k_exact_fix
+    const int *xbeg;            // k_exact_fix: first list entry to process (null: 0)
+    int xmode;                  // k_exact_fix on overflow: 0 scan the slab, 1 nothing (a later launch scans)
     int xcap;                   //         capacity of xlist
     int mgz1;                   //         slab slices (k_exact_fix scan fallback)
     int zrn;                    // multi-cell items: z-regions per item (z-cells + 3, <= MC_ZRN)
@@ -1681,9 +1683,16 @@ __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
     const int cnt = *a.xcount;
     const long long wid = blockIdx.x * 4LL + wib, nw = gridDim.x * 4LL;
     if (cnt <= a.xcap) {
-        for (long long i = wid; i < cnt; i += nw) exact_fix_voxel<ORI>(a, a.xlist[i], sp, lane);
+        const int beg = a.xbeg ? *a.xbeg : 0;
+        for (long long i = beg + wid; i < cnt; i += nw) {
+            const int idx = a.xlist[i];
+            exact_fix_voxel<ORI>(a, idx, sp, lane);
+            // clear the flag: a later overflow scan (pass 2 run in parts) must not fix it again
+            if (lane == 0) a.MG[idx].x = -1.0f - a.MG[idx].x;
+        }
         return;
     }
+    if (a.xmode == 1) return;
     // list overflowed: scan the slab's MG flags, 32 voxels per warp step
     const long long slab = (long long)g.nxy * a.mgz1;
     for (long long b = wid * 32; b < slab; b += nw * 32) {

@@ -299,3 +299,33 @@ def test_graph_replay_matches_eager_launches():
     assert st["ms_pass1"] > 0 and st["ms_pass2"] > 0 and st["ms_total"] >= st["ms_pass1"] + st["ms_pass2"]
     ge.close()
     gg.close()
+
+
+@pytest.mark.parametrize("xcap", [None, "1"])
+def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap):
+    """Host params / host gradient on one rank: the params upload overlaps pass 1 and the
+    final gradient layers go back while pass 2's last items run (here with 4-item
+    "waves" so that a reduced volume is split; xcap=1 forces the list overflow, whose
+    final scan re-copies the whole gradient).  Same result as the device-buffer path and
+    the oracle."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("SRWCR_PIPE_WAVE", "4")
+    if xcap:
+        monkeypatch.setenv("SRWCR_XCAP", xcap)
+    g, pb, Fn, Mn, params = problem("C5", 1, params_kind="large")
+    st = g.stats()
+    assert st["pipe_items1"] > 0 and st["pipe_items2"] > 0, st
+    hp = torch.from_numpy(params.copy()).pin_memory()
+    hg = torch.empty_like(hp).pin_memory()
+    D1, _ = g.eval(hp, grad=hg)
+    pt = hp.cuda()
+    gt = torch.empty_like(pt)
+    D2, _ = g.eval(pt, grad=gt)
+    D3, g3 = g.eval(params)            # pageable host buffers: the same pipelined path
+    g.close()
+    assert rel(D1, D2) <= 2e-7 and rel(D3, D2) <= 2e-7
+    assert rel_l2(hg.numpy(), gt.cpu().numpy()) <= 1e-5
+    assert rel_l2(g3, gt.cpu().numpy()) <= 1e-5
+    Do, go = O.eval_moments(pb, Fn, Mn, params)
+    assert rel(D1, Do) <= D_TOL
+    assert rel_l2(hg.numpy(), go) <= G_TOL
