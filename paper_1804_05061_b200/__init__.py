@@ -142,15 +142,28 @@ def plan_slab(nz: int, nranks: int, rank: int):
     return z0.value, z1.value
 
 
-def _ptr(a):
-    """(pointer, keepalive) of a contiguous numpy array or torch tensor."""
+def _ptr(a, n=None, what="array", out=False):
+    """(pointer, keepalive) of a contiguous numpy array or torch tensor.  With n it must be
+    float64 with n elements (params / gradient: the library reads or writes n doubles);
+    an input is made contiguous by a copy, an output (out=True) must already be."""
     if a is None:
         return None, None
     if hasattr(a, "data_ptr"):          # torch tensor
+        if n is not None:
+            import torch
+            if a.dtype != torch.float64 or a.numel() != n:
+                raise ValueError(f"{what}: need a float64 tensor of {n} elements, got {a.dtype} x {a.numel()}")
         if not a.is_contiguous():
+            if out:
+                raise ValueError(f"{what}: output tensor must be contiguous")
             a = a.contiguous()
         return ctypes.c_void_p(a.data_ptr()), a
-    a = np.ascontiguousarray(a)
+    if n is not None and (a.dtype != np.float64 or a.size != n):
+        raise ValueError(f"{what}: need a float64 array of {n} elements, got {a.dtype} x {a.size}")
+    if not a.flags["C_CONTIGUOUS"]:
+        if out:
+            raise ValueError(f"{what}: output array must be C-contiguous")
+        a = np.ascontiguousarray(a)
     return a.ctypes.data_as(ctypes.c_void_p), a
 
 
@@ -202,6 +215,7 @@ class Srwcr:
         self.grid = tuple(gd)                       # (Gx, Gy, Gz)
         self.ndim = 2 if self.dims[2] == 1 else 3
         self.params_shape = (self.ndim, self.grid[2], self.grid[1], self.grid[0])
+        self._nparams = int(np.prod(self.params_shape))
         self.bins = int(bins)
 
     # -- core
@@ -217,17 +231,19 @@ class Srwcr:
 
         grad: optional preallocated output (numpy or torch, host or device); by default a
         numpy array is returned when want_grad.  Returns (D, grad or None)."""
-        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        n = self._nparams
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.ascontiguousarray(params, dtype=np.float64), n, "params")
         if want_grad and grad is None:
             grad = np.empty(self.params_shape, dtype=np.float64)
-        gp, gk = _ptr(grad) if want_grad else (None, None)
+        gp, gk = _ptr(grad, n, "grad", out=True) if want_grad else (None, None)
         D = ctypes.c_double()
         st = lib().srwcr_eval(self._ctx, pp, ctypes.byref(D), gp)
         self._check(st)
         return D.value, (grad if want_grad else None)
 
     def eval_begin(self, params):
-        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.ascontiguousarray(params, dtype=np.float64),
+                      self._nparams, "params")
         self._check(lib().srwcr_eval_begin(self._ctx, pp))
 
     def stats_buffer(self):
@@ -239,17 +255,18 @@ class Srwcr:
     def eval_end(self, grad=None, want_grad=True):
         if want_grad and grad is None:
             grad = np.empty(self.params_shape, dtype=np.float64)
-        gp, gk = _ptr(grad) if want_grad else (None, None)
+        gp, gk = _ptr(grad, self._nparams, "grad", out=True) if want_grad else (None, None)
         D = ctypes.c_double()
         self._check(lib().srwcr_eval_end(self._ctx, ctypes.byref(D), gp))
         return D.value, (grad if want_grad else None)
 
     def bending(self, params, grad=None, want_grad=True):
         """(C_p, dC_p/dPhi): bending energy of the FFD (Eq 1; reading c19)."""
-        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        n = self._nparams
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.ascontiguousarray(params, dtype=np.float64), n, "params")
         if want_grad and grad is None:
             grad = np.empty(self.params_shape, dtype=np.float64)
-        gp, gk = _ptr(grad) if want_grad else (None, None)
+        gp, gk = _ptr(grad, n, "grad", out=True) if want_grad else (None, None)
         E = ctypes.c_double()
         self._check(lib().srwcr_bending(self._ctx, pp, ctypes.byref(E), gp))
         return E.value, (grad if want_grad else None)
@@ -267,6 +284,8 @@ class Srwcr:
             setattr(c, k, v)
         x = np.zeros(self.params_shape) if params is None else np.array(params, dtype=np.float64, copy=True)
         x = np.ascontiguousarray(x)
+        if x.size != self._nparams:
+            raise ValueError(f"params: need {self._nparams} elements, got {x.size}")
         rep = _Report()
         rep.struct_size = ctypes.sizeof(_Report)
         self._check(lib().srwcr_register(self._ctx, x.ctypes.data_as(ctypes.c_void_p), ctypes.byref(c),
@@ -277,10 +296,14 @@ class Srwcr:
 
     def field(self, params, out=None):
         """Dense FFD displacement field u(x), float32 [3, Nz, Ny, Nx] (numpy, or `out`)."""
-        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.asarray(params, dtype=np.float64))
+        pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.ascontiguousarray(params, dtype=np.float64),
+                      self._nparams, "params")
         if out is None:
             out = np.empty((3, self.dims[2], self.dims[1], self.dims[0]), dtype=np.float32)
-        op, ok_ = _ptr(out)
+        nv = 3 * self.dims[0] * self.dims[1] * self.dims[2]
+        if (out.numel() if hasattr(out, "numel") else out.size) != nv or str(out.dtype).split(".")[-1] != "float32":
+            raise ValueError(f"out: need a float32 buffer of {nv} elements")
+        op, ok_ = _ptr(out, out=True)
         self._check(lib().srwcr_field(self._ctx, pp, op))
         return out
 

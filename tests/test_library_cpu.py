@@ -157,3 +157,26 @@ def test_zslab_decomposition_gloo_two_ranks():
     D, D1, gerr = q.get(timeout=10)
     assert abs(D - D1) <= 1e-12 * abs(D1)
     assert gerr <= 1e-12
+
+
+def test_buffer_marshalling_rejects_wrong_params_and_outputs():
+    """The binding hands raw pointers to the C ABI, which reads / writes nparams doubles:
+    wrong dtypes or sizes, and non-contiguous outputs, must be refused before the call."""
+    import numpy as np
+    import pytest
+    from paper_1804_05061_b200 import _ptr
+    ok = np.zeros(12)
+    assert _ptr(ok, 12, "params")[0] is not None
+    with pytest.raises(ValueError):
+        _ptr(np.zeros(12, dtype=np.float32), 12, "params")
+    with pytest.raises(ValueError):
+        _ptr(np.zeros(11), 12, "params")
+    with pytest.raises(ValueError):
+        _ptr(np.zeros((4, 6))[:, ::2], 12, "grad", out=True)
+    p, keep = _ptr(np.zeros((4, 6))[:, ::2], 12, "params")   # inputs are copied contiguous
+    assert keep.flags["C_CONTIGUOUS"]
+    torch = pytest.importorskip("torch")
+    with pytest.raises(ValueError):
+        _ptr(torch.zeros(12, dtype=torch.float32), 12, "params")
+    with pytest.raises(ValueError):
+        _ptr(torch.zeros(4, 6, dtype=torch.float64)[:, ::2], 12, "grad", out=True)
