@@ -90,7 +90,7 @@ srwcr_status srwcr_default_options(srwcr_options *opt);
  * (Eq 3; they do not depend on Phi) and estimates the per-bin moment shifts
  * with one identity pass.  (An evaluation is 6 kernels on the context's stream,
  * replayed as one CUDA graph when options.use_graph applies.)
- *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2
+ *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2, Nx Ny Nz < 2^31
  *   spacing_mm[3]      voxel spacing (> 0)
  *   intensity_bins     L + 1, in [2, 128] (paper: L = 31); orientation 1: <= 83
  *   spatial_bins[3]    k cells per axis (>= 0; 0 = one region on that axis)

@@ -389,6 +389,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     if (!dims || !sp || !sbins || !csp) return fail(c, SRWCR_EINVAL, "dims/spacing_mm/spatial_bins/control_spacing_mm is NULL");
     if (dims[0] < 2 || dims[1] < 2 || dims[2] < 1) return fail(c, SRWCR_EINVAL, "dims: need Nx >= 2, Ny >= 2, Nz >= 1");
     if (dims[0] > (1 << 20) || dims[1] > (1 << 20) || dims[2] > (1 << 20)) return fail(c, SRWCR_EINVAL, "dims too large");
+    if (dims[0] * dims[1] * dims[2] > INT32_MAX)   // the passes index voxels with 32-bit offsets
+        return fail(c, SRWCR_EINVAL, "volume too large: %lld voxels, at most 2^31 - 1",
+                    (long long)(dims[0] * dims[1] * dims[2]));
     if (bins < 2 || bins > 128) return fail(c, SRWCR_EINVAL, "intensity_bins must be in [2, 128], got %d", bins);
     if (o.orientation != 0 && o.orientation != 1) return fail(c, SRWCR_EINVAL, "orientation must be 0 or 1");
     if (o.orientation == 1 && bins > 83)

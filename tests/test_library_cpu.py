@@ -82,6 +82,12 @@ def test_default_options_and_argument_errors(lib):
     ctx = ctypes.c_void_p()
     assert lib.srwcr_create(ctypes.byref(ctx), p, p, dims, sp, 32, sb, cs, ctypes.byref(opt)) == S.EINVAL
     lib.srwcr_destroy(ctx)
+    # the passes use 32-bit voxel offsets: >= 2^31 voxels is refused before any allocation
+    big = (ctypes.c_int64 * 3)(2048, 2048, 512)
+    ctx = ctypes.c_void_p()
+    assert lib.srwcr_create(ctypes.byref(ctx), p, p, big, sp, 32, sb, cs, None) == S.EINVAL
+    assert b"volume too large" in lib.srwcr_last_error(ctx)
+    lib.srwcr_destroy(ctx)
 
 
 @pytest.mark.parametrize("nz,P", [(320, 8), (128, 3), (7, 4), (1, 1), (5, 5)])
