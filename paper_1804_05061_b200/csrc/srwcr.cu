@@ -92,7 +92,8 @@ struct srwcr_ctx {
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     unsigned *ticket = nullptr;   // k_combine's last-CTA ticket
     double *dpart = nullptr;      // k_combine's per-CTA partial sums
-    double *S_out = nullptr;
+    double *S_out = nullptr;   // unshifted S[r][a], written by the combine only for a debug dump
+    bool dump_S = false;
     float *shiftc = nullptr, *alpha = nullptr, *beta = nullptr, *gamma = nullptr;
     double Z = 0;
     size_t smem1 = 0, smem2 = 0;
@@ -369,13 +370,13 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     ca.SQ = c->SQ; ca.Qt = c->Qt; ca.Nlo = c->Nlo; ca.Nup = c->Nup; ca.shiftc = c->shiftc;
     ca.R = (int)c->R; ca.B = c->g.B; ca.Z = c->Z;
     ca.eps_mass = c->opt.eps_mass; ca.eps_sigma = c->opt.eps_sigma;
-    ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->S_out;
+    ca.dterm = c->dterm; ca.reg = c->reg; ca.S_out = c->dump_S ? c->S_out : nullptr;
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
     ca.NQ = c->NQ; ca.gstride = c->gstride;
     ca.ticket = c->ticket; ca.Dout = c->Dout; ca.part = c->dpart;   // D reduced by the launch's last CTA
-    const int wpb = 8;
-    if (c->opt.orientation) k_combineA<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
-    else k_combine<<<(unsigned)((c->R + wpb - 1) / wpb), 32 * wpb, 0, c->stream>>>(ca);
+    const unsigned nb = (unsigned)std::min<int64_t>((c->R + 7) / 8, 148 * 8);   // fixed grid (deterministic D)
+    if (c->opt.orientation) k_combineA<<<nb, 256, 0, c->stream>>>(ca);
+    else k_combine<<<nb, 256, 0, c->stream>>>(ca);
     CKL();
     return SRWCR_OK;
 }
@@ -766,7 +767,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
     CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
     CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
-    CK(cudaMalloc(&c->dpart, sizeof(double) * 2 * (size_t)((c->R + 7) / 8)));
+    CK(cudaMalloc(&c->dpart, sizeof(double) * 2 * (size_t)std::min<int64_t>((c->R + 7) / 8, 148 * 8)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
     CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
@@ -1185,10 +1186,17 @@ extern "C" srwcr_status srwcr_debug_dump(srwcr_ctx *c, int32_t what, void *out, 
                 for (int b = 0; b < B; ++b) o[r * B + b] = lo[r * B + b] + (b > 0 ? up[r * B + b - 1] : 0.0);
             break;
         }
-        case SRWCR_DUMP_SQ:
+        case SRWCR_DUMP_SQ: {
+            // re-run the (deterministic) combine of the last statistics with the S output on
+            c->dump_S = true;
+            const srwcr_status st = run_combine(c);
+            c->dump_S = false;
+            if (st != SRWCR_OK) return st;
+            CK(cudaStreamSynchronize(c->stream));
             CK(cudaMemcpy(out, c->S_out, sizeof(double) * RB, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy((double *)out + RB, c->Qt, sizeof(double) * c->R, cudaMemcpyDeviceToHost));
             break;
+        }
         case SRWCR_DUMP_REGIONS: CK(cudaMemcpy(out, c->reg, need, cudaMemcpyDeviceToHost)); break;
         case SRWCR_DUMP_COEFS:
             CK(cudaMemcpy(out, c->alpha, sizeof(float) * c->R, cudaMemcpyDeviceToHost));

@@ -957,9 +957,8 @@ __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, doubl
 }
 
 // returns (in dt, rt; lane 0 of the region's warp) the region's dterm and retained flag
-__device__ __forceinline__ void combine_region(const CombineArgs &a, double &dt, double &rt) {
+__device__ __forceinline__ void combine_region(const CombineArgs &a, int r, double &dt, double &rt) {
     const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     dt = rt = 0.0;
     if (r >= a.R) return;
     const int B = a.B;
@@ -1039,9 +1038,8 @@ __device__ __forceinline__ void bin_NS_A(const CombineArgs &a, int r, int b, dou
     }
 }
 
-__device__ __forceinline__ void combineA_region(const CombineArgs &a, double &dt, double &rt) {
+__device__ __forceinline__ void combineA_region(const CombineArgs &a, int r, double &dt, double &rt) {
     const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     dt = rt = 0.0;
     if (r >= a.R) return;
     const int B = a.B;
@@ -1097,14 +1095,26 @@ __device__ __forceinline__ void combineA_region(const CombineArgs &a, double &dt
     }
 }
 
+// a fixed grid: warp w of CTA b takes regions b*8 + w, then + 8*gridDim (fine lattices have
+// 10^5-10^6 regions; one CTA per 8 regions made the last-CTA ticket a serial hot spot)
 __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
-    double dt, rt;
-    combine_region(a, dt, rt);
+    double dt = 0, rt = 0;
+    for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < a.R; r += gridDim.x * 8) {
+        double d1, r1;
+        combine_region(a, r, d1, r1);
+        dt += d1;
+        rt += r1;
+    }
     combine_tail(a, dt, rt);
 }
 __global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
-    double dt, rt;
-    combineA_region(a, dt, rt);
+    double dt = 0, rt = 0;
+    for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < a.R; r += gridDim.x * 8) {
+        double d1, r1;
+        combineA_region(a, r, d1, r1);
+        dt += d1;
+        rt += r1;
+    }
     combine_tail(a, dt, rt);
 }
 

@@ -329,3 +329,21 @@ def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap):
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     assert rel(D1, Do) <= D_TOL
     assert rel_l2(hg.numpy(), go) <= G_TOL
+
+
+def test_debug_dump_statistics_match_oracle_moments():
+    """SRWCR_DUMP_SQ re-runs the last combine with its S output on: the unshifted binned
+    first moments S[r][a] and the binless Q[r] of the last pass 1 equal the oracle's
+    moments (Eq 3 in moment form) to fp32-accumulation accuracy."""
+    g, pb, Fn, Mn, params = problem("C3", 1, params_kind="small")
+    D, _ = g.eval(params)
+    N, Sx, Q = O.moments(pb, Fn, Mn, params)
+    d = g.debug_dump("SQ")
+    R, B = Sx.shape
+    Sg, Qg = d[:R * B].reshape(R, B), d[R * B:R * B + R]
+    assert np.abs(Sg - Sx).max() <= 2e-5 * np.abs(Sx).max()
+    Qr = Q.sum(axis=1)          # the GPU keeps the binless per-region second moment
+    assert np.abs(Qg - Qr).max() <= 2e-5 * np.abs(Qr).max()
+    D2, _ = g.eval(params)     # the dump left the evaluation state as it was
+    assert rel(D2, D) <= 2e-7
+    g.close()
