@@ -322,7 +322,7 @@ def main():
             except Exception:
                 traffic = None
         cpu = None
-        if not args.no_cpu_baseline:
+        if not args.no_cpu_baseline and ws == 1:   # the oracle baseline: rank 0 at N = 1 only
             slices = args.cpu_sample_slices or auto_slices(cfg)
             dt, vox, threads = oracle_sample(args.config, cfg, F, M, params_np, slices)
             cpu = {"value": vox / (dt * nvox), "unit": "evals/s", "cores": threads, "kind": "oracle",
@@ -349,7 +349,7 @@ def main():
                                                         "warps_per_cta2", "items2")},
             "clocks": clk.summary(),
             "D": D,
-            "paper_workloads": None if args.no_paper_workloads else paper_workloads(local),
+            "paper_workloads": None if args.no_paper_workloads or ws > 1 else paper_workloads(local),
         }
         print(json.dumps(line), flush=True)
     g.close()
