@@ -301,8 +301,8 @@ def test_graph_replay_matches_eager_launches():
     gg.close()
 
 
-@pytest.mark.parametrize("xcap", [None, "1"])
-def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap):
+@pytest.mark.parametrize("xcap,orientation", [(None, 0), ("1", 0), (None, 1)])
+def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap, orientation):
     """Host params / host gradient on one rank: the params upload overlaps pass 1 and the
     final gradient layers go back while pass 2's last items run (here with 4-item
     "waves" so that a reduced volume is split; xcap=1 forces the list overflow, whose
@@ -312,7 +312,8 @@ def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap):
     monkeypatch.setenv("SRWCR_PIPE_WAVE", "4")
     if xcap:
         monkeypatch.setenv("SRWCR_XCAP", xcap)
-    g, pb, Fn, Mn, params = problem("C5", 1, params_kind="large")
+    g, pb, Fn, Mn, params = problem("C5", 1, params_kind="large", orientation=orientation,
+                                    bins=64 if orientation else None)
     st = g.stats()
     assert st["pipe_items1"] > 0 and st["pipe_items2"] > 0, st
     hp = torch.from_numpy(params.copy()).pin_memory()
