@@ -895,6 +895,15 @@ extern "C" srwcr_status srwcr_num_params(const srwcr_ctx *c, int64_t *n, int64_t
     return SRWCR_OK;
 }
 
+// per-pass timing event: an external event-record node when the stream is being captured
+// into the evaluation graph (the flag is invalid outside a capture)
+static cudaError_t record_ev(srwcr_ctx *c, int i) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(c->stream, &cs);
+    return cs == cudaStreamCaptureStatusActive ? cudaEventRecordWithFlags(c->ev[i], c->stream, cudaEventRecordExternal)
+                                               : cudaEventRecord(c->ev[i], c->stream);
+}
+
 static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev = -1) {
     if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned by an earlier CUDA error");
     if (!params) return fail(c, SRWCR_EINVAL, "params is NULL");
@@ -905,7 +914,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
         pd = c->params64;
     }
     c->cur_params = pd;
-    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[4], c->stream, cudaEventRecordExternal));
+    if (c->timing) CK(record_ev(c, 4));
     // only the node layers this rank's slab reads: taps of slices [z0, z1) (all of them on
     // one rank), converted to fp32, and their tap-window max |phi_c| (x, y into scratch,
     // z -> float4) for pass 1's rounding bound
@@ -919,9 +928,9 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
         CKL();
     }
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
-    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[0], c->stream, cudaEventRecordExternal));
+    if (c->timing) CK(record_ev(c, 0));
     TRY(launch_pass1(c, false));
-    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[1], c->stream, cudaEventRecordExternal));
+    if (c->timing) CK(record_ev(c, 1));
     return SRWCR_OK;
 }
 
@@ -929,7 +938,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
 // also the body of the captured evaluation graph)
 static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_grad, int gdev = -1) {
     TRY(run_combine(c));
-    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[2], c->stream, cudaEventRecordExternal));
+    if (c->timing) CK(record_ev(c, 2));
     double *gd = nullptr;
     const bool grad_dev = grad && (gdev < 0 ? is_device_ptr(grad) : gdev != 0);
     if (grad) {
@@ -938,7 +947,7 @@ static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_gra
         TRY(launch_pass2(c, gd));
         if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
     }
-    if (c->timing) CK(cudaEventRecordWithFlags(c->ev[3], c->stream, cudaEventRecordExternal));
+    if (c->timing) CK(record_ev(c, 3));
     CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (grad) CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     if (grad && !grad_dev) CK(cudaMemcpyAsync(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost, c->stream));

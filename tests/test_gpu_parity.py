@@ -348,3 +348,20 @@ def test_debug_dump_statistics_match_oracle_moments():
     D2, _ = g.eval(params)     # the dump left the evaluation state as it was
     assert rel(D2, D) <= 2e-7
     g.close()
+
+
+def test_timing_on_every_path():
+    """srwcr_set_timing: per-pass CUDA events on the host-buffer path, the device-buffer
+    (graph) path and inside srwcr_register."""
+    torch = pytest.importorskip("torch")
+    g, pb, Fn, Mn, params = problem("C3", 1, params_kind="small")
+    g.set_timing(True)
+    D1, _ = g.eval(params)
+    st = g.stats()
+    assert st["ms_pass1"] > 0 and st["ms_pass2"] > 0
+    pt = torch.from_numpy(params).cuda()
+    D2, _ = g.eval(pt, grad=torch.empty_like(pt))
+    assert g.stats()["ms_pass1"] > 0 and rel(D2, D1) <= 2e-7
+    x, rep = g.register(None, max_iter=2)
+    assert rep["iterations"] >= 1
+    g.close()
