@@ -1160,27 +1160,28 @@ struct ExactGeo { int nx, ny, nz, L, Gx, Gy, GzExt, ndim; };
 // 1e-4 of an integer (the Parzen kink of c4): there the per-voxel derivative is
 // discontinuous and the side must be decided as the fp64 definition decides it.
 // (returned by value: reference outputs would force the caller's locals into local memory)
-// Called by a whole warp for one voxel: the lanes stage the 64 x ndim control values in
-// the warp's shared buffer sp[3][64] (independent loads in flight together), then every
-// lane sums them in the definition's order (identical result in every lane).
+// Called by a group of 16 lanes (half a warp, mask gm) for one voxel: the lanes stage the
+// 64 x ndim control values in the group's shared buffer sp[3][64] (independent loads in
+// flight together), then every lane sums them in the definition's order (identical result
+// in every lane).
 struct ExactOut { float gx, gy, gz, g1p, c2; };
 __device__ __forceinline__ ExactOut exact_sample(ExactGeo g, const double *__restrict__ p64, const float *__restrict__ M,
                                                  const double4 *__restrict__ cwx64, const double4 *__restrict__ cwy64,
                                                  const double4 *__restrict__ cwz64, int bx, int by, int bz, int x,
-                                                 int y, int z, double *sp, int lane) {
+                                                 int y, int z, double *sp, int gl, unsigned gm) {
     const double4 wx = cwx64[x], wy = cwy64[y], wz = cwz64[z];
     ExactOut o;
     const long long plane = (long long)g.Gx * g.Gy, cs = plane * g.GzExt;
     const long long nxy = (long long)g.nx * g.ny;
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int tp = lane + 32 * h, n = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+    for (int h = 0; h < 4; ++h) {
+        const int tp = gl + 16 * h, n = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
         const long long s = (long long)(bz + n) * plane + (long long)(by + mm) * g.Gx + bx + l;
         const bool in = bz + n < g.GzExt;
 #pragma unroll
         for (int c = 0; c < 3; ++c) sp[c * 64 + tp] = (in && c < g.ndim) ? p64[c * cs + s] : 0.0;
     }
-    __syncwarp();
+    __syncwarp(gm);
     double u[3] = {0.0, 0.0, 0.0};
     for (int n = 0; n < 4; ++n) {
         const double wn = d4(wz, n);
@@ -1617,20 +1618,38 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 5) : 1) k_pass2(
 // One warp per deferred voxel: the 64 tap loads of each stage are spread over the lanes
 // (a thread-per-voxel version was a serial chain of ~250 dependent-latency loads, ~120 us).
 template <int ORI>
-__device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx, double *sp, int lane) {
+__device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx, double *sp, int gl, unsigned gm) {
     const Geo &g = a.g;
     const int x = (int)(idx % g.nx);
     const long long t = idx / g.nx;
     const int y = (int)(t % g.ny), z = (int)(t / g.ny) + a.mgz0;
     const int bx = a.t.cb[0][x], by = a.t.cb[1][y], bz = a.t.cb[2][z];
-    const ExactOut e = exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
-                                    a.t.cw64[0], a.t.cw64[1], a.t.cw64[2], bx, by, bz, x, y, z, sp, lane);
+    // everything that does not depend on the fp64 sample is read before it (fewer serial
+    // round trips per voxel): F and its bins, the spatial taps, and (ORI 0) this lane's
+    // 4 region coefficients
     const float Fv = a.F[(long long)z * g.nxy + (long long)y * g.nx + x];
     const int a0 = min((int)Fv, g.L - 1);
     float hlo, hhi;
     parzen_pair(Fv - (float)a0, hlo, hhi);
     const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
     const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
+    float al[4], be[4], ga[4];
+    long long rr[4];
+    float ww[4];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const int tp = gl + 16 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+        ww[h] = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+        rr[h] = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        al[h] = be[h] = ga[h] = 0.f;
+        if (ORI == 0 && ww[h] != 0.f) {
+            al[h] = a.alpha[rr[h]];
+            be[h] = a.beta[rr[h]];
+            ga[h] = fmaf(hlo, a.gamma[rr[h] * a.gstride + a0], hhi * a.gamma[rr[h] * a.gstride + a0 + 1]);
+        }
+    }
+    const ExactOut e = exact_sample(ExactGeo{g.nx, g.ny, g.nz, g.L, g.Gx, g.Gy, g.GzExt, g.ndim}, a.p64, a.M,
+                                    a.t.cw64[0], a.t.cw64[1], a.t.cw64[2], bx, by, bz, x, y, z, sp, gl, gm);
     // ORI 1: exact_sample's c2 is 2m at integer m (even) and 2n + 1 otherwise (odd)
     int jm = 0, jp = 0;
     float dm = 0.f, dp = 0.f, em = 0.f, ep = 0.f;
@@ -1645,73 +1664,79 @@ __device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx
     }
     float At = 0.f, Bt = 0.f, Gt = 0.f;   // ORI 1 accumulates into At only
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int tp = lane + 32 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
-        const float w = f4(sz, nn) * f4(sy, mm) * f4(sx, l);
+    for (int h = 0; h < 4; ++h) {
+        const float w = ww[h];
         if (w == 0.f) continue;
-        const long long r = ((long long)(cz + nn) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
         if (ORI == 0) {
-            At = fmaf(w, a.alpha[r], At);
-            Bt = fmaf(w, a.beta[r], Bt);
-            Gt = fmaf(w, fmaf(hlo, a.gamma[r * a.gstride + a0], hhi * a.gamma[r * a.gstride + a0 + 1]), Gt);
+            At = fmaf(w, al[h], At);
+            Bt = fmaf(w, be[h], Bt);
+            Gt = fmaf(w, ga[h], Gt);
         } else {
-            const float *row = a.gamma + r * a.gstride;
+            const float *row = a.gamma + rr[h] * a.gstride;
             const float pm = fmaf(em * em, row[jm], fmaf(2.0f * em, row[jm + 1], row[jm + 2]));
             const float pp = fmaf(ep * ep, row[jp], fmaf(2.0f * ep, row[jp + 1], row[jp + 2]));
             At = fmaf(w, fmaf(dm, pm, dp * pp), At);
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        At += __shfl_xor_sync(0xffffffffu, At, o);
+    for (int o = 8; o > 0; o >>= 1) {
+        At += __shfl_xor_sync(gm, At, o);
         if (ORI == 0) {
-            Bt += __shfl_xor_sync(0xffffffffu, Bt, o);
-            Gt += __shfl_xor_sync(0xffffffffu, Gt, o);
+            Bt += __shfl_xor_sync(gm, Bt, o);
+            Gt += __shfl_xor_sync(gm, Gt, o);
         }
     }
     const float d = ORI == 0 ? e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt)) : a.invZ * At;
     const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
     const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-        const int tp = lane + 32 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
+    for (int h = 0; h < 4; ++h) {
+        const int tp = gl + 16 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
         if (bz + nn >= g.GzExt || f4(wz, nn) == 0.f) continue;
         const float w = f4(wz, nn) * f4(wy, mm) * f4(wx, l);
         for (int c = 0; c < g.ndim; ++c)
             atomicAdd(a.grad + (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l,
                       (double)(w * dc[c]));
     }
-    __syncwarp();   // sp is reused by the warp's next voxel
+    __syncwarp(gm);   // sp is reused by the group's next voxel
 }
 
+// Two voxels per warp (one per half-warp group of 16 lanes).
 template <int ORI = 0>
 __global__ void __launch_bounds__(128) k_exact_fix(PassArgs a) {
-    __shared__ double spb[4][3 * 64];
+    __shared__ double spb[8][3 * 64];
     const Geo &g = a.g;
-    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    double *sp = spb[wib];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, half = lane >> 4, gl = lane & 15;
+    const unsigned gm = half ? 0xffff0000u : 0x0000ffffu;
+    double *sp = spb[2 * wib + half];
     const int cnt = *a.xcount;
-    const long long wid = blockIdx.x * 4LL + wib, nw = gridDim.x * 4LL;
+    const long long gid = (blockIdx.x * 4LL + wib) * 2 + half, ng = gridDim.x * 8LL;
     if (cnt <= a.xcap) {
         const int beg = a.xbeg ? *a.xbeg : 0;
-        for (long long i = beg + wid; i < cnt; i += nw) {
+        for (long long i = beg + gid; i < cnt; i += ng) {
             const int idx = a.xlist[i];
-            exact_fix_voxel<ORI>(a, idx, sp, lane);
+            exact_fix_voxel<ORI>(a, idx, sp, gl, gm);
             // clear the flag: a later overflow scan (pass 2 run in parts) must not fix it again
-            if (lane == 0) a.MG[idx].x = -1.0f - a.MG[idx].x;
+            if (gl == 0) a.MG[idx].x = -1.0f - a.MG[idx].x;
         }
         return;
     }
     if (a.xmode == 1) return;
-    // list overflowed: scan the slab's MG flags, 32 voxels per warp step
+    // list overflowed: scan the slab's MG flags, 32 voxels per warp step, the flagged ones
+    // two at a time (one per half-warp)
     const long long slab = (long long)g.nxy * a.mgz1;
+    const long long wid = blockIdx.x * 4LL + wib, nw = gridDim.x * 4LL;
     for (long long b = wid * 32; b < slab; b += nw * 32) {
         const long long i = b + lane;
         unsigned fl = __ballot_sync(0xffffffffu, i < slab && a.MG[i].x < 0.f);
         while (fl) {
-            const int k = __ffs(fl) - 1;
+            const int k0 = __ffs(fl) - 1;
             fl &= fl - 1;
-            exact_fix_voxel<ORI>(a, b + k, sp, lane);
+            const int k1 = fl ? __ffs(fl) - 1 : -1;
+            if (k1 >= 0) fl &= fl - 1;
+            const int k = half ? k1 : k0;
+            if (k >= 0) exact_fix_voxel<ORI>(a, b + k, sp, gl, gm);
+            __syncwarp();
         }
     }
 }
