@@ -69,7 +69,7 @@ struct PassArgs {
     int gstride;                // pass 2: row stride of the gamma table (B; ORI 1: 3 (B + 2))
     int W, S, S2;               // warps per CTA, slot capacity, pass-2 bin-list capacity
     const double *p64;          // pass 2: fp64 params, external layout (exact-sample path)
-    const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 4e-6 max |phi_c| over the tap window (c = x,y,z)
+    const float4 *tolw;         // pass 1: [Gz][Gy][Gx] 2e-6 max |phi_c| over the tap window (c = x,y,z)
     int *xlist, *xcount;        // pass 2: slab-linear indices of the voxels deferred to k_exact_fix
     const int *xbeg;            // k_exact_fix: first list entry to process (null: 0)
     int xmode;                  // k_exact_fix on overflow: 0 scan the slab, 1 nothing (a later launch scans)
@@ -492,9 +492,10 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
                 const float ux = fmaf(cw.w, U[3][v][0], fmaf(cw.z, U[2][v][0], fmaf(cw.y, U[1][v][0], cw.x * U[0][v][0])));
                 const float uy = fmaf(cw.w, U[3][v][1], fmaf(cw.z, U[2][v][1], fmaf(cw.y, U[1][v][1], cw.x * U[0][v][1])));
                 const float uz = fmaf(cw.w, U[3][v][2], fmaf(cw.z, U[2][v][2], fmaf(cw.y, U[1][v][2], cw.x * U[0][v][2])));
-                // rounding bound of u_c: |u32 - u64| <= ~1e-6 max_taps |phi_c| (fp32 phi
-                // and weights, 12 fma levels; weights >= 0 sum to 1); tolerance 4x that.
-                // The max is over this voxel's own 4x4x4 tap window (k_window_max).
+                // rounding bound of u_c: |u32 - u64| <= gamma_16 max_taps |phi_c| ~ 9.5e-7
+                // max |phi_c| (16 roundings on any path: fp32 phi and the 3 weights, 3 x 4
+                // fma levels; weights >= 0 sum to 1); tolerance 2e-6, 2.1x that.  The max is
+                // over this voxel's own 4x4x4 tap window (k_prep_tol).
                 const float4 tl = __ldg(a.tolw + (gzl * g.Gy + cby) * g.Gx + relx[v] + xn0);
                 bool clx, cly, clz, nrx, nry, nrz;
                 const int ccx = axis_fast_fl(xv[v], ux, nxm2, tl.x, T[v][0], clx, nrx);
@@ -1827,12 +1828,12 @@ __global__ void k_prep_tol(const float *__restrict__ wx, float4 *__restrict__ ou
                 for (int dy = 0; dy < 4; ++dy)
                     if (k + dz < zhi && gy + dy < g.Gy)
                         m[c] = fmaxf(m[c], __ldg(wx + c * cs + i + dz * plane + dy * g.Gx));
-        out[i] = make_float4(4e-6f * m[0], 4e-6f * m[1], 4e-6f * m[2], 0.f);
+        out[i] = make_float4(2e-6f * m[0], 2e-6f * m[1], 2e-6f * m[2], 0.f);
     }
 }
 
 // last (z) pass of the window max, all 3 components of a node into one float4, already
-// scaled to pass 1's tolerance 4e-6 max |phi_c|; base layers [zlo, zb) reading up to zhi
+// scaled to pass 1's tolerance 2e-6 max |phi_c|; base layers [zlo, zb) reading up to zhi
 __global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict__ out, Geo g, int zlo, int zb, int zhi) {
     const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zb - zlo) * plane;
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
@@ -1844,7 +1845,7 @@ __global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict
 #pragma unroll
             for (int d = 0; d < 4; ++d)
                 if (k + d < zhi) m[c] = fmaxf(m[c], fabsf(in[c * cs + i + d * plane]));
-        out[i] = make_float4(4e-6f * m[0], 4e-6f * m[1], 4e-6f * m[2], 0.f);
+        out[i] = make_float4(2e-6f * m[0], 2e-6f * m[1], 2e-6f * m[2], 0.f);
     }
 }
 
