@@ -1,9 +1,10 @@
 // srwcr_kernels.cuh -- sm_100a kernels of the SRWCR hot path (arXiv 1804.05061).
 //
 // One SRWCR evaluation = pass 1 (k_pass1: FFD + trilinear warp + Parzen moments +
-// privatised histogram), combine (k_combine + k_reduce_D: per-region correlation
-// ratios, D and the backward coefficient tables), pass 2 (k_pass2: FFD + trilinear
-// value and gradient + dD/dm + adjoint B-spline scatter onto the control lattice).
+// privatised histogram), combine (k_combine, D reduced by its last CTA: per-region correlation
+// ratios, D and the backward coefficient tables), pass 2 (k_pass2: pass 1's (m, dM/dy)
+// per voxel + dD/dm + adjoint B-spline scatter onto the control lattice), k_exact_fix
+// (the voxels whose derivative the fp64 definition must decide).
 // The warped image and every per-voxel intermediate stay in registers (the paper's
 // kernels 1-4 materialise them).  DESIGN.md s5-s6 describe the data flow,
 // the roofline of each kernel and what differs from the paper's GPU design.
@@ -1119,22 +1120,6 @@ __global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
     combine_tail(a, dt, rt);
 }
 
-// D = (1/Z) sum_r dterm[r] in a fixed order (deterministic); out[0] = D, out[1] = #retained
-__global__ void __launch_bounds__(1024) k_reduce_D(const double *dterm, const double *reg, int R, double Z,
-                                                    double *out) {
-    __shared__ double sd[1024];
-    __shared__ double sc[1024];
-    double s = 0, c = 0;
-    for (int r = threadIdx.x; r < R; r += blockDim.x) { s += dterm[r]; c += reg[(long long)r * 6 + 4]; }
-    sd[threadIdx.x] = s;
-    sc[threadIdx.x] = c;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) { sd[threadIdx.x] += sd[threadIdx.x + o]; sc[threadIdx.x] += sc[threadIdx.x + o]; }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) { out[0] = sd[0] / Z; out[1] = sc[0]; }
-}
 
 // ----------------------------------------------- pass 2: exact-sample path (fp64)
 __device__ __forceinline__ double d4(const double4 &v, int i) {
@@ -1762,30 +1747,9 @@ __global__ void k_params_to_f32(const double *__restrict__ p, float *__restrict_
     }
 }
 
-// max of |phi_c| over the 4 nodes [k, k+3] along axis AX (clipped to the grid), for all
-// 3 components, over node layers [zlo, zhi): three passes give the max over each voxel's
-// 4x4x4 tap window keyed by its base node -- the scale of pass 1's rounding bound of u
-template <int AX>
-__global__ void k_window_max(const float *__restrict__ in, float *__restrict__ out, Geo g, int zlo, int zhi) {
-    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < 3 * span; j += (long long)gridDim.x * blockDim.x) {
-        const long long comp = j / span, r = (long long)zlo * plane + (j - comp * span);
-        const long long i = comp * cs + r;
-        int k, G;
-        long long st;
-        if (AX == 0) { k = (int)(r % g.Gx); G = g.Gx; st = 1; }
-        else if (AX == 1) { k = (int)((r / g.Gx) % g.Gy); G = g.Gy; st = g.Gx; }
-        else { k = (int)(r / plane); G = zhi; st = plane; }
-        float m = 0.f;
-#pragma unroll
-        for (int d = 0; d < 4; ++d)
-            if (k + d < G) m = fmaxf(m, fabsf(in[i + d * st]));
-        out[i] = m;
-    }
-}
 
-// Fused prep, step 1: fp64 params -> fp32 phi (as k_params_to_f32) and, per node, the
-// max |phi_c| over the 4 nodes [k, k+3] along x (k_window_max<0>), node layers [zlo, zhi)
+// Prep, step 1: fp64 params -> fp32 phi (as k_params_to_f32) and, per node, the max
+// |phi_c| over the 4 nodes [k, k+3] along x, node layers [zlo, zhi)
 __global__ void k_prep_phi_wx(const double *__restrict__ p, float *__restrict__ phi, float *__restrict__ wx, Geo g,
                               int zlo, int zhi) {
     const long long plane = (long long)g.Gx * g.Gy;
@@ -1812,8 +1776,8 @@ __global__ void k_prep_phi_wx(const double *__restrict__ p, float *__restrict__ 
     }
 }
 
-// Fused prep, step 2: the y and z window max of step 1's x-max (k_window_max<1> and
-// k_window_max_z4 in one pass), base layers [zlo, zb) reading node layers up to zhi
+// Prep, step 2: the y and z window max of step 1's x-max in one pass (-> the 4x4x4 tap
+// window max keyed by the base node), base layers [zlo, zb) reading node layers up to zhi
 __global__ void k_prep_tol(const float *__restrict__ wx, float4 *__restrict__ out, Geo g, int zlo, int zb, int zhi) {
     const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zb - zlo) * plane;
     for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
@@ -1832,22 +1796,6 @@ __global__ void k_prep_tol(const float *__restrict__ wx, float4 *__restrict__ ou
     }
 }
 
-// last (z) pass of the window max, all 3 components of a node into one float4, already
-// scaled to pass 1's tolerance 2e-6 max |phi_c|; base layers [zlo, zb) reading up to zhi
-__global__ void k_window_max_z4(const float *__restrict__ in, float4 *__restrict__ out, Geo g, int zlo, int zb, int zhi) {
-    const long long plane = (long long)g.Gx * g.Gy, cs = (long long)g.Gz * plane, span = (long long)(zb - zlo) * plane;
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)gridDim.x * blockDim.x) {
-        const long long i = (long long)zlo * plane + j;
-        const int k = (int)(i / plane);
-        float m[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-        for (int c = 0; c < 3; ++c)
-#pragma unroll
-            for (int d = 0; d < 4; ++d)
-                if (k + d < zhi) m[c] = fmaxf(m[c], fabsf(in[c * cs + i + d * plane]));
-        out[i] = make_float4(2e-6f * m[0], 2e-6f * m[1], 2e-6f * m[2], 0.f);
-    }
-}
 
 // min / max of a volume (exact; order independent)
 __global__ void k_minmax(const float *__restrict__ v, long long n, float *out /*[2] encoded keys*/) {
