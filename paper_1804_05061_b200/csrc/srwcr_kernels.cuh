@@ -5,12 +5,14 @@
 // ratios, D and the backward coefficient tables), pass 2 (k_pass2: pass 1's (m, dM/dy)
 // per voxel + dD/dm + adjoint B-spline scatter onto the control lattice), k_exact_fix
 // (the voxels whose derivative the fp64 definition must decide).
-// The warped image and every per-voxel intermediate stay in registers (the paper's
-// kernels 1-4 materialise them).  DESIGN.md s5-s6 describe the data flow,
+// Per-voxel intermediates stay in registers except one float4 (m, dM/dy) per voxel that
+// pass 1 streams to pass 2 (the paper's kernels 1-4 materialise the warped image and the
+// derivative volumes).  DESIGN.md s5-s6 describe the data flow,
 // the roofline of each kernel and what differs from the paper's GPU design.
 //
-// Work decomposition (v2): a CTA owns one "item" = a box of voxels inside ONE spatial
-// cell (all its voxels share the same 4x4x4 = 64 regions of Eq 7).  Each warp owns
+// Work decomposition: a CTA owns one "item" = a box of voxels inside ONE spatial cell
+// (all its voxels share the same 4x4x4 = 64 regions of Eq 7) -- or, on fine spatial
+// lattices (MC variants), up to 5 x-cells by 3 z-cells with per-lane region offsets.  Each warp owns
 // whole rows of the item: lane = x (XV voxels per lane: x0+lane, x0+lane+32), and the
 // warp marches z through the item independently of the other warps (no CTA barrier
 // inside the march).  CTA-level tables are touched only at row and item ends.
