@@ -28,11 +28,13 @@ for k, d in seen.items():
         if m in d:
             print(f"   {m:36s} {d[m]}")
 raw = run(["--page", "source", "--csv", "--print-source", "cuda,sass", "-k", f"regex:{kfilter}"])
-# the source page prints one block per kernel; split on 'Function Name'
-blocks = raw.split('"Function Name"')
+# the source page prints one block per (kernel, source file): each starts with a
+# "File Path" row (the kernel file, or a CUDA header holding an inlined intrinsic)
+blocks = raw.split('"File Path"')
 for b in blocks[1:]:
-    rows = list(csv.reader(io.StringIO('"Function Name"' + b)))
-    name = rows[0][1] if len(rows[0]) > 1 else "?"
+    rows = list(csv.reader(io.StringIO('"File Path"' + b)))
+    path = rows[0][1].rsplit("/", 1)[-1] if len(rows[0]) > 1 else "?"
+    name = (rows[1][1] if len(rows) > 1 and len(rows[1]) > 1 else "?")
     hi = [i for i, r in enumerate(rows) if r and r[0] == "Line No"]
     if not hi:
         continue
@@ -49,7 +51,7 @@ for b in blocks[1:]:
             return 0.0
     tot = sum(f(r[ii]) for r in lines)
     stot = sum(f(r[wi]) for r in lines) or 1
-    print(f"== {name[:60]}: warp-instructions {tot:.3e} = {tot / (vox / 32):.0f} per 32 voxels")
+    print(f"== {name[:60]} [{path}]: warp-instructions {tot:.3e} = {tot / (vox / 32):.0f} per 32 voxels")
     st = {hdr[i]: sum(f(r[i]) for r in lines) for i in cols}
     print("   stalls: " + ", ".join(f"{k[6:]} {v / stot * 100:.0f}%" for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:7]))
     for r in sorted(lines, key=lambda r: -f(r[wi]))[:ntop]:
