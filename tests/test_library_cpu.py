@@ -186,3 +186,15 @@ def test_buffer_marshalling_rejects_wrong_params_and_outputs():
         _ptr(torch.zeros(12, dtype=torch.float32), 12, "params")
     with pytest.raises(ValueError):
         _ptr(torch.zeros(4, 6, dtype=torch.float64)[:, ::2], 12, "grad", out=True)
+
+
+def test_missing_library_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: with the CUDA library absent the product path raises instead of
+    computing anything (the oracle is test infrastructure, never a fallback)."""
+    monkeypatch.setattr(S, "_lib", None)
+    monkeypatch.setattr(S, "_LIB", str(tmp_path / "libsrwcr.so"))
+    with pytest.raises(RuntimeError, match="missing"):
+        S.lib()
+    f = np.zeros((4, 8, 8), np.float32)
+    with pytest.raises(RuntimeError, match="missing"):
+        S.Srwcr(f, f, (1.0, 1.0, 1.0), 8, (1, 1, 1), (4.0, 4.0, 4.0))
