@@ -162,9 +162,12 @@ def run_reference(args):
     T = sum(times)
     nvox = nx * ny * nz
     evals_per_s = args.steps * vox / (T * nvox)
+    # a step is the bounded sample (so K steps fit the driver's run); ms_per_step is the time of
+    # the work actually done, value the full-volume-equivalent rate of the same metric
     line = {
         "impl": "reference", "metric": METRIC, "value": evals_per_s, "unit": "evals/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / evals_per_s, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * T / args.steps,
+        "step_fraction_of_eval": vox / nvox, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": workload_desc(args.config, cfg), "phi": args.phi, "seed": args.seed},
         "gvoxel_per_s": evals_per_s * nvox / 1e9,
@@ -281,6 +284,32 @@ def main():
     ms_step = ms / args.steps
     evals = 1e3 / ms_step
 
+    # ---- the same step at the worst-gather Phi point (SURVEY 8(d) Phi_large), a short run
+    phi_large = None
+    if args.phi != "large":
+        pl_np = synth.make_params(g.params_shape, "large", args.seed)
+        pl = torch.from_numpy(pl_np).cuda()
+        for _ in range(3):
+            g.eval(pl, grad=grad)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        nl = max(5, args.steps // 4)
+        e0.record(stream)
+        for _ in range(nl):
+            g.eval(pl, grad=grad)
+        e1.record(stream)
+        e1.synchronize()
+        msl = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([msl], device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            msl = float(t.item())
+        st = g.stats()
+        phi_large = {"value": nl * 1e3 / msl, "unit": "evals/s", "ms_per_step": msl / nl, "steps": nl,
+                     "exact_voxels": st["exact_voxels"]}
+        del pl
+
     # ---- end to end through the public API with pinned HOST buffers (H2D params, D2H D + grad)
     g.set_timing(False)
     hp = torch.from_numpy(params_np.copy()).pin_memory()
@@ -312,7 +341,9 @@ def main():
         bytes_p1 = 8 * vox_rank + 12 * G
         bytes_p2 = 8 * vox_rank + 12 * G + 24 * G
         t1, t2 = statistics.mean(p1), statistics.mean(p2)
-        dom, tdom, bdom = ("k_pass1", t1, bytes_p1) if t1 >= t2 else ("k_pass2", t2, bytes_p2)
+        fast = g.stats()["fast_path"] == 1
+        n1, n2 = ("k_p1f", "k_p2f") if fast else ("k_pass1", "k_pass2")
+        dom, tdom, bdom = (n1, t1, bytes_p1) if t1 >= t2 else (n2, t2, bytes_p2)
         achieved = bdom / (tdom * 1e-3) / 1e9
         traffic = None
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -325,7 +356,16 @@ def main():
         if not args.no_cpu_baseline and ws == 1:   # the oracle baseline: rank 0 at N = 1 only
             slices = args.cpu_sample_slices or auto_slices(cfg)
             dt, vox, threads = oracle_sample(args.config, cfg, F, M, params_np, slices)
+            s1 = max(1, slices // 16)   # single-thread figure on a smaller slab
+            dt1, vox1, _ = oracle_sample(args.config, cfg, F, M, params_np, s1, nthreads=1)
+            try:
+                aff = len(os.sched_getaffinity(0))
+            except Exception:
+                aff = None
             cpu = {"value": vox / (dt * nvox), "unit": "evals/s", "cores": threads, "kind": "oracle",
+                   "cores_affinity": aff, "cpu_count": os.cpu_count(),
+                   "single_thread": {"value": vox1 / (dt1 * nvox), "unit": "evals/s", "cores": 1,
+                                     "sample": f"z-slab [0,{s1}) ({vox1} voxels) in {dt1:.1f} s"},
                    "sample": f"z-slab [0,{slices}) of {nz} slices ({vox} voxels), fp64 moment route "
                              f"(pass 1 + combine + pass 2) in {dt:.1f} s, scaled to the full volume"}
         line = {
@@ -345,8 +385,10 @@ def main():
             "e2e": {"value": e2e, "unit": "evals/s", "h2d_bytes_per_step": int(params_np.nbytes),
                     "d2h_bytes_per_step": int(params_np.nbytes) + 8},
             "gpu_launches": int(launches),
-            "decomposition": {k: g.stats()[k] for k in ("warps_per_cta", "slot_capacity", "voxels_per_lane", "items",
+            "decomposition": {k: g.stats()[k] for k in ("fast_path", "fast_items", "fast_warps", "fast_slots",
+                                                        "warps_per_cta", "slot_capacity", "voxels_per_lane", "items",
                                                         "warps_per_cta2", "items2")},
+            "phi_large": phi_large,
             "clocks": clk.summary(),
             "D": D,
             "paper_workloads": None if args.no_paper_workloads or ws > 1 else paper_workloads(local),

@@ -226,12 +226,17 @@ srwcr_status srwcr_upsample2_field(const float *coarse, const int64_t coarse_dim
  *   SRWCR_DUMP_SQ               S[r][a], Q[r][a] of the last pass 1 (unshifted), fp64 [2][R][L+1]
  *   SRWCR_DUMP_REGIONS          per region {p(r), sigma_r^2, mu_r, 1-CR_r, retained, Z}, fp64 [R][6]
  *   SRWCR_DUMP_COEFS            alpha[R], beta[R], gamma[R][L+1] (fp32) of the last combine
+ *   SRWCR_DUMP_WARPED           pass 1's per-voxel (m, dM/dy_x, dM/dy_y, dM/dy_z) of this rank's
+ *                               z-slab after the last evaluation, fp32 [z1-z0][Ny][Nx][4]: the warped
+ *                               moving intensity m = M(T(x)) that decides the dynamic Parzen bin
+ *                               n(m) = min(floor m, L-1) (Eq 5) -- for the fp32-vs-fp64 bin
+ *                               mismatch report
  *   SRWCR_DUMP_DDM              per-voxel dD/dm of the last pass 2 is not stored: ENOTSUP
  * `bytes` must be at least the size given by srwcr_debug_size. */
 enum {
     SRWCR_DUMP_FIXED = 1, SRWCR_DUMP_MOVING = 2, SRWCR_DUMP_A0 = 3, SRWCR_DUMP_CTRL_TAPS = 4,
     SRWCR_DUMP_SPAT_TAPS = 5, SRWCR_DUMP_N = 6, SRWCR_DUMP_SQ = 7, SRWCR_DUMP_REGIONS = 8,
-    SRWCR_DUMP_COEFS = 9
+    SRWCR_DUMP_COEFS = 9, SRWCR_DUMP_WARPED = 10
 };
 srwcr_status srwcr_debug_size(const srwcr_ctx *ctx, int32_t what, size_t *bytes);
 srwcr_status srwcr_debug_dump(srwcr_ctx *ctx, int32_t what, void *out, size_t bytes);
@@ -254,6 +259,11 @@ typedef struct {
                                    part of the params upload (0: not pipelined) */
     int32_t pipe_items2;        /* pass-2 items after which the final gradient layers go back
                                    while the rest run (0: not pipelined) */
+    int32_t fast_path;          /* 1: the round-2 passes of srwcr_fast.cuh evaluate (coarse
+                                   spatial lattice, orientation 0, 3-D); 0: round-1 passes */
+    int32_t fast_items;         /* work items (CTAs) of the fast passes on this rank */
+    int32_t fast_warps;         /* warps per CTA of the fast passes */
+    int32_t fast_slots;         /* line-table slot stride (max fixed bins of an item + 2) */
 } srwcr_stats;
 srwcr_status srwcr_set_timing(srwcr_ctx *ctx, int32_t enable);
 srwcr_status srwcr_get_stats(const srwcr_ctx *ctx, srwcr_stats *out);

@@ -19,7 +19,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
 _LIB = os.path.join(_HERE, "libsrwcr.so")
-_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("srwcr.cu", "srwcr_kernels.cuh", "srwcr_register.inc",
+_SRCS = [os.path.join(_HERE, "csrc", f) for f in ("srwcr.cu", "srwcr_kernels.cuh", "srwcr_fast.cuh", "srwcr_register.inc",
                                                   "srwcr_fields.inc")]
 _HDR = os.path.join(_ROOT, "include", "srwcr.h")
 
@@ -28,7 +28,7 @@ NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", 
 
 # status codes (include/srwcr.h)
 OK, EINVAL, ENOMEM, ECUDA, ENCCL, EDEGENERATE, ENOTSUP, ESTATE, ENONFINITE = 0, -1, -2, -3, -4, -5, -6, -7, -8
-DUMP = dict(fixed=1, moving=2, a0=3, ctrl_taps=4, spat_taps=5, N=6, SQ=7, regions=8, coefs=9)
+DUMP = dict(fixed=1, moving=2, a0=3, ctrl_taps=4, spat_taps=5, N=6, SQ=7, regions=8, coefs=9, warped=10)
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -64,7 +64,9 @@ class _Stats(ctypes.Structure):
                 ("voxels_per_lane", ctypes.c_int32), ("items", ctypes.c_int32), ("ms_prep", ctypes.c_float),
                 ("warps_per_cta2", ctypes.c_int32), ("items2", ctypes.c_int32),
                 ("exact_voxels", ctypes.c_int32), ("exact_capacity", ctypes.c_int32),
-                ("pipe_items1", ctypes.c_int32), ("pipe_items2", ctypes.c_int32)]
+                ("pipe_items1", ctypes.c_int32), ("pipe_items2", ctypes.c_int32),
+                ("fast_path", ctypes.c_int32), ("fast_items", ctypes.c_int32), ("fast_warps", ctypes.c_int32),
+                ("fast_slots", ctypes.c_int32)]
 
 
 class _LbfgsConfig(ctypes.Structure):
@@ -236,14 +238,27 @@ class Srwcr:
         if want_grad and grad is None:
             grad = np.empty(self.params_shape, dtype=np.float64)
         gp, gk = _ptr(grad, n, "grad", out=True) if want_grad else (None, None)
+        self._order_after_caller(pk, gk)
         D = ctypes.c_double()
         st = lib().srwcr_eval(self._ctx, pp, ctypes.byref(D), gp)
         self._check(st)
         return D.value, (grad if want_grad else None)
 
+    def _order_after_caller(self, *tensors):
+        """The library works on its own stream: when params / grad are CUDA tensors, order it
+        after torch's current stream (pending writes of params, reads of an earlier grad).  The
+        call returns after its stream has finished, so later torch work is ordered too."""
+        if not any(getattr(t, "is_cuda", False) for t in tensors):
+            return
+        import torch
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream())
+        torch.cuda.ExternalStream(self.stream_handle()).wait_event(ev)
+
     def eval_begin(self, params):
         pp, pk = _ptr(params if hasattr(params, "data_ptr") else np.ascontiguousarray(params, dtype=np.float64),
                       self._nparams, "params")
+        self._order_after_caller(pk)
         self._check(lib().srwcr_eval_begin(self._ctx, pp))
 
     def stats_buffer(self):
@@ -312,7 +327,7 @@ class Srwcr:
         n = ctypes.c_size_t()
         self._check(lib().srwcr_debug_size(self._ctx, code, ctypes.byref(n)))
         dtype = {"fixed": np.float32, "moving": np.float32, "a0": np.int16, "ctrl_taps": np.int32,
-                 "spat_taps": np.int32, "coefs": np.float32}.get(what, np.float64)
+                 "spat_taps": np.int32, "coefs": np.float32, "warped": np.float32}.get(what, np.float64)
         out = np.empty(n.value // np.dtype(dtype).itemsize, dtype=dtype)
         self._check(lib().srwcr_debug_dump(self._ctx, code, out.ctypes.data_as(ctypes.c_void_p), n.value))
         return out

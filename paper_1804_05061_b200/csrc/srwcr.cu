@@ -20,6 +20,7 @@
 
 #include "../../include/srwcr.h"
 #include "srwcr_kernels.cuh"
+#include "srwcr_fast.cuh"
 
 using namespace srwcr;
 
@@ -127,6 +128,21 @@ struct srwcr_ctx {
     double *dot_part = nullptr;   // deterministic dot-product partials
     double *dot_host = nullptr;   // pinned, 16 doubles
     int64_t gram_G = 0;
+    // round-2 fast passes (coarse spatial lattice, orientation 0; srwcr_fast.cuh)
+    bool fast = false;
+    int fXV = 1, fW = 16, fS = 0, nfitems = 0;
+    size_t fsmem1 = 0;
+    FItem *fitems = nullptr;
+    ItemW *fitemw = nullptr;
+    int *fslotbins = nullptr, *fiflag = nullptr;
+    unsigned *frec = nullptr, *floff = nullptr, *flent = nullptr;
+    uint4 *frmask = nullptr;
+    unsigned long long *SQi = nullptr;   // int64 statistics (units 2^-16), same layout as SQ
+    unsigned long long *gradi = nullptr; // int64 gradient (units 2^-k of Z dD/dphi)
+    int fW2 = 16, fnpmax = 0;
+    size_t fsmem2 = 0;
+    float fdxz = 1.f;
+    std::vector<FItem> h_fitems;
 };
 
 static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
@@ -374,6 +390,7 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     ca.alpha = c->alpha; ca.beta = c->beta; ca.gamma = c->gamma;
     ca.NQ = c->NQ; ca.gstride = c->gstride;
     ca.ticket = c->ticket; ca.Dout = c->Dout; ca.part = c->dpart;   // D reduced by the launch's last CTA
+    ca.gbound = c->Dout + 2;
     const unsigned nb = (unsigned)std::min<int64_t>((c->R + 7) / 8, 148 * 8);   // fixed grid (deterministic D)
     if (c->opt.orientation) k_combineA<<<nb, 256, 0, c->stream>>>(ca);
     else k_combine<<<nb, 256, 0, c->stream>>>(ca);
@@ -381,6 +398,291 @@ static srwcr_status run_combine(srwcr_ctx *c) {
     return SRWCR_OK;
 }
 
+
+// ------------------------------------------------------------------ round-2 fast passes
+// Items, static fixed-image records and per-line touched-slot lists of srwcr_fast.cuh.
+// Eligible: 3-D, orientation 0, coarse spatial lattice (no multi-cell items), every
+// x-chunk reading at most 32 control x-nodes.  SRWCR_NOFAST=1 keeps the round-1 passes.
+static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
+    const Geo &g = c->g;
+    if (getenv("SRWCR_NOFAST")) return SRWCR_OK;
+    if (g.nz == 1 || c->opt.orientation != 0 || c->MC || c->z1 <= c->z0) return SRWCR_OK;
+    int XV = c->XV;
+    if (const char *e = getenv("SRWCR_FXV")) XV = std::min(XV, std::max(1, atoi(e)));
+    int ymax = 32, zmax = FZMAX;
+    std::vector<Item> its;
+    for (;;) {
+        its.clear();
+        auto xr = runs(c->h_sb[0], 0, g.nx, 32 * XV);
+        auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
+        auto zr = runs(c->h_sb[2], (int)c->z0, (int)c->z1, zmax);
+        for (auto &zz : zr)
+            for (auto &yy : yr)
+                for (auto &xx : xr) its.push_back(Item{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second, 0, 0, 0.f, 0});
+        if ((long long)its.size() * 2 < 3LL * nsm && (ymax > 16 || zmax > 16)) {
+            if (ymax > 16) ymax = 16;
+            else zmax /= 2;
+            continue;
+        }
+        break;
+    }
+    for (const Item &it : its) {
+        const int nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
+        if (nxn > 32 || it.zlen > FZMAX) return SRWCR_OK;   // not eligible: round-1 passes
+    }
+    const size_t n = its.size();
+    // per item: fixed bins present, binless shift, spatial weight sums
+    Item *d_it = nullptr;
+    unsigned *d_mask = nullptr;
+    double *d_sum = nullptr;
+    CK(cudaMalloc(&d_it, sizeof(Item) * n));
+    CK(cudaMalloc(&d_mask, sizeof(unsigned) * 4 * n));
+    CK(cudaMalloc(&d_sum, sizeof(double) * n));
+    CK(cudaMemcpy(d_it, its.data(), sizeof(Item) * n, cudaMemcpyHostToDevice));
+    k_item_scan<<<(unsigned)n, 256, 0, c->stream>>>(c->F, c->M, d_it, g, d_mask, d_sum);
+    CKL();
+    std::vector<unsigned> mask(4 * n);
+    std::vector<double> sum(n);
+    CK(cudaMemcpyAsync(mask.data(), d_mask, sizeof(unsigned) * 4 * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(sum.data(), d_sum, sizeof(double) * n, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_it);
+    cudaFree(d_mask);
+    cudaFree(d_sum);
+    std::vector<FItem> fi(n);
+    std::vector<ItemW> w(n);
+    std::vector<int> slotbins;
+    long long lines = 0, rows = 0;
+    int smax = 1;
+    for (size_t i = 0; i < n; ++i) {
+        const Item &it = its[i];
+        FItem &f = fi[i];
+        f.x0 = it.x0; f.xlen = it.xlen; f.y0 = it.y0; f.ylen = it.ylen; f.z0 = it.z0; f.zlen = it.zlen;
+        f.slot_off = (int)slotbins.size();
+        int ns = 0;
+        for (int b = 0; b < g.B; ++b)
+            if ((mask[4 * i + (b >> 5)] >> (b & 31)) & 1u) { slotbins.push_back(b); ++ns; }
+        f.nslots = ns;
+        smax = std::max(smax, ns);
+        f.line_off = (int)lines;
+        f.row_off = (int)rows;
+        lines += (long long)it.ylen * it.zlen;
+        rows += it.ylen;
+        f.cI = (float)(sum[i] / ((double)it.xlen * it.ylen * it.zlen));
+        f.pad = 0;
+        ItemW &iw = w[i];
+        for (int l = 0; l < 8; ++l) iw.sx[l] = iw.sz[l] = 0.0;
+        for (int l = 0; l < 4; ++l) iw.sy[l] = 0.0;
+        const int lo[3] = {it.x0, it.y0, it.z0}, len[3] = {it.xlen, it.ylen, it.zlen};
+        double *dst[3] = {iw.sx, iw.sy, iw.sz};
+        for (int ax = 0; ax < 3; ++ax)
+            for (int k = lo[ax]; k < lo[ax] + len[ax]; ++k) {
+                const float4 q = c->h_sw[ax][k];
+                dst[ax][0] += q.x; dst[ax][1] += q.y; dst[ax][2] += q.z; dst[ax][3] += q.w;
+            }
+    }
+    if (lines >= (1LL << 31) || smax + 2 > 255) return SRWCR_OK;
+    const int S = smax + 2;   // + binless pseudo-slot + dummy slot of padding lanes
+    int maxsm = 0;
+    cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
+    int W = 0;
+    for (int Wc : {16, 12, 8, 4})
+        if (!W && p1_smem(Wc, S).total <= maxsm) W = Wc;
+    if (const char *e = getenv("SRWCR_FW")) {   // experiments: up to 24 warps (XV 1: <= 85 registers)
+        const int w = std::max(1, atoi(e));
+        if (w <= 16 || (XV == 1 && w <= 24 && p1_smem(w, S).total <= maxsm)) W = w;
+    }
+    if (W == 0) return SRWCR_OK;
+    // device copies
+    CK(cudaMalloc(&c->fitems, sizeof(FItem) * n));
+    CK(cudaMemcpy(c->fitems, fi.data(), sizeof(FItem) * n, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->fitemw, sizeof(ItemW) * n));
+    CK(cudaMemcpy(c->fitemw, w.data(), sizeof(ItemW) * n, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->fslotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
+    CK(cudaMemcpy(c->fslotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->fiflag, sizeof(int) * n));
+    CK(cudaMemset(c->fiflag, 0, sizeof(int) * n));
+    const long long slab = (c->z1 - c->z0) * (long long)g.nxy;
+    CK(cudaMalloc(&c->frec, sizeof(unsigned) * slab));
+    k_frec<<<(unsigned)n, 256, 0, c->stream>>>(c->F, c->fitems, c->fslotbins, g, (int)c->z0, c->frec);
+    CKL();
+    // per-line lists: count, prefix sum on the host, write
+    std::vector<int> iol(lines);
+    for (size_t i = 0; i < n; ++i)
+        for (long long k = 0; k < (long long)fi[i].ylen * fi[i].zlen; ++k) iol[fi[i].line_off + k] = (int)i;
+    int *d_iol = nullptr;
+    unsigned *d_cnt = nullptr;
+    CK(cudaMalloc(&d_iol, sizeof(int) * lines));
+    CK(cudaMalloc(&d_cnt, sizeof(unsigned) * lines));
+    CK(cudaMemcpy(d_iol, iol.data(), sizeof(int) * lines, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->frmask, sizeof(uint4) * rows));
+    CK(cudaMemset(c->frmask, 0, sizeof(uint4) * rows));
+    const unsigned lb = (unsigned)((lines * 32 + 255) / 256);
+    if (XV == 2) k_lists<2><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, d_cnt, nullptr, nullptr, nullptr, lines, 0);
+    else k_lists<1><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, d_cnt, nullptr, nullptr, nullptr, lines, 0);
+    CKL();
+    std::vector<unsigned> cnt(lines), off(lines + 1);
+    CK(cudaMemcpyAsync(cnt.data(), d_cnt, sizeof(unsigned) * lines, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    off[0] = 0;
+    for (long long i = 0; i < lines; ++i) off[i + 1] = off[i] + cnt[i];
+    CK(cudaMalloc(&c->floff, sizeof(unsigned) * (lines + 1)));
+    CK(cudaMemcpy(c->floff, off.data(), sizeof(unsigned) * (lines + 1), cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&c->flent, sizeof(unsigned) * std::max<unsigned>(1, off[lines])));
+    if (XV == 2) k_lists<2><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, nullptr, c->floff, c->flent, reinterpret_cast<unsigned *>(c->frmask), lines, 1);
+    else k_lists<1><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, nullptr, c->floff, c->flent, reinterpret_cast<unsigned *>(c->frmask), lines, 1);
+    CKL();
+    CK(cudaStreamSynchronize(c->stream));
+    cudaFree(d_iol);
+    cudaFree(d_cnt);
+    CK(cudaMalloc(&c->SQi, sizeof(unsigned long long) * stats_count(c)));
+    CK(cudaMemset(c->SQi, 0, sizeof(unsigned long long) * stats_count(c)));
+    c->fXV = XV;
+    c->fW = W;
+    c->fS = S;
+    c->nfitems = (int)n;
+    c->fsmem1 = p1_smem(W, S).total;
+    c->h_fitems = fi;
+    // pass 2: node window and warps per CTA
+    int npmax = 0;
+    for (const FItem &f : fi) {
+        const int nxn = c->h_cb[0][f.x0 + f.xlen - 1] + 4 - c->h_cb[0][f.x0];
+        const int nyn = c->h_cb[1][f.y0 + f.ylen - 1] + 4 - c->h_cb[1][f.y0];
+        const int nzn = c->h_cb[2][f.z0 + f.zlen - 1] + 4 - c->h_cb[2][f.z0];
+        npmax = std::max(npmax, nzn * 3 * nyn * nxn);
+    }
+    int W2 = 0;
+    for (int Wc : {16, 12, 8, 4})
+        if (!W2 && p2_smem(Wc, S, npmax).total <= maxsm) W2 = Wc;
+    if (const char *e = getenv("SRWCR_FW2")) W2 = std::min(W2, std::max(1, atoi(e)));
+    if (W2 == 0) return SRWCR_OK;
+    c->fW2 = W2;
+    c->fnpmax = npmax;
+    c->fsmem2 = p2_smem(W2, S, npmax).total;
+    c->fdxz = (float)((std::ceil(c->delta[0]) + 1.0) * (std::ceil(c->delta[2]) + 1.0));
+    CK(cudaMalloc(&c->gradi, sizeof(unsigned long long) * c->nparams));
+    CK(cudaMemset(c->gradi, 0, sizeof(unsigned long long) * c->nparams));
+    {
+        const int sm = (int)c->fsmem2;
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        if (XV == 2) {
+            CK(cudaFuncSetAttribute(k_p2f<2, 512>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<2, 384>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<2, 256>, attr, sm));
+        } else {
+            CK(cudaFuncSetAttribute(k_p2f<1, 512>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<1, 384>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<1, 256>, attr, sm));
+        }
+    }
+    {
+        const int sm = (int)c->fsmem1;
+        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+        if (XV == 2) {
+            CK(cudaFuncSetAttribute(k_p1f<2, 512>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<2, 384>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<2, 256>, attr, sm));
+        } else {
+            CK(cudaFuncSetAttribute(k_p1f<1, 768>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<1, 512>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<1, 384>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<1, 256>, attr, sm));
+        }
+    }
+    c->fast = true;
+    return SRWCR_OK;
+}
+
+static FArgs fast_args(srwcr_ctx *c) {
+    FArgs a{};
+    a.g = c->g;
+    for (int i = 0; i < 3; ++i) {
+        a.t.cb[i] = c->cb[i]; a.t.cw[i] = c->cw[i]; a.t.cw64[i] = c->cw64[i]; a.t.sb[i] = c->sb[i]; a.t.sw[i] = c->sw[i];
+    }
+    a.M = c->M; a.phi = c->phi; a.rec = c->frec; a.loff = c->floff; a.lent = c->flent; a.rmask = c->frmask;
+    a.items = c->fitems; a.itemw = c->fitemw; a.slotbins = c->fslotbins; a.iflag = c->fiflag; a.shiftc = c->shiftc;
+    a.SQi = c->SQi; a.Qi = c->SQi + (size_t)c->R * c->g.B * 2;
+    a.MG = c->MG; a.mgz0 = (int)c->z0;
+    a.S = c->fS; a.W = c->fW; a.i0 = 0;
+    a.L1 = p1_smem(c->fW, c->fS);
+    a.ablate = 0;
+    if (const char *e = getenv("SRWCR_ABLATE")) a.ablate = atoi(e);
+    return a;
+}
+
+// fast pass 1 over items [i0, i0 + cnt) and the int64 -> fp64 statistics conversion
+static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bool convert = true) {
+    FArgs a = fast_args(c);
+    a.i0 = i0;
+    const int n = cnt >= 0 ? cnt : c->nfitems - i0;
+    if (n > 0) {
+        const int T = 32 * c->fW;
+        if (c->fXV == 2) {
+            if (T > 384) k_p1f<2, 512><<<n, T, c->fsmem1, c->stream>>>(a);
+            else if (T > 256) k_p1f<2, 384><<<n, T, c->fsmem1, c->stream>>>(a);
+            else k_p1f<2, 256><<<n, T, c->fsmem1, c->stream>>>(a);
+        } else {
+            if (T > 512) k_p1f<1, 768><<<n, T, c->fsmem1, c->stream>>>(a);
+            else if (T > 384) k_p1f<1, 512><<<n, T, c->fsmem1, c->stream>>>(a);
+            else if (T > 256) k_p1f<1, 384><<<n, T, c->fsmem1, c->stream>>>(a);
+            else k_p1f<1, 256><<<n, T, c->fsmem1, c->stream>>>(a);
+        }
+        CKL();
+    }
+    if (convert) {
+        k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c));
+        CKL();
+    }
+    return SRWCR_OK;
+}
+
+// per-eval flags of the fast items (the fp32 phi itself comes from k_prep_phi_wx)
+static srwcr_status launch_fast_prep(srwcr_ctx *c, const double *pd) {
+    Tables t{};
+    for (int i = 0; i < 3; ++i) { t.cb[i] = c->cb[i]; t.cw[i] = c->cw[i]; t.sb[i] = c->sb[i]; t.sw[i] = c->sw[i]; }
+    const int nconv = 296;   // blocks converting the params layers [pz0, pz1) to fp32; then one per item
+    k_fprep<<<(unsigned)(nconv + c->nfitems), 256, 0, c->stream>>>(pd, c->phi, c->g, c->pz0, c->pz1, nconv, c->fitems,
+                                                                    c->nfitems, t, c->fiflag);
+    CKL();
+    return SRWCR_OK;
+}
+
+// fast pass 2 (+ the fp64 exact-path voxels, + the int64 -> fp64 gradient conversion)
+static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad) {
+    F2Args A{};
+    A.f = fast_args(c);
+    A.MG = c->MG;
+    A.alpha = c->alpha; A.beta = c->beta; A.gamma = c->gamma;
+    A.gbound = c->Dout + 2;
+    A.dxz = c->fdxz;
+    A.gradi = c->gradi;
+    A.xlist = c->xlist; A.xcount = c->xcount; A.xcap = c->xcap;
+    A.npmax = c->fnpmax;
+    A.f.W = c->fW2;
+    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax);
+    CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
+    const int n = c->nfitems, T = 32 * c->fW2;
+    if (c->fXV == 2) {
+        if (T > 384) k_p2f<2, 512><<<n, T, c->fsmem2, c->stream>>>(A);
+        else if (T > 256) k_p2f<2, 384><<<n, T, c->fsmem2, c->stream>>>(A);
+        else k_p2f<2, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+    } else {
+        if (T > 384) k_p2f<1, 512><<<n, T, c->fsmem2, c->stream>>>(A);
+        else if (T > 256) k_p2f<1, 384><<<n, T, c->fsmem2, c->stream>>>(A);
+        else k_p2f<1, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+    }
+    CKL();
+    PassArgs pa = pass_args(c);
+    pa.invZ = 1.f;              // the int64 gradient holds Z dD/dphi
+    pa.gradi = c->gradi;
+    pa.gbound = c->Dout + 2;
+    pa.dxz = c->fdxz;
+    k_exact_fix<0><<<1184, 128, 0, c->stream>>>(pa);
+    CKL();
+    k_grad_convert<<<592, 256, 0, c->stream>>>(c->gradi, grad, (long long)c->nparams, c->Dout + 2, c->fdxz, 1.0 / c->Z);
+    CKL();
+    return SRWCR_OK;
+}
 
 static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *moving, const int64_t dims[3],
                                 const double sp[3], int32_t bins, const int32_t sbins[3], const double csp[3]) {
@@ -765,9 +1067,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->S_out, sizeof(double) * RB));
     CK(cudaMalloc(&c->dterm, sizeof(double) * c->R));
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
-    CK(cudaMalloc(&c->Dout, sizeof(double) * 2));
+    CK(cudaMalloc(&c->Dout, sizeof(double) * 4));   // D, #retained, gradient bound (fast pass 2)
+    CK(cudaMemset(c->Dout, 0, sizeof(double) * 4));
     CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
-    CK(cudaMalloc(&c->dpart, sizeof(double) * 2 * (size_t)std::min<int64_t>((c->R + 7) / 8, 148 * 8)));
+    CK(cudaMalloc(&c->dpart, sizeof(double) * 3 * (size_t)std::min<int64_t>((c->R + 7) / 8, 148 * 8)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
     CK(cudaMalloc(&c->shiftc, sizeof(float) * g.B));
     CK(cudaMalloc(&c->alpha, sizeof(float) * c->R));
@@ -828,7 +1131,10 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     }
 
     // static weighted counts N[r][a] (lower / upper Parzen half) over the whole volume
-    // (every rank holds the full F, so no create-time collective is needed)
+    // (every rank holds the full F, so no create-time collective is needed).  The work above
+    // ran on the legacy stream (uploads, normalisation, scans, memsets): order it before the
+    // context stream's first launch.
+    CK(cudaDeviceSynchronize());
     CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
     TRY(launch_pass1(c, true, true));
     k_split_counts<<<512, 256, 0, c->stream>>>(c->SQ, c->Nlo, c->Nup, RB);
@@ -863,6 +1169,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         }
     }
     c->launches_per_eval = 6;  // prep (phi + x-max, y/z-max), pass 1, combine (+ D), pass 2, exact fix
+    TRY(build_fast(c, nsm));
+    if (c->fast) c->launches_per_eval = 7;   // prep, pass 1, stats conversion, combine, pass 2, exact fix, gradient conversion
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -918,7 +1226,7 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
     // only the node layers this rank's slab reads: taps of slices [z0, z1) (all of them on
     // one rank), converted to fp32, and their tap-window max |phi_c| (x, y into scratch,
     // z -> float4) for pass 1's rounding bound
-    {
+    if (!c->fast) {
         const size_t G = (size_t)c->g.Gx * c->g.Gy * c->g.Gz;
         float *s1 = c->phimax + 4 * G;
         k_prep_phi_wx<<<592, 256, 0, c->stream>>>(pd, c->phi, s1, c->g, c->pz0, c->pz1);
@@ -927,9 +1235,15 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
                                                c->pz1);
         CKL();
     }
-    CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
-    if (c->timing) CK(record_ev(c, 0));
-    TRY(launch_pass1(c, false));
+    if (c->fast) {
+        TRY(launch_fast_prep(c, pd));
+        if (c->timing) CK(record_ev(c, 0));
+        TRY(launch_fast_pass1(c));
+    } else {
+        CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
+        if (c->timing) CK(record_ev(c, 0));
+        TRY(launch_pass1(c, false));
+    }
     if (c->timing) CK(record_ev(c, 1));
     return SRWCR_OK;
 }
@@ -943,8 +1257,12 @@ static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_gra
     const bool grad_dev = grad && (gdev < 0 ? is_device_ptr(grad) : gdev != 0);
     if (grad) {
         gd = grad_dev ? grad : c->grad64;
-        CK(cudaMemsetAsync(gd, 0, sizeof(double) * c->nparams, c->stream));
-        TRY(launch_pass2(c, gd));
+        if (c->fast) {
+            TRY(launch_fast_pass2(c, gd));
+        } else {
+            CK(cudaMemsetAsync(gd, 0, sizeof(double) * c->nparams, c->stream));
+            TRY(launch_pass2(c, gd));
+        }
         if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
     }
     if (c->timing) CK(record_ev(c, 3));
@@ -1110,7 +1428,7 @@ extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *v
     if (c->opt.use_graph && !c->comm && !c->poisoned && params && is_device_ptr(params) &&
         (!grad || is_device_ptr(grad)))
         return eval_graph(c, params, value, grad);
-    if (!c->comm && !c->timing && !c->poisoned && params && (c->p1_split > 0 || c->p2_split > 0) &&
+    if (!c->comm && !c->timing && !c->poisoned && !c->fast && params && (c->p1_split > 0 || c->p2_split > 0) &&
         !is_device_ptr(params) && (!grad || !is_device_ptr(grad)))
         return eval_host_pipelined(c, params, value, grad);
     TRY(eval_begin_impl(c, params));
@@ -1150,6 +1468,7 @@ extern "C" srwcr_status srwcr_debug_size(const srwcr_ctx *c, int32_t what, size_
         case SRWCR_DUMP_SQ: *bytes = sizeof(double) * (RB + c->R); break;
         case SRWCR_DUMP_REGIONS: *bytes = sizeof(double) * c->R * 6; break;
         case SRWCR_DUMP_COEFS: *bytes = sizeof(float) * (2 * c->R + RB); break;
+        case SRWCR_DUMP_WARPED: *bytes = sizeof(float4) * (size_t)((c->z1 - c->z0) * (long long)c->g.nxy); break;
         default: return SRWCR_EINVAL;
     }
     return SRWCR_OK;
@@ -1207,6 +1526,7 @@ extern "C" srwcr_status srwcr_debug_dump(srwcr_ctx *c, int32_t what, void *out, 
             break;
         }
         case SRWCR_DUMP_REGIONS: CK(cudaMemcpy(out, c->reg, need, cudaMemcpyDeviceToHost)); break;
+        case SRWCR_DUMP_WARPED: CK(cudaMemcpy(out, c->MG, need, cudaMemcpyDeviceToHost)); break;
         case SRWCR_DUMP_COEFS:
             CK(cudaMemcpy(out, c->alpha, sizeof(float) * c->R, cudaMemcpyDeviceToHost));
             CK(cudaMemcpy((float *)out + c->R, c->beta, sizeof(float) * c->R, cudaMemcpyDeviceToHost));
@@ -1240,6 +1560,10 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->pipe_items1 = c->p1_split;
     out->pipe_items2 = c->p2_split;
     out->exact_voxels = c->pinned ? reinterpret_cast<const int *>(c->pinned + 2)[0] : 0;
+    out->fast_path = c->fast ? 1 : 0;
+    out->fast_items = c->nfitems;
+    out->fast_warps = c->fW;
+    out->fast_slots = c->fS;
     return SRWCR_OK;
 }
 extern "C" srwcr_status srwcr_stream(const srwcr_ctx *c, void **stream) {
@@ -1261,7 +1585,8 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     if (c->cstream) cudaStreamDestroy(c->cstream);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
-                    c->beta, c->gamma, c->ticket, c->dpart, c->xbeg};
+                    c->beta, c->gamma, c->ticket, c->dpart, c->xbeg, c->fitems, c->fitemw, c->fslotbins,
+                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

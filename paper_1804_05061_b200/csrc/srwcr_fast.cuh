@@ -1,0 +1,1340 @@
+// srwcr_fast.cuh -- round-2 sm_100a passes of the SRWCR hot path for the coarse spatial
+// lattice in the moving-as-B orientation (every config whose spatial x-cells are >= 32
+// voxels wide; the fine-lattice (MC) and moving-as-A (ORI 1) variants stay in
+// srwcr_kernels.cuh).  DESIGN.md s6 gives the instruction / byte budget behind each choice.
+//
+// What changed against round 1 (same method, same per-voxel arithmetic, fewer instructions):
+//  * static fixed-image record: F never changes in this orientation, so its Parzen bin a0
+//    and upper weight h_hi (Eq 5) are decided ONCE at create and stored per voxel
+//    as a 32-bit record  slot << 24 | round(h_hi 2^23)  (slot = the item-local index of
+//    a0); the passes read it instead of F (same 4 B/voxel);
+//  * static per-line touched-slot lists (F static => the bins of each 32*XV-voxel line are
+//    known at create): the line fold visits exactly the touched (slot, entry) pairs, and
+//    the per-entry add counts let the line-table atomics skip the magic-number offset
+//    subtraction;
+//  * magic-number floor / int conversions (full-rate FADD.RM + IADD) instead of FRND / F2I
+//    (quarter-rate conversion pipe, measured in tools/microbench/micro3.cu);
+//  * packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2) over the lane's two voxels;
+//  * deterministic accumulation: int32 line tables, per-warp fp32 column tables folded
+//    into the CTA cell table in a fixed order (one barrier per round of rows), and int64
+//    fixed-point global statistics (units 2^-16) -- two evaluations are bitwise identical;
+//  * per-item interior flag (convex-hull bound of the displacement: u is a convex
+//    combination of the supporting node values): items whose samples can never clamp
+//    run a variant without the clamp logic of reading c2.
+#pragma once
+#include "srwcr_kernels.cuh"
+
+namespace srwcr {
+
+constexpr float MAGIC = 12582912.f;        // 1.5 * 2^23: float bits 0x4B400000 + round(x), |x| < 2^22
+constexpr int MAGIC_I = 0x4B400000;
+constexpr double STAT_UNIT = 65536.0;      // global statistics: int64 fixed point, units 2^-16
+constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
+constexpr int FZMAX = 128;                 // max slices per item
+
+struct FItem {
+    int x0, xlen, y0, ylen, z0, zlen;
+    int slot_off, nslots;   // the item's fixed bins a0, ascending (slotbins)
+    int line_off;           // line (row r, slice z) = line_off + r * zlen + (z - z0)
+    int row_off;            // row mask index of row r = row_off + r
+    float cI;               // binless moment shift (mean of M over the box)
+    int pad;
+};
+
+// ------------------------------------------------------------------ packed fp32 pairs
+// VF<2> maps onto the sm_100 FFMA2 / FADD2 / FMUL2 instructions (one issue slot for the
+// lane's two voxels); VF<1> is the scalar version of the same code.
+template <int XV> struct VF { float v[XV]; };
+
+template <int XV> __device__ __forceinline__ VF<XV> vsplat(float a) {
+    VF<XV> r;
+#pragma unroll
+    for (int i = 0; i < XV; ++i) r.v[i] = a;
+    return r;
+}
+template <int XV> __device__ __forceinline__ VF<XV> vfma(VF<XV> a, VF<XV> b, VF<XV> c) {
+    VF<XV> r;
+    if constexpr (XV == 2) {
+        const float2 t = __ffma2_rn(make_float2(a.v[0], a.v[1]), make_float2(b.v[0], b.v[1]), make_float2(c.v[0], c.v[1]));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        r.v[0] = fmaf(a.v[0], b.v[0], c.v[0]);
+    }
+    return r;
+}
+template <int XV> __device__ __forceinline__ VF<XV> vadd(VF<XV> a, VF<XV> b) {
+    VF<XV> r;
+    if constexpr (XV == 2) {
+        const float2 t = __fadd2_rn(make_float2(a.v[0], a.v[1]), make_float2(b.v[0], b.v[1]));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        r.v[0] = a.v[0] + b.v[0];
+    }
+    return r;
+}
+template <int XV> __device__ __forceinline__ VF<XV> vsub(VF<XV> a, VF<XV> b) {
+    VF<XV> r;
+    if constexpr (XV == 2) {
+        const float2 t = __fadd2_rn(make_float2(a.v[0], a.v[1]), make_float2(-b.v[0], -b.v[1]));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        r.v[0] = a.v[0] - b.v[0];
+    }
+    return r;
+}
+template <int XV> __device__ __forceinline__ VF<XV> vmul(VF<XV> a, VF<XV> b) {
+    VF<XV> r;
+    if constexpr (XV == 2) {
+        const float2 t = __fmul2_rn(make_float2(a.v[0], a.v[1]), make_float2(b.v[0], b.v[1]));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        r.v[0] = a.v[0] * b.v[0];
+    }
+    return r;
+}
+// a + t (b - a)
+template <int XV> __device__ __forceinline__ VF<XV> vlerp(VF<XV> a, VF<XV> b, VF<XV> t) {
+    return vfma(t, vsub(b, a), a);
+}
+
+// floor(u) as float and as int (|u| < 2^22), full-rate FADD.RM instead of FRND / F2I
+__device__ __forceinline__ float mfloor(float u, int &iu) {
+    const float m = __fadd_rd(u, MAGIC);
+    iu = __float_as_int(m) - MAGIC_I;
+    return m - MAGIC;
+}
+
+// shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
+struct P1Smem {
+    int lt, k, ct, pl, lm, lo, wx, wy, rm, zs, zc, zb, sh, ts, total;
+};
+__host__ __device__ inline P1Smem p1_smem(int W, int S) {
+    P1Smem o;
+    int off = 0;
+    auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
+    o.lt = take(W * S * 9 * 4);          // int   LT[W][S][9]
+    o.k = take(W * S * 32 * 4);          // float K[W][S][8 e][4 n]
+    o.ct = take(S * 128 * 4);            // float CT[S][4 m][8 e][4 n]
+    o.pl = take(W * 32 * 16);            // float4 PL[W][32]   layer node buffer
+    o.lm = take(W * 4 * 4 * 4);          // float LM[W][4 layers][4]
+    o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]  the row's line-list offsets
+    o.wx = take(64 * 16);                // float4 WX[XV * 32]  the lane voxels' spatial x weights (0: padding)
+    o.wy = take(W * 16);                 // float4 WY[W]
+    o.rm = take(W * 16);                 // uint4 RM[W]
+    o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
+    o.zc = take(FZMAX * 16);             // float4 ZC[z]  control z weights
+    o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
+    o.sh = take(S * 4);                  // float  SH[S]  per-slot shift
+    o.ts = take(160 * 4);                // int    TS[]   touched-slot list of a round
+    o.total = off;
+    return o;
+}
+
+struct FArgs {
+    Geo g;
+    Tables t;
+    const float *M;
+    const float *phi;               // fp32 [3][Gz][Gy][Gx]
+    const unsigned *rec;            // [slab voxels] slot << 24 | round(h_hi 2^23)
+    const unsigned *loff;           // [lines + 1] offsets of the per-line entry lists
+    const unsigned *lent;           // entries: slot | n_lo << 8 | n_hi << 16 (adds per entry)
+    const uint4 *rmask;             // [rows] the slots a row touches (bitmask, B <= 128)
+    const FItem *items;             // this rank's items (pass 1 and pass 2)
+    const ItemW *itemw;
+    const int *slotbins;
+    const int *iflag;               // per eval: 1 = no sample of the item can clamp
+    const float *shiftc;            // per-bin shift c_a of the binned first moment
+    unsigned long long *SQi;        // [R][B][2] int64, units 2^-16 (shifted, as SQ)
+    unsigned long long *Qi;         // [R] binless second moments, int64 units 2^-16
+    float4 *MG;                     // pass 1 out: (m, dM/dy) per slab voxel, m < 0 flags exact
+    int mgz0;
+    int S;                          // table stride in slots (max slots + binless + dummy)
+    int W;                          // warps per CTA
+    int i0;                         // first item of this launch
+    P1Smem L1;                      // pass-1 shared-memory layout (host-computed: p1_smem(W, S))
+    int ablate;                     // timing experiments only (SRWCR_ABLATE; wrong results): bit 0 no MG
+                                    // store, bit 1 no line-table atomics / fold, bit 2 no M gathers;
+                                    // (correct results) bit 3 no uniform-line path, bit 4 no dither
+};
+
+// ------------------------------------------------------------------ create-time builders
+// Per item (one CTA): the voxel records.  a0 = min(floor F, L-1), f = F - a0,
+// h_hi = h(1 - f) (Eq 5; parzen_pair as in the round-1 passes), stored as
+// round(h_hi 2^23) (|error| <= 2^-24) with the item-local slot of a0.
+__global__ void k_frec(const float *__restrict__ F, const FItem *items, const int *slotbins, Geo g, int mgz0,
+                       unsigned *rec) {
+    __shared__ unsigned char smap[256];
+    const FItem it = items[blockIdx.x];
+    for (int i = threadIdx.x; i < g.B; i += blockDim.x) smap[i] = 0xFF;
+    __syncthreads();
+    for (int s = threadIdx.x; s < it.nslots; s += blockDim.x) smap[slotbins[it.slot_off + s]] = (unsigned char)s;
+    __syncthreads();
+    const long long n = (long long)it.xlen * it.ylen * it.zlen;
+    for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+        const int x = it.x0 + (int)(i % it.xlen);
+        const long long t = i / it.xlen;
+        const int y = it.y0 + (int)(t % it.ylen), z = it.z0 + (int)(t / it.ylen);
+        const float Fv = F[(long long)z * g.nxy + (long long)y * g.nx + x];
+        const int a0 = min((int)Fv, g.L - 1);
+        float hlo, hhi;
+        parzen_pair_F(Fv - (float)a0, hlo, hhi);
+        const unsigned k = __float2uint_rn(hhi * 8388608.f);
+        rec[((long long)(z - mgz0) * g.ny + y) * g.nx + x] = ((unsigned)smap[a0] << 24) | k;
+    }
+}
+
+// One warp per line (item, row, slice): the touched slots of the line, ascending, with the
+// number of line-table adds each of their lo / hi entries receives (one per valid voxel of
+// the slot: the magic-number offsets the fold subtracts).  mode 0: count only (cnt[line]);
+// mode 1: write the entries at loff[line] and OR the slots into the row mask.
+template <int XV>
+__global__ void k_lists(const unsigned *__restrict__ rec, const FItem *items, int nitems, Geo g, int mgz0,
+                        const int *item_of_line, unsigned *cnt, const unsigned *loff, unsigned *lent,
+                        unsigned *rmask, long long nlines, int mode) {
+    const int lane = threadIdx.x & 31;
+    const long long line = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    if (line >= nlines) return;
+    const int ii = item_of_line[line];
+    const FItem it = items[ii];
+    const int rl = (int)((line - it.line_off) / it.zlen), zl = (int)((line - it.line_off) % it.zlen);
+    const int y = it.y0 + rl, z = it.z0 + zl;
+    int slot[2] = {-1, -1}, hz[2] = {0, 0};
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        if (lane + 32 * v < it.xlen) {
+            const unsigned r = rec[((long long)(z - mgz0) * g.ny + y) * g.nx + it.x0 + lane + 32 * v];
+            slot[v] = (int)(r >> 24);
+            hz[v] = (r & 0xFFFFFFu) != 0u;
+        }
+    }
+    // contributions: every valid voxel adds once to each of the 8 entries of its slot
+    int cs[2] = {-1, -1}, clo[2] = {0, 0}, chi[2] = {0, 0};
+#pragma unroll
+    for (int v = 0; v < XV; ++v)
+        if (slot[v] >= 0) { cs[v] = slot[v]; clo[v] = 1; chi[v] = 1; }
+    (void)hz;
+    unsigned n = 0, mask[4] = {0u, 0u, 0u, 0u};
+    const unsigned base = mode ? loff[line] : 0u;
+    for (;;) {
+        const int mine = min(cs[0] < 0 ? 1 << 30 : cs[0], cs[1] < 0 ? 1 << 30 : cs[1]);
+        const int s = (int)__reduce_min_sync(FULL, (unsigned)mine);
+        if (s == 1 << 30) break;
+        int nl = 0, nh = 0;
+#pragma unroll
+        for (int k = 0; k < 2; ++k)
+            if (cs[k] == s) { nl += clo[k]; nh += chi[k]; cs[k] = -1; }
+        nl = (int)__reduce_add_sync(FULL, (unsigned)nl);
+        nh = (int)__reduce_add_sync(FULL, (unsigned)nh);
+        if (mode && lane == 0) lent[base + n] = (unsigned)s | ((unsigned)nl << 8) | ((unsigned)nh << 16);
+        mask[s >> 5] |= 1u << (s & 31);
+        ++n;
+    }
+    if (lane == 0) {
+        if (mode == 0) cnt[line] = n;
+        else
+            for (int k = 0; k < 4; ++k)
+                if (mask[k]) atomicOr(rmask + 4LL * (it.row_off + rl) + k, mask[k]);
+    }
+}
+
+// ------------------------------------------------------------------ per-eval prep
+// Blocks [0, nconv): fp64 params -> fp32 phi (node layers [zlo, zhi)).  Blocks after: one
+// warp per item, the interior flag: with umax_c = max |phi_c| over the item's node box
+// (u_c is a convex combination of those values: B-spline weights >= 0, sum 1, P:51/Eq 8),
+// no sample of the item leaves [0, N-2] along any axis.
+__global__ void k_fprep(const double *__restrict__ p, float *__restrict__ phi, Geo g, int zlo, int zhi, int nconv,
+                        const FItem *items, int nitems, Tables t, int *iflag) {
+    if ((int)blockIdx.x < nconv) {
+        const long long plane = (long long)g.Gx * g.Gy;
+        const long long cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
+        for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)nconv * blockDim.x) {
+            const long long i = (long long)zlo * plane + j;
+            const long long gz = i / plane, xy = i - gz * plane;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                double v = 0.0;
+                if (c < g.ndim && gz < g.GzExt) v = p[(c * g.GzExt + gz) * plane + xy];
+                phi[c * cs + i] = (float)v;
+            }
+        }
+        return;
+    }
+    // one CTA per item
+    __shared__ float red[3][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ii = (int)blockIdx.x - nconv;
+    if (ii >= nitems) return;
+    const FItem it = items[ii];
+    const int lo[3] = {it.x0, it.y0, it.z0}, len[3] = {it.xlen, it.ylen, it.zlen};
+    int n0[3], nn[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        n0[ax] = t.cb[ax][lo[ax]];
+        nn[ax] = t.cb[ax][lo[ax] + len[ax] - 1] + 4 - n0[ax];
+    }
+    const long long plane = (long long)g.Gx * g.Gy, cs = plane * g.GzExt;
+    float um[3] = {0.f, 0.f, 0.f};
+    const int tot = nn[0] * nn[1] * nn[2];
+    for (int k = threadIdx.x; k < tot; k += blockDim.x) {
+        const int ix = k % nn[0], iy = (k / nn[0]) % nn[1], iz = k / (nn[0] * nn[1]);
+        const int gz = n0[2] + iz;
+        if (gz >= g.GzExt) continue;
+        const long long s = (long long)gz * plane + (long long)(n0[1] + iy) * g.Gx + n0[0] + ix;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+            if (c < g.ndim) um[c] = fmaxf(um[c], (float)fabs(p[c * cs + s]));
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float m = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(um[c])));
+        if (lane == 0) red[c][warp] = m;
+    }
+    __syncthreads();
+    if (warp != 0) return;
+    bool ok = true;
+    const int N[3] = {g.nx, g.ny, g.nz};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+        const float v = lane < (int)(blockDim.x >> 5) ? red[c][lane] : 0.f;
+        const float m = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(v)));
+        const float mm = m * 1.00001f + 1e-5f;
+        ok = ok && (lo[c] - (int)ceilf(mm) >= 0) && (lo[c] + len[c] - 1 + (int)floorf(mm) <= N[c] - 2);
+    }
+    if (lane == 0) iflag[ii] = ok ? 1 : 0;
+}
+
+// int64 statistics (units 2^-16) -> fp64 SQ / Q (exact below 2^53 units), zeroing the int64
+// buffer for the next evaluation
+__global__ void k_stats_convert(unsigned long long *__restrict__ si, double *__restrict__ sd, long long n) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const long long v = (long long)si[i];
+        sd[i] = (double)v * (1.0 / STAT_UNIT);
+        si[i] = 0ull;
+    }
+}
+
+__device__ __forceinline__ void atomic_add_i64(unsigned long long *p, double v) {
+    atomicAdd(p, (unsigned long long)__double2ll_rn(v * STAT_UNIT));
+}
+
+// ------------------------------------------------------------------ pass 1 (fast)
+// Per voxel: FFD displacement from the 4 register layers (a3), split
+// sample coordinates and 8 gathers (a4, reading c1-c3, H11), Parzen moments g1, g2 of m
+// (a5), and the moment accumulation (a6):
+//   binned:  S_ra  += w_r h_a(F) (g1 - c_a0)    a in {a0, a0+1}: 2 channels (lo, hi) x 4 x-taps
+//            -> int32 line table LT[slot][tap][ch] (ATOMS), folded per line with the 4 z-taps
+//               into the warp's column table K, per round of rows with the 4 y-taps into the
+//               CTA cell table CT (fixed order), per item into int64 global SQi;
+//   binless: Q_r   += w_r ((g1 - cI)^2 + w1 (1 - w1))  and  w_r (g1 - cI): per-lane register
+//            accumulators over the z-march (4 z-taps x 2 channels), warp-reduced per row into
+//            the binless pseudo-slot of K.
+// The warp marches z through one row of its item; rows are dealt to warps in rounds.
+template <int XV, bool INT>
+struct P1Lane {
+    // per-lane constants of the item
+    int xv[XV], relx[XV];
+    bool valid[XV];
+    VF<XV> wr[4];        // rotated spatial x weights: entry k holds tap (k + q) & 3, q = lane & 3
+    unsigned lts[4];     // shared address of the rotated tap-k entry pair of slot 0 in the warp's line table
+};
+
+// shared-memory reductions on 32-bit shared addresses (no generic -> shared conversion in the loop)
+__device__ __forceinline__ void red_s32(unsigned addr, int v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void red_s32_pair(unsigned addr, int v0, int v1) {
+    asm volatile("red.shared.add.u32 [%0], %1;\n\tred.shared.add.u32 [%0+4], %2;" ::"r"(addr), "r"(v0), "r"(v1)
+                 : "memory");
+}
+__device__ __forceinline__ void red_shared(int *p, int v) {
+    red_s32((unsigned)__cvta_generic_to_shared(p), v);
+}
+template <int XV> __device__ __forceinline__ VF<XV> vfloor_rd(VF<XV> u) {   // u + MAGIC rounded down
+    VF<XV> r;
+    if constexpr (XV == 2) {
+        const float2 t = __fadd2_rd(make_float2(u.v[0], u.v[1]), make_float2(MAGIC, MAGIC));
+        r.v[0] = t.x; r.v[1] = t.y;
+    } else {
+        r.v[0] = __fadd_rd(u.v[0], MAGIC);
+    }
+    return r;
+}
+
+template <int XV, bool INT>
+__device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1Smem &L, unsigned char *smem, int y,
+                                       int warp, int lane, const P1Lane<XV, INT> &pl) {
+    const Geo &g = a.g;
+    const int S = a.S, ns = it.nslots, dummy = it.nslots + 1;
+    int *LTw = reinterpret_cast<int *>(smem + L.lt) + warp * S * 9;
+    float *Kw = reinterpret_cast<float *>(smem + L.k) + warp * S * 32;
+    float4 *PLw = reinterpret_cast<float4 *>(smem + L.pl) + warp * 32;
+    float *LMw = reinterpret_cast<float *>(smem + L.lm) + warp * 16;
+    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);
+    const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
+    const float4 *ZC = reinterpret_cast<const float4 *>(smem + L.zc);
+    const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
+    const float *SH = reinterpret_cast<const float *>(smem + L.sh);
+
+    const int r = y - it.y0;
+    const int cby = a.t.cb[1][y];
+    const float4 cwy = a.t.cw[1][y];
+    const int xn0 = a.t.cb[0][it.x0];
+    const int nxn = a.t.cb[0][it.x0 + it.xlen - 1] + 4 - xn0;
+    const int z0 = it.z0, zlen = it.zlen;
+    const long long line0 = (long long)it.line_off + (long long)r * zlen;
+    // the row's line-list offsets, staged once per row
+    for (int k = lane; k <= zlen; k += 32) LOw[k] = __ldg(a.loff + line0 + k);
+
+    // ---- FFD layers (a3): U[n][c] = sum_{l,m} cwx_l cwy_m phi[c][gz_n][cby+m][cbx+l]
+    VF<XV> U[4][3];
+    const int Gx = g.Gx, plane = g.Gx * g.Gy, cs = plane * g.Gz;
+    const int pbase = cby * Gx + xn0 + lane;
+    auto load_layer = [&](int gz, VF<XV>(&Un)[3], int slotn) {
+        float p0 = 0.f, p1 = 0.f, p2 = 0.f, mx = 0.f;
+        if (lane < nxn) {
+            const float *q = a.phi + (gz * plane + pbase);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const float w = f4(cwy, m);
+                const float f0 = __ldg(q + m * Gx), f1 = __ldg(q + (cs + m * Gx)), f2 = __ldg(q + (2 * cs + m * Gx));
+                p0 = fmaf(w, f0, p0);
+                p1 = fmaf(w, f1, p1);
+                p2 = fmaf(w, f2, p2);
+                mx = fmaxf(mx, fmaxf(fabsf(f0), fmaxf(fabsf(f1), fabsf(f2))));
+            }
+            PLw[lane] = make_float4(p0, p1, p2, 0.f);
+        }
+        mx = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(mx)));
+        if (lane == 0) LMw[slotn] = mx;
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Un[c] = vsplat<XV>(0.f);
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            VF<XV> w, q0, q1, q2;
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                const float4 P = PLw[pl.relx[v] + l];
+                w.v[v] = __ldg(reinterpret_cast<const float *>(a.t.cw[0] + pl.xv[v]) + l);
+                q0.v[v] = P.x;
+                q1.v[v] = P.y;
+                q2.v[v] = P.z;
+            }
+            Un[0] = vfma(w, q0, Un[0]);
+            Un[1] = vfma(w, q1, Un[1]);
+            Un[2] = vfma(w, q2, Un[2]);
+        }
+        __syncwarp();
+    };
+    int gzl = ZB[0];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) load_layer(gzl + n, U[n], (gzl + n) & 3);
+    // rounding bound of u (any component): |u32 - u64| <= gamma_16 max_taps |phi| ~ 9.5e-7 max|phi|
+    // (16 roundings on any path: fp32 phi and 3 weights, 3 x 4 fma levels; weights >= 0 sum to 1);
+    // 2e-6 of the max over the line's 4 active layers (all x-nodes of the item, 4 y-taps, 3 comps)
+    float tol = 2e-6f * fmaxf(fmaxf(LMw[0], LMw[1]), fmaxf(LMw[2], LMw[3]));
+
+    // ---- binless accumulators (per lane, over the z-march): 4 z-taps x {q', g1 - cI}
+    VF<XV> accq[4], acca[4];
+#pragma unroll
+    for (int n = 0; n < 4; ++n) { accq[n] = vsplat<XV>(0.f); acca[n] = vsplat<XV>(0.f); }
+
+    // per-lane row base index (slab-linear; slices add nxy)
+    const int vb = ((z0 - a.mgz0) * g.ny + y) * g.nx + pl.xv[0];
+    const int nxy = g.nxy32, nx = g.nx, dzo = g.dzo;
+
+    // ---- software pipeline: the records, gathers and coordinate flags of slice z+1 are in
+    // flight while slice z is processed
+    unsigned recn[XV];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) recn[v] = __ldg(a.rec + (vb + 32 * v));
+    float C[XV][8];
+    VF<XV> T[3];
+    int fl[XV];   // bit 0-2: clamped x, y, z (reading c2); bit 3: near an integer (exact path); bit 4: at rest
+    const VF<XV> vone = vsplat<XV>(1.f), vmagic = vsplat<XV>(MAGIC);
+    auto gather = [&](int zz) {
+        const float4 cw = ZC[zz - z0];
+        VF<XV> u[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            VF<XV> s = vmul(vsplat<XV>(cw.x), U[0][c]);
+            s = vfma(vsplat<XV>(cw.y), U[1][c], s);
+            s = vfma(vsplat<XV>(cw.z), U[2][c], s);
+            u[c] = vfma(vsplat<XV>(cw.w), U[3][c], s);
+        }
+        // split coordinates (H11): cell = i + floor(u) as an integer, t = u - floor(u) exact
+        VF<XV> mf[3], om[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            mf[c] = vfloor_rd(u[c]);
+            T[c] = vsub(u[c], vsub(mf[c], vmagic));
+            om[c] = vsub(vone, T[c]);
+        }
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            int ci[3];
+            ci[0] = __float_as_int(mf[0].v[v]) - MAGIC_I + pl.xv[v];
+            ci[1] = __float_as_int(mf[1].v[v]) - MAGIC_I + y;
+            ci[2] = __float_as_int(mf[2].v[v]) - MAGIC_I + zz;
+            // near an integer (a cell / clamp boundary: the derivative of the interpolant jumps)
+            // unless u is exactly 0 (tap window at rest: identical in fp32 and fp64)
+            const float emin = fminf(fminf(fminf(T[0].v[v], om[0].v[v]), fminf(T[1].v[v], om[1].v[v])),
+                                     fminf(T[2].v[v], om[2].v[v]));
+            const float umax = fmaxf(fmaxf(fabsf(u[0].v[v]), fabsf(u[1].v[v])), fabsf(u[2].v[v]));
+            const bool rest = umax == 0.f;
+            int f = (emin < tol && !rest ? 8 : 0) | (rest ? 16 : 0);
+            if (!INT) {   // reading c2: clamp to [0, N-1], cell = min(floor y, N-2)
+                const int nm2[3] = {g.nxm2, g.nym2, g.nzm2};
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    const bool lo = ci[c] < 0, hi = ci[c] > nm2[c];
+                    const float tt = T[c].v[v];
+                    T[c].v[v] = lo ? 0.f : (hi ? 1.f : tt);
+                    f |= (lo || (hi && !(ci[c] == nm2[c] + 1 && tt == 0.f))) ? (1 << c) : 0;
+                    ci[c] = min(max(ci[c], 0), nm2[c]);
+                }
+            }
+            fl[v] = f;
+            const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[2] * nxy + ci[1] * nx + ci[0];
+            const float *b0 = a.M + o0, *b1 = a.M + (o0 + nx), *b2 = a.M + (o0 + dzo), *b3 = a.M + (o0 + dzo + nx);
+            C[v][0] = __ldg(b0); C[v][1] = __ldg(b0 + 1);
+            C[v][2] = __ldg(b1); C[v][3] = __ldg(b1 + 1);
+            C[v][4] = __ldg(b2); C[v][5] = __ldg(b2 + 1);
+            C[v][6] = __ldg(b3); C[v][7] = __ldg(b3 + 1);
+        }
+    };
+    gather(z0);
+    // first list entries of the next line, prefetched one slice ahead (lane's passes 0, 1)
+    __syncwarp();
+    // the next line's list entries, one per lane (a line touches <= 32 slots but rarely)
+    unsigned entn;
+    {
+        const unsigned o = LOw[0], o1 = LOw[1];
+        entn = o + lane < o1 ? __ldg(a.lent + o + lane) : 0u;
+    }
+    const float cI = it.cI;
+    const float Lm1 = (float)(g.L - 1);
+    const unsigned kw_s = (unsigned)__cvta_generic_to_shared(Kw), lt_s = (unsigned)__cvta_generic_to_shared(LTw);
+
+    for (int iz = 0; iz < zlen; ++iz) {
+        const int izn = min(iz + 1, zlen - 1);   // the last slice re-issues its own loads (no branch)
+        // ---- this slice's inputs
+        unsigned rc[XV];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            rc[v] = recn[v];
+            recn[v] = __ldg(a.rec + (vb + izn * nxy + 32 * v));
+        }
+        VF<XV> c000, c100, c010, c110, c001, c101, c011, c111;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            c000.v[v] = C[v][0]; c100.v[v] = C[v][1]; c010.v[v] = C[v][2]; c110.v[v] = C[v][3];
+            c001.v[v] = C[v][4]; c101.v[v] = C[v][5]; c011.v[v] = C[v][6]; c111.v[v] = C[v][7];
+        }
+        const VF<XV> tx = T[0], ty = T[1], tz = T[2];
+        int flc[XV];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) flc[v] = fl[v];
+        // ---- trilinear value and gradient (a4, nested lerps; readings c1, c3)
+        const VF<XV> d00 = vsub(c100, c000), d10 = vsub(c110, c010), d01 = vsub(c101, c001), d11 = vsub(c111, c011);
+        const VF<XV> e00 = vfma(tx, d00, c000), e10 = vfma(tx, d10, c010);
+        const VF<XV> e01 = vfma(tx, d01, c001), e11 = vfma(tx, d11, c011);
+        const VF<XV> f0 = vlerp(e00, e10, ty), f1 = vlerp(e01, e11, ty);
+        const VF<XV> m = vlerp(f0, f1, tz);
+        VF<XV> dgx = vlerp(vlerp(d00, d10, ty), vlerp(d01, d11, ty), tz);
+        VF<XV> dgy = vlerp(vsub(e10, e00), vsub(e11, e01), tz);
+        VF<XV> dgz = vsub(f1, f0);
+        // ---- Parzen moments of m (a5, Eq 5): n = min(floor m, L-1), f = m - n
+        const VF<XV> mfm = vfloor_rd(m);
+        VF<XV> nf;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) nf.v[v] = fminf(mfm.v[v] - MAGIC, Lm1);
+        const VF<XV> fm = vsub(m, nf);
+        const VF<XV> omf = vsub(vone, fm);
+        VF<XV> sfold;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) sfold.v[v] = fm.v[v] < 0.5f ? fm.v[v] : omf.v[v];
+        const VF<XV> wq = vmul(sfold, vfma(vsplat<XV>(1.8f), sfold, vsplat<XV>(0.1f)));   // s (0.1 + 1.8 s)
+        const VF<XV> owq = vsub(vone, wq);
+        VF<XV> w1, w1l;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            const bool lowh = fm.v[v] < 0.5f;
+            w1.v[v] = lowh ? wq.v[v] : owq.v[v];
+            w1l.v[v] = lowh ? owq.v[v] : wq.v[v];
+        }
+        // (g1 itself is never formed: n + w1 in fp32 would round w1 to the ulp of n; the shifted
+        // moments are (n - c) + w1 with the small difference first)
+        // ---- (m, dM/dy) for pass 2; the exact fp64 path where the derivative jumps: a
+        // coordinate within rounding of an integer (cell / clamp boundary) or m at the Parzen
+        // kink (reading c4) of a non-flat cell whose tap window is not at rest
+        int ex[XV];   // 1: decided in fp64 by k_exact_fix
+        int kink[XV], anyk = 0;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            ex[v] = (flc[v] >> 3) & 1;
+            kink[v] = (int)(fminf(fm.v[v], omf.v[v]) < 5e-5f) & (int)((flc[v] & 24) == 0);
+            anyk |= kink[v];
+        }
+        if (__any_sync(FULL, anyk)) {   // rare: the flatness test (8 equal corners: m exact)
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                const float c0 = C[v][0];
+                const int flat = (int)(C[v][1] == c0) & (int)(C[v][2] == c0) & (int)(C[v][3] == c0) &
+                                 (int)(C[v][4] == c0) & (int)(C[v][5] == c0) & (int)(C[v][6] == c0) & (int)(C[v][7] == c0);
+                ex[v] |= kink[v] & (flat ^ 1);
+            }
+        }
+        // ---- next slice: slide the layer window, issue its gathers (the last slice re-issues);
+        // slice z's corners are dead from here on: the loads of z+1 overlap the rest of slice z
+        {
+            const int bz1 = ZB[izn];
+            if (gzl < bz1) {
+                while (gzl < bz1) {
+#pragma unroll
+                    for (int n = 0; n < 3; ++n)
+#pragma unroll
+                        for (int c = 0; c < 3; ++c) U[n][c] = U[n + 1][c];
+                    ++gzl;
+                    load_layer(gzl + 3, U[3], (gzl + 3) & 3);
+                }
+                tol = 2e-6f * fmaxf(fmaxf(LMw[0], LMw[1]), fmaxf(LMw[2], LMw[3]));
+            }
+            gather(z0 + izn);
+        }
+        // ---- record: slot and Parzen weights of F (static); the shifted first moment A
+        int slot[XV];
+        VF<XV> hhi, A;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            slot[v] = pl.valid[v] ? (int)(rc[v] >> 24) : dummy;
+            hhi.v[v] = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu));
+            A.v[v] = SH[slot[v]];
+        }
+        hhi = vsub(hhi, vone);
+        A = vadd(vsub(nf, A), w1);                                // g1 - c_a0 = (n - c_a0) + w1
+        // line fixed-point scale from the line's max |A|: one add (w <= 2/3) stays below 2^22
+        // (exact magic-number conversion), a line entry's sum below 2^28
+        float am = fabsf(A.v[0]);
+#pragma unroll
+        for (int v = 1; v < XV; ++v) am = fmaxf(am, fabsf(A.v[v]));
+        const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(am)) >> 23);
+        const int ksc = min(148 - EA, 126);
+        const float lsc = __int_as_float((ksc + 127) << 23), lisc = __int_as_float((127 - ksc) << 23);
+        if (!INT) {
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                dgx.v[v] = (flc[v] & 1) ? 0.f : dgx.v[v];
+                dgy.v[v] = (flc[v] & 2) ? 0.f : dgy.v[v];
+                dgz.v[v] = (flc[v] & 4) ? 0.f : dgz.v[v];
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < XV; ++v)   // (a padding lane samples its clamped neighbour: identical values)
+            if (!(a.ablate & 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
+                       make_float4(ex[v] ? -1.0f - m.v[v] : m.v[v], dgx.v[v], dgy.v[v], dgz.v[v]));
+        // ---- binless (z-taps folded in registers)
+        {
+            const float4 wz = ZS[iz];
+            const VF<XV> Ab = vadd(vsub(nf, vsplat<XV>(cI)), w1);   // g1 - cI
+            const VF<XV> qv = vfma(Ab, Ab, vmul(w1, w1l));       // sum_b (b - cI)^2 h(b - m)
+            accq[0] = vfma(vsplat<XV>(wz.x), qv, accq[0]);
+            accq[1] = vfma(vsplat<XV>(wz.y), qv, accq[1]);
+            accq[2] = vfma(vsplat<XV>(wz.z), qv, accq[2]);
+            accq[3] = vfma(vsplat<XV>(wz.w), qv, accq[3]);
+            acca[0] = vfma(vsplat<XV>(wz.x), Ab, acca[0]);
+            acca[1] = vfma(vsplat<XV>(wz.y), Ab, acca[1]);
+            acca[2] = vfma(vsplat<XV>(wz.z), Ab, acca[2]);
+            acca[3] = vfma(vsplat<XV>(wz.w), Ab, acca[3]);
+        }
+        // ---- binned: int32 line table (magic-number fixed point at the line scale lsc; the
+        // fold subtracts the per-entry offset count); every voxel adds its 8 values.  A line whose
+        // voxels all share one slot (static list count 1) reduces across the warp instead
+        // (REDUX: a 32-lane same-address atomic serialises), and its lane 0 adds the 8 totals.
+        const unsigned lo_o = LOw[iz], lo_o1 = LOw[iz + 1];
+        const bool uni = lo_o1 - lo_o == 1u && !(a.ablate & 8);
+        if (!(a.ablate & 2)) {
+            const VF<XV> As = vmul(A, vsplat<XV>(lsc));
+            const VF<XV> hiv = vmul(hhi, As), lov = vsub(As, hiv);   // h_hi A, h_lo A (scaled)
+            // deterministic dither in (-1/2, 1/2) before the round to integer: identical values
+            // (flat regions) would otherwise round alike in every voxel and bias the sums; with
+            // the dither the rounding is unbiased (R2 low-discrepancy sequence over lane, slice, row)
+            VF<XV> dith;
+            {
+                const float h = fmaf((float)lane, 0.7548776662f, fmaf((float)iz, 0.5698402910f, (float)y * 0.41421356f));
+                const float d0 = (a.ablate & 16) ? 0.f : h - floorf(h) - 0.5f;
+                dith.v[0] = d0;
+                if (XV == 2) dith.v[XV - 1] = (a.ablate & 16) ? 0.f : (d0 < 0.f ? d0 + 0.5f : d0 - 0.5f);
+            }
+            if (uni) {
+                const float4 *WXw = reinterpret_cast<const float4 *>(smem + L.wx);
+                int tot[8];
+#pragma unroll
+                for (int l = 0; l < 4; ++l) {
+                    tot[2 * l] = 0;
+                    tot[2 * l + 1] = 0;
+                }
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    const float4 w = WXw[v * 32 + lane];   // unrotated spatial x weights (0: padding)
+#pragma unroll
+                    for (int l = 0; l < 4; ++l) {
+                        tot[2 * l] += __float_as_int(fmaf(lov.v[v], f4(w, l), dith.v[v]) + MAGIC);
+                        tot[2 * l + 1] += __float_as_int(fmaf(hiv.v[v], f4(w, l), dith.v[v]) + MAGIC);
+                    }
+                }
+                int red8[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) red8[e] = (int)__reduce_add_sync(FULL, (unsigned)tot[e]);
+                if (lane == 0) {
+                    // padding voxels added a bare offset each: the list counts valid voxels only
+                    const int pad = (32 * XV - it.xlen) * MAGIC_I;
+                    const unsigned row = lt_s + (unsigned)slot[0] * 36u;
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) red_s32(row + 4u * e, red8[e] - pad);
+                }
+            } else {
+                // lanes 4-7 (mod 8) add the hi entry first: with the tap rotation by lane & 3, 8
+                // neighbouring lanes of one slot hit 8 distinct entries in each instruction
+                const bool chA = (lane >> 2) & 1;
+                VF<XV> va, vb;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    va.v[v] = chA ? hiv.v[v] : lov.v[v];
+                    vb.v[v] = chA ? lov.v[v] : hiv.v[v];
+                }
+                const int db = chA ? -4 : 4;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const VF<XV> xa = vadd(vfma(va, pl.wr[k], dith), vmagic), xb = vadd(vfma(vb, pl.wr[k], dith), vmagic);
+#pragma unroll
+                    for (int v = 0; v < XV; ++v) {
+                        const unsigned ad = pl.lts[k] + (unsigned)slot[v] * 36u;
+                        red_s32(ad, __float_as_int(xa.v[v]));
+                        red_s32(ad + db, __float_as_int(xb.v[v]));
+                    }
+                }
+            }
+        }
+        // ---- fold the line into the column table K (touched entries only, from the static list)
+        __syncwarp();
+        if (!(a.ablate & 2)) {
+            const unsigned o = LOw[iz], o1 = LOw[iz + 1], o2 = LOw[iz + 2 <= zlen ? iz + 2 : zlen];
+            const int cnt = (int)(o1 - o);
+            const unsigned ecur = entn;
+            entn = o1 + lane < o2 ? __ldg(a.lent + o1 + lane) : 0u;   // the next line's entries
+            const float4 wz = ZS[iz];
+            const float2 wzs01 = make_float2(wz.x * lisc, wz.y * lisc), wzs23 = make_float2(wz.z * lisc, wz.w * lisc);
+            const int e = lane & 7;
+            const int nsh = (e & 1) ? 16 : 8;
+            for (int p = 0; 4 * p < cnt; ++p) {
+                const int j = 4 * p + (lane >> 3);
+                unsigned ent = __shfl_sync(FULL, ecur, j & 31);
+                if (j >= 32) ent = j < cnt ? __ldg(a.lent + o + j) : 0u;   // > 32 slots in one line
+                if (j < cnt) {
+                    const int s = (int)(ent & 0xFFu);
+                    const int nadd = (int)((ent >> nsh) & 0xFFu);
+                    const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
+                    int raw;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
+                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(0) : "memory");
+                    const float val = (float)(raw - nadd * MAGIC_I);
+                    const unsigned ka = kw_s + (unsigned)(s * 128 + e * 16);
+                    float4 k4;
+                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(k4.x), "=f"(k4.y), "=f"(k4.z), "=f"(k4.w) : "r"(ka));
+                    const float2 vv = make_float2(val, val);
+                    const float2 r01 = __ffma2_rn(wzs01, vv, make_float2(k4.x, k4.y));
+                    const float2 r23 = __ffma2_rn(wzs23, vv, make_float2(k4.z, k4.w));
+                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(ka), "f"(r01.x), "f"(r01.y), "f"(r23.x), "f"(r23.y) : "memory");
+                }
+            }
+        }
+        __syncwarp();
+    }
+    // ---- row end: binless -> K[ns]; lane j of the reduction holds value j = (l, ch, n)
+    {
+        float vals[32];
+        const int q4 = lane & 3;
+        // un-rotate the x weights: true tap l is rotated index (l - q) & 3
+#pragma unroll
+        for (int l = 0; l < 4; ++l) {
+            const int k = (l - q4) & 3;
+            VF<XV> wl;
+#pragma unroll
+            for (int v = 0; v < XV; ++v)
+                wl.v[v] = k == 0 ? pl.wr[0].v[v] : k == 1 ? pl.wr[1].v[v] : k == 2 ? pl.wr[2].v[v] : pl.wr[3].v[v];
+#pragma unroll
+            for (int n = 0; n < 4; ++n) {
+                float sq = 0.f, sa = 0.f;
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    sq = fmaf(wl.v[v], accq[n].v[v], sq);
+                    sa = fmaf(wl.v[v], acca[n].v[v], sa);
+                }
+                vals[(l * 2 + 0) * 4 + n] = sq;
+                vals[(l * 2 + 1) * 4 + n] = sa;
+            }
+        }
+        // recursive halving: after the step with mask h each lane keeps the half its lane bit selects
+#pragma unroll
+        for (int h = 16; h >= 1; h >>= 1) {
+            const bool up = (lane & h) != 0;
+#pragma unroll
+            for (int i = 0; i < h; ++i) {
+                const float send = up ? vals[i] : vals[i + h];
+                const float keep = up ? vals[i + h] : vals[i];
+                vals[i] = keep + __shfl_xor_sync(FULL, send, h);
+            }
+        }
+        Kw[ns * 32 + lane] = vals[0];   // lane = (l * 2 + ch) * 4 + n
+    }
+}
+
+template <int XV, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int W = a.W, S = a.S;
+    const P1Smem &L = a.L1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ii = a.i0 + blockIdx.x;
+    const FItem it = a.items[ii];
+    const Geo &g = a.g;
+    const int ns = it.nslots;
+    int *LT = reinterpret_cast<int *>(smem + L.lt);
+    float *K = reinterpret_cast<float *>(smem + L.k);
+    float *CT = reinterpret_cast<float *>(smem + L.ct);
+    float4 *WY = reinterpret_cast<float4 *>(smem + L.wy);
+    uint4 *RM = reinterpret_cast<uint4 *>(smem + L.rm);
+    float4 *ZS = reinterpret_cast<float4 *>(smem + L.zs);
+    float4 *ZC = reinterpret_cast<float4 *>(smem + L.zc);
+    int *ZB = reinterpret_cast<int *>(smem + L.zb);
+    float *SH = reinterpret_cast<float *>(smem + L.sh);
+    int *TS = reinterpret_cast<int *>(smem + L.ts);
+
+    for (int i = threadIdx.x; i < W * S * 9; i += blockDim.x) LT[i] = 0;
+    for (int i = threadIdx.x; i < W * S * 32; i += blockDim.x) K[i] = 0.f;
+    for (int i = threadIdx.x; i < (ns + 1) * 128; i += blockDim.x) CT[i] = 0.f;
+    for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {
+        ZS[i] = a.t.sw[2][it.z0 + i];
+        ZC[i] = a.t.cw[2][it.z0 + i];
+        ZB[i] = a.t.cb[2][it.z0 + i];
+    }
+    for (int s = threadIdx.x; s < S; s += blockDim.x) SH[s] = s < ns ? a.shiftc[a.slotbins[it.slot_off + s]] : 0.f;
+    for (int i = threadIdx.x; i < 32 * XV; i += blockDim.x)
+        reinterpret_cast<float4 *>(smem + L.wx)[i] = i < it.xlen ? a.t.sw[0][it.x0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+
+    // per-lane constants
+    const int q4 = lane & 3;
+    const int xn0 = a.t.cb[0][it.x0];
+    const bool interior = a.iflag[ii] != 0;
+    // the two template variants share the lane setup
+    auto setup = [&](auto &pl) {
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            pl.valid[v] = lane + 32 * v < it.xlen;
+            pl.xv[v] = pl.valid[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+            pl.relx[v] = a.t.cb[0][pl.xv[v]] - xn0;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int l = (k + q4) & 3;
+#pragma unroll
+            for (int v = 0; v < XV; ++v) pl.wr[k].v[v] = pl.valid[v] ? f4(a.t.sw[0][pl.xv[v]], l) : 0.f;
+            pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * 9) + 8u * (unsigned)l + 4u * ((lane >> 2) & 1);
+        }
+    };
+    __syncthreads();
+
+    const int rounds = (it.ylen + W - 1) / W;
+    for (int rd = 0; rd < rounds; ++rd) {
+        const int y = it.y0 + rd * W + warp;
+        const bool active = y < it.y0 + it.ylen;
+        if (lane == 0) {
+            WY[warp] = active ? a.t.sw[1][y] : make_float4(0.f, 0.f, 0.f, 0.f);
+            RM[warp] = active ? a.rmask[it.row_off + (y - it.y0)] : make_uint4(0u, 0u, 0u, 0u);
+        }
+        if (active) {
+            if (interior) {
+                P1Lane<XV, true> pl;
+                setup(pl);
+                p1_row<XV, true>(a, it, L, smem, y, warp, lane, pl);
+            } else {
+                P1Lane<XV, false> pl;
+                setup(pl);
+                p1_row<XV, false>(a, it, L, smem, y, warp, lane, pl);
+            }
+        }
+        __syncthreads();
+        // ---- round fold: CT[s][m][j] += sum_w WY[w].m K[w][s][j] (fixed warp order), over
+        // the slots the round's rows touched plus the binless pseudo-slot
+        if (threadIdx.x < 32) {
+            unsigned u[4] = {0u, 0u, 0u, 0u};
+            for (int w = 0; w < W; ++w) {
+                const uint4 rm = RM[w];
+                u[0] |= rm.x; u[1] |= rm.y; u[2] |= rm.z; u[3] |= rm.w;
+            }
+            // lane k handles bits [4k, 4k+4) of the 128-bit mask
+            int pos = 0;
+            const int word = lane >> 3, sh = (lane & 7) * 4;
+            for (int k = 0; k < 4; ++k)
+                if (k < word) pos += __popc(u[k]);
+            pos += __popc(u[word] & ((1u << sh) - 1u));
+            const unsigned bits = (u[word] >> sh) & 0xFu;
+            int pp = pos;
+            for (int b = 0; b < 4; ++b)
+                if (bits & (1u << b)) TS[pp++] = lane * 4 + b;
+            const int tot = __popc(u[0]) + __popc(u[1]) + __popc(u[2]) + __popc(u[3]);
+            if (lane == 0) { TS[tot] = ns; TS[159] = tot + 1; }
+        }
+        __syncthreads();
+        const int nts = TS[159];
+        for (int pidx = threadIdx.x; pidx < nts * 32; pidx += blockDim.x) {
+            const int s = TS[pidx >> 5], j = pidx & 31;
+            float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
+            for (int w = 0; w < W; ++w) {
+                float *kp = K + (w * S + s) * 32 + j;
+                const float kv = *kp;
+                *kp = 0.f;
+                const float4 wy = WY[w];
+                acc0 = fmaf(wy.x, kv, acc0);
+                acc1 = fmaf(wy.y, kv, acc1);
+                acc2 = fmaf(wy.z, kv, acc2);
+                acc3 = fmaf(wy.w, kv, acc3);
+            }
+            float *ct = CT + s * 128 + j;
+            ct[0] += acc0;
+            ct[32] += acc1;
+            ct[64] += acc2;
+            ct[96] += acc3;
+        }
+        __syncthreads();
+    }
+    // ---- item flush: CT[s][m][(l ch) n] -> int64 global (units 2^-16).  Binned slots: SQi of
+    // region (cz + n, cy + m, cx + l), bin slotbins[s], channel ch.  Binless slot ns:
+    // Q_r += Q' + 2 cI S' + cI^2 N (unshift; N = the item's spatial weight sums).
+    const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
+    const int B = g.B;
+    for (int t = threadIdx.x; t < ns * 128; t += blockDim.x) {
+        const float val = CT[t];
+        if (val == 0.f) continue;
+        const int s = t >> 7, mm = (t >> 5) & 3, e = (t >> 2) & 7, n = t & 3;
+        const int l = e >> 1, ch = e & 1;
+        const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        atomic_add_i64(a.SQi + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
+    }
+    if (threadIdx.x < 64) {
+        const int l = threadIdx.x >> 4, mm = (threadIdx.x >> 2) & 3, n = threadIdx.x & 3;
+        const double Qp = CT[ns * 128 + mm * 32 + (l * 2 + 0) * 4 + n];
+        const double Sp = CT[ns * 128 + mm * 32 + (l * 2 + 1) * 4 + n];
+        const ItemW &iw = a.itemw[ii];
+        const double N = iw.sx[l] * iw.sy[mm] * iw.sz[n];
+        if (N > 0.0) {
+            const double c = it.cI;
+            const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+            atomic_add_i64(a.Qi + r, Qp + 2.0 * c * Sp + c * c * N);
+        }
+    }
+}
+
+}  // namespace srwcr
+
+namespace srwcr {
+
+// ------------------------------------------------------------------ pass 2 (fast)
+// Per voxel: (m, dM/dy) from pass 1 (MG; m < 0 flags the voxels the
+// fp64 definition must decide, deferred to k_exact_fix), the record of F (slot, h_hi), and
+//   Z dD/dm = g1' [c2 A~ - 2 G~ + 2 B~]      (Eq 27 after the b-sum)
+//   A~ = sum_r w_r alpha_r, B~ = sum_r w_r beta_r, G~ = sum_r w_r (h_lo gamma_{r,a0} + h_hi gamma_{r,a0+1})
+// with the region tables contracted over the row's y-taps once per row (GY: the slots the
+// row touches), over the line's z-taps once per line (GZ: the slots the line touches, from
+// the static list; alpha / beta in pseudo-slot ns), so a voxel reads 4 float4 and dots them
+// with its spatial x weights.  Then the adjoint of the FFD (Eq 15-17):
+//   Z dD/dphi_{s,c} += (Z dD/dm) dM/dy_c cwx_l cwy_m cwz_n
+// accumulated in registers over the z-march (4 active control layers), x-contracted across
+// lanes into the warp row buffer (int32 fixed point, per-warp exponent) when a layer retires,
+// y-contracted into the CTA node window (exact int32 (hi, lo) pairs in units 2^-k, k from the
+// combine's bound), flushed once per item into the int64 global gradient: deterministic.
+struct P2Smem {
+    int gam, ab, gy, gz, rb, nph, npl, lo, zc, zb, zs, cx, total;
+};
+__host__ __device__ inline P2Smem p2_smem(int W, int S, int npn) {
+    P2Smem o;
+    int off = 0;
+    auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
+    o.gam = take(S * 2 * 64 * 4);        // float  GAM[S][2][64]    gamma of the item's regions, bins a0, a0+1
+    o.ab = take(2 * 64 * 4);             // float  AB[2][64]        alpha, beta of the item's regions
+    o.gy = take(W * S * 8 * 16);         // float4 GY[W][S][2][4 l] (over n), y-contracted per row
+    o.gz = take(W * 2 * S * 2 * 16);     // float4 GZ[W][2][S][2]   (over l), z-contracted per line (2 buffers)
+    o.rb = take(W * 3 * 32 * 4);         // int    RB[W][3][32]     x-contraction of a retiring layer
+    o.nph = take(npn * 4);               // int    NPH[npn], NPL[npn] node window (hi, lo)
+    o.npl = take(npn * 4);
+    o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]
+    o.zc = take(FZMAX * 16);             // float4 ZC[z]  control z weights
+    o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
+    o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
+    o.cx = take(32 * 4);                 // int    CX[32] adds per x-node of a retire (magic offsets)
+    o.total = off;
+    return o;
+}
+
+struct F2Args {
+    FArgs f;                        // items, records, lists, tables (pass 1's)
+    const float4 *MG;
+    const float *alpha, *beta, *gamma;   // combine output: [R], [R], [R][B]
+    const double *gbound;           // combine output: per-voxel bound of |Z dD/dm dM/dy_c|
+    float dxz;                      // (delta_x + 1)(delta_z + 1)
+    unsigned long long *gradi;      // [ndim][GzExt][Gy][Gx] int64, units 2^-k (Z dD/dphi)
+    int *xlist, *xcount;            // deferred exact-path voxels (slab-linear indices)
+    int xcap;
+    int npmax;                      // node-window capacity (entries)
+    P2Smem L2;                      // pass-2 shared-memory layout (host-computed: p2_smem(W, S, npmax))
+};
+
+template <int XV>
+struct P2Lane {
+    int xv[XV], relx[XV];
+    bool valid[XV];
+    VF<XV> ws[4];        // spatial x weights (tap l)
+    VF<XV> cr[4];        // rotated control x weights: entry k holds tap (k + q) & 3
+};
+
+template <int XV>
+__device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const P2Smem &L, unsigned char *smem, int y,
+                                       int warp, int lane, const P2Lane<XV> &pl, float gunit, int zn0, int yn0, int nxn,
+                                       int nyn) {
+    const FArgs &a = A2.f;
+    const Geo &g = a.g;
+    const int S = a.S, ns = it.nslots;
+    const float *GAM = reinterpret_cast<const float *>(smem + L.gam);
+    const float *AB = reinterpret_cast<const float *>(smem + L.ab);
+    float4 *GYw = reinterpret_cast<float4 *>(smem + L.gy) + warp * S * 8;
+    float4 *GZw = reinterpret_cast<float4 *>(smem + L.gz) + warp * 2 * S * 2;
+    int *RBw = reinterpret_cast<int *>(smem + L.rb) + warp * 96;
+    int *NPH = reinterpret_cast<int *>(smem + L.nph);
+    int *NPL = reinterpret_cast<int *>(smem + L.npl);
+    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);
+    const float4 *ZC = reinterpret_cast<const float4 *>(smem + L.zc);
+    const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
+    const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
+    const int *CX = reinterpret_cast<const int *>(smem + L.cx);
+
+    const int r = y - it.y0;
+    const int cby = a.t.cb[1][y];
+    const float4 cwy = a.t.cw[1][y];
+    const float4 swy = a.t.sw[1][y];
+    const int z0 = it.z0, zlen = it.zlen;
+    const long long line0 = (long long)it.line_off + (long long)r * zlen;
+    for (int k = lane; k <= zlen; k += 32) LOw[k] = __ldg(a.loff + line0 + k);
+    // ---- per row: gamma of the touched slots contracted over the y-taps, GY[s][b2][l].n;
+    // alpha / beta over y: lane = 16 ab + 4 l + n
+    {
+        const uint4 rm = a.rmask[it.row_off + r];
+        const unsigned words[4] = {rm.x, rm.y, rm.z, rm.w};
+        const int b2 = lane >> 4, l = (lane >> 2) & 3, n = lane & 3;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+            unsigned bits = words[w];
+            while (bits) {
+                const int s = 32 * w + __ffs(bits) - 1;
+                bits &= bits - 1;
+                const float *src = GAM + (s * 2 + b2) * 64 + n * 16 + l;
+                const float v = fmaf(swy.x, src[0], fmaf(swy.y, src[4], fmaf(swy.z, src[8], swy.w * src[12])));
+                reinterpret_cast<float *>(GYw + (s * 2 + b2) * 4 + l)[n] = v;
+            }
+        }
+    }
+    float abY;
+    {
+        const int ab = lane >> 4, l = (lane >> 2) & 3, n = lane & 3;
+        const float *src = AB + ab * 64 + n * 16 + l;
+        abY = fmaf(swy.x, src[0], fmaf(swy.y, src[4], fmaf(swy.z, src[8], swy.w * src[12])));
+    }
+    __syncwarp();
+
+    // ---- adjoint accumulators: 4 active control layers x 3 components
+    VF<XV> Ad[4][3];
+#pragma unroll
+    for (int n = 0; n < 4; ++n)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) Ad[n][c] = vsplat<XV>(0.f);
+    int gzl = ZB[0];
+    const int q4 = lane & 3;
+    // retire layer gzr with adjoints R (Z dD/dphi partials of this row): x-contract into RB
+    // (int32, warp exponent), then y-contract into the node window (exact (hi, lo) pairs)
+    auto retire = [&](int gzr, const VF<XV>(&R)[3]) {
+        float mx = 0.f;
+#pragma unroll
+        for (int c = 0; c < 3; ++c)
+#pragma unroll
+            for (int v = 0; v < XV; ++v) mx = fmaxf(mx, fabsf(R[c].v[v]));
+        const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(mx)) >> 23);
+        if (EA == 0) return;   // every adjoint zero (or denormal): nothing to retire
+        const int ks = min(148 - EA, 120);
+        const float sc = __int_as_float((ks + 127) << 23), isc = __int_as_float((127 - ks) << 23);
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            const float R0 = R[0].v[v] * sc, R1 = R[1].v[v] * sc, R2 = R[2].v[v] * sc;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int nd = pl.relx[v] + ((k + q4) & 3);
+                const float w = pl.cr[k].v[v];
+                red_shared(RBw + nd, __float_as_int(fmaf(w, R0, MAGIC)));
+                red_shared(RBw + 32 + nd, __float_as_int(fmaf(w, R1, MAGIC)));
+                red_shared(RBw + 64 + nd, __float_as_int(fmaf(w, R2, MAGIC)));
+            }
+        }
+        __syncwarp();
+        const int lz = gzr - zn0;
+        for (int i = lane; i < 3 * nxn; i += 32) {
+            const int c = i >= 2 * nxn ? 2 : (i >= nxn ? 1 : 0), j = i - c * nxn;
+            const int raw = RBw[c * 32 + j];
+            RBw[c * 32 + j] = 0;
+            const float rv = (float)(raw - CX[j] * MAGIC_I) * isc * gunit;
+            if (rv != 0.f) {
+                int *nh = NPH + ((lz * 3 + c) * nyn + (cby - yn0)) * nxn + j;
+                int *nl = NPL + ((lz * 3 + c) * nyn + (cby - yn0)) * nxn + j;
+#pragma unroll
+                for (int mm = 0; mm < 4; ++mm) {
+                    const float x = f4(cwy, mm) * rv;                 // |x| < 2^40
+                    int hi;
+                    const float hf = mfloor(x * (1.f / 1048576.f), hi);
+                    const float lo = fmaf(-hf, 1048576.f, x);         // [0, 2^20), exact
+                    const int loi = __float_as_int(lo + MAGIC) - MAGIC_I;
+                    red_shared(nh + mm * nxn, hi);
+                    red_shared(nl + mm * nxn, loi);
+                }
+            }
+        }
+        __syncwarp();
+    };
+
+    // per-lane row bases
+    const unsigned vb = (unsigned)(((z0 - a.mgz0) * g.ny + y) * g.nx + pl.xv[0]);
+    const int nxy = g.nxy32;
+    unsigned recn[XV];
+    float4 mgn[XV];
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        recn[v] = __ldg(a.rec + (vb + 32 * v));
+        mgn[v] = ld_stream4(A2.MG + (vb + 32 * v));
+    }
+    unsigned entn;
+    {
+        const unsigned o = LOw[0], o1 = LOw[1];
+        entn = o + lane < o1 ? __ldg(a.lent + o + lane) : 0u;
+    }
+    const float Lm1 = (float)(g.L - 1);
+    // the line tables of line jz into GZb; entn holds line jz's list entries (one per lane) on
+    // entry and line jz+1's on exit
+    auto gz_line = [&](int jz, float4 *GZb) {
+        const float4 wz = ZS[jz];
+        const unsigned o = LOw[jz], o1 = LOw[jz + 1], o2 = LOw[jz + 2 <= zlen ? jz + 2 : zlen];
+        const int cnt = (int)(o1 - o);
+        const unsigned ecur = entn;
+        entn = o1 + lane < o2 ? __ldg(a.lent + o1 + lane) : 0u;
+        // lane = (slot j of the pass, b2): the four x-taps of GZ[s][b2] from four independent loads
+        const int b2 = lane & 1;
+        {   // first pass (<= 16 slots: nearly every line) straight-line
+            const int j = lane >> 1;
+            const int s = (int)(__shfl_sync(FULL, ecur, j) & 0xFFu);
+            if (j < cnt) {
+                const float4 *gy = GYw + (s * 2 + b2) * 4;
+                const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
+                GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
+            }
+        }
+        for (int p = 1; 16 * p < cnt; ++p) {
+            const int j = 16 * p + (lane >> 1);
+            unsigned ent = __shfl_sync(FULL, ecur, j & 31);
+            if (j >= 32) ent = j < cnt ? __ldg(a.lent + o + j) : 0u;
+            if (j < cnt) {
+                const int s = (int)(ent & 0xFFu);
+                const float4 *gy = GYw + (s * 2 + b2) * 4;
+                const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
+                GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
+            }
+        }
+        float t = f4(wz, lane & 3) * abY;
+        t += __shfl_xor_sync(FULL, t, 1);
+        t += __shfl_xor_sync(FULL, t, 2);
+        if ((lane & 3) == 0) reinterpret_cast<float *>(GZb + ns * 2 + (lane >> 4))[(lane >> 2) & 3] = t;
+    };
+    gz_line(0, GZw);
+    for (int iz = 0; iz < zlen; ++iz) {
+        const int izn = min(iz + 1, zlen - 1);
+        unsigned rc[XV];
+        float4 mg[XV];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            rc[v] = recn[v];
+            mg[v] = mgn[v];
+            recn[v] = __ldg(a.rec + (vb + (unsigned)izn * (unsigned)nxy + 32 * v));
+            mgn[v] = ld_stream4(A2.MG + (vb + (unsigned)izn * (unsigned)nxy + 32 * v));
+        }
+        // ---- retire the control layers this slice no longer reads
+        const int bz = ZB[iz];
+        while (gzl < bz) {
+            retire(gzl, Ad[0]);
+#pragma unroll
+            for (int n = 0; n < 3; ++n)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) Ad[n][c] = Ad[n + 1][c];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) Ad[3][c] = vsplat<XV>(0.f);
+            ++gzl;
+        }
+        // ---- the NEXT line's tables (double-buffered; independent of this slice's voxels, so
+        // their shared-memory latency overlaps the voxel work below): gamma of the touched slots
+        // over z (GZ[s][b2].l), alpha / beta over z (GZ[ns][ab].l)
+        __syncwarp();
+        if (iz + 1 < zlen) gz_line(iz + 1, GZw + ((iz + 1) & 1) * S * 2);
+        const float4 *GZc = GZw + (iz & 1) * S * 2;
+        // ---- per voxel: Z dD/dm and the adjoint
+        VF<XV> dx, dy, dzv;
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            float m = mg[v].x;
+            const bool ex = m < 0.f;
+            m = ex ? -1.0f - m : m;
+            const int slot = (int)(rc[v] >> 24);
+            const float hhi = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu)) - 1.0f;
+            int im;
+            const float fl = mfloor(m, im);
+            const float nf = fminf(fl, Lm1);
+            const float fm = m - nf;
+            const bool integral = m == fl;
+            const float g1p = integral ? 0.1f : (fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f));
+            const float c2 = integral ? 2.0f * m : fmaf(2.0f, nf, 1.0f);
+            const float4 G0 = GZc[slot * 2], G1 = GZc[slot * 2 + 1], AY = GZc[ns * 2], BY = GZc[ns * 2 + 1];
+            const float w0 = pl.ws[0].v[v], w1 = pl.ws[1].v[v], w2 = pl.ws[2].v[v], w3 = pl.ws[3].v[v];
+            const float At = fmaf(w3, AY.w, fmaf(w2, AY.z, fmaf(w1, AY.y, w0 * AY.x)));
+            const float Bt = fmaf(w3, BY.w, fmaf(w2, BY.z, fmaf(w1, BY.y, w0 * BY.x)));
+            const float g0 = fmaf(w3, G0.w, fmaf(w2, G0.z, fmaf(w1, G0.y, w0 * G0.x)));
+            const float g1 = fmaf(w3, G1.w, fmaf(w2, G1.z, fmaf(w1, G1.y, w0 * G1.x)));
+            const float Gt = fmaf(hhi, g1 - g0, g0);
+            float d = g1p * fmaf(c2, At, 2.0f * (Bt - Gt));
+            if (ex && pl.valid[v]) {   // deferred to k_exact_fix (fp64)
+                const int pos = atomicAdd(A2.xcount, 1);
+                if (pos < A2.xcap) A2.xlist[pos] = ((z0 + iz - a.mgz0) * g.ny + y) * g.nx + pl.xv[v];
+            }
+            d = (ex || !pl.valid[v]) ? 0.f : d;
+            dx.v[v] = d * mg[v].y;
+            dy.v[v] = d * mg[v].z;
+            dzv.v[v] = d * mg[v].w;
+        }
+        const float4 cwz = ZC[iz];
+#pragma unroll
+        for (int n = 0; n < 4; ++n) {
+            const VF<XV> w = vsplat<XV>(f4(cwz, n));
+            Ad[n][0] = vfma(w, dx, Ad[n][0]);
+            Ad[n][1] = vfma(w, dy, Ad[n][1]);
+            Ad[n][2] = vfma(w, dzv, Ad[n][2]);
+        }
+        __syncwarp();
+    }
+#pragma unroll
+    for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
+}
+
+template <int XV, int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_p2f(F2Args A2) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const FArgs &a = A2.f;
+    const int W = a.W, S = a.S;
+    const Geo &g = a.g;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ii = a.i0 + blockIdx.x;
+    const FItem it = a.items[ii];
+    const int ns = it.nslots;
+    const int xn0 = a.t.cb[0][it.x0], nxn = a.t.cb[0][it.x0 + it.xlen - 1] + 4 - xn0;
+    const int yn0 = a.t.cb[1][it.y0], nyn = a.t.cb[1][it.y0 + it.ylen - 1] + 4 - yn0;
+    const int zn0 = a.t.cb[2][it.z0], nzn = a.t.cb[2][it.z0 + it.zlen - 1] + 4 - zn0;
+    const int npn = nzn * 3 * nyn * nxn;
+    const P2Smem &L = A2.L2;
+    float *GAM = reinterpret_cast<float *>(smem + L.gam);
+    float *AB = reinterpret_cast<float *>(smem + L.ab);
+    int *RB = reinterpret_cast<int *>(smem + L.rb);
+    int *NPH = reinterpret_cast<int *>(smem + L.nph);
+    int *NPL = reinterpret_cast<int *>(smem + L.npl);
+    float4 *ZC = reinterpret_cast<float4 *>(smem + L.zc);
+    int *ZB = reinterpret_cast<int *>(smem + L.zb);
+    float4 *ZS = reinterpret_cast<float4 *>(smem + L.zs);
+    int *CX = reinterpret_cast<int *>(smem + L.cx);
+
+    const int cx = a.t.sb[0][it.x0], cy = a.t.sb[1][it.y0], cz = a.t.sb[2][it.z0];
+    // region (n, m, l) of the item at n*16 + m*4 + l
+    for (int i = threadIdx.x; i < ns * 128; i += blockDim.x) {
+        const int s = i >> 7, b2 = (i >> 6) & 1, rr = i & 63;
+        const int n = rr >> 4, mm = (rr >> 2) & 3, l = rr & 3;
+        const long long reg = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        GAM[i] = __ldg(A2.gamma + reg * g.B + a.slotbins[it.slot_off + s] + b2);
+    }
+    for (int i = threadIdx.x; i < 128; i += blockDim.x) {
+        const int ab = i >> 6, rr = i & 63;
+        const int n = rr >> 4, mm = (rr >> 2) & 3, l = rr & 3;
+        const long long reg = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
+        AB[i] = __ldg((ab ? A2.beta : A2.alpha) + reg);
+    }
+    for (int i = threadIdx.x; i < npn; i += blockDim.x) { NPH[i] = 0; NPL[i] = 0; }
+    for (int i = threadIdx.x; i < W * 96; i += blockDim.x) RB[i] = 0;
+    for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {
+        ZC[i] = a.t.cw[2][it.z0 + i];
+        ZB[i] = a.t.cb[2][it.z0 + i];
+        ZS[i] = a.t.sw[2][it.z0 + i];
+    }
+    if (threadIdx.x < 32) {   // adds per x-node of one retire (every lane voxel; padding ones add 0)
+        int cnt = 0;
+        for (int k = 0; k < 32 * XV; ++k) {
+            const int rx = a.t.cb[0][min(it.x0 + k, it.x0 + it.xlen - 1)] - xn0;
+            cnt += (rx <= (int)threadIdx.x && (int)threadIdx.x <= rx + 3) ? 1 : 0;
+        }
+        CX[threadIdx.x] = cnt;
+    }
+    const int kg = grad_shift(*A2.gbound, A2.dxz);
+    const float gunit = ldexpf(1.f, kg);
+    P2Lane<XV> pl;
+    const int q4 = lane & 3;
+#pragma unroll
+    for (int v = 0; v < XV; ++v) {
+        pl.valid[v] = lane + 32 * v < it.xlen;
+        pl.xv[v] = pl.valid[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+        pl.relx[v] = a.t.cb[0][pl.xv[v]] - xn0;
+    }
+#pragma unroll
+    for (int l = 0; l < 4; ++l)
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            pl.ws[l].v[v] = pl.valid[v] ? f4(a.t.sw[0][pl.xv[v]], l) : 0.f;
+            pl.cr[l].v[v] = pl.valid[v] ? f4(a.t.cw[0][pl.xv[v]], (l + q4) & 3) : 0.f;
+        }
+    __syncthreads();
+    for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W)
+        p2_row<XV>(A2, it, L, smem, y, warp, lane, pl, gunit, zn0, yn0, nxn, nyn);
+    __syncthreads();
+    // ---- flush the node window: int64 (hi 2^20 + lo) into the global gradient
+    const long long plane = (long long)g.Gx * g.Gy;
+    for (int i = threadIdx.x; i < npn; i += blockDim.x) {
+        const long long v = (long long)NPH[i] * 1048576LL + (long long)NPL[i];
+        if (v == 0) continue;
+        const int gxl = i % nxn;
+        int t = i / nxn;
+        const int gyl = t % nyn;
+        t /= nyn;
+        const int c = t % 3, lz = t / 3;
+        const int gzn = zn0 + lz;
+        if (c >= g.ndim || gzn >= g.GzExt) continue;
+        atomicAdd(A2.gradi + ((long long)c * g.GzExt + gzn) * plane + (long long)(yn0 + gyl) * g.Gx + (xn0 + gxl),
+                  (unsigned long long)v);
+    }
+}
+
+// int64 gradient (units 2^-k, Z dD/dphi) -> fp64 dD/dphi, zeroing the int64 buffer
+__global__ void k_grad_convert(unsigned long long *__restrict__ gi, double *__restrict__ gd, long long n,
+                               const double *gbound, float dxz, double invZ) {
+    const double s = ldexp(invZ, -grad_shift(*gbound, dxz));
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        gd[i] = (double)(long long)gi[i] * s;
+        gi[i] = 0ull;
+    }
+}
+
+}  // namespace srwcr

@@ -84,7 +84,22 @@ struct PassArgs {
     const float *alpha, *beta, *gamma;  // pass 2 in: [R], [R], [R][B]
     float invZ;
     double *grad;               // pass 2 out: [ndim][GzExt][Gy][Gx] (fp64)
+    unsigned long long *gradi;  // fast pass 2: int64 gradient (units 2^-k, without 1/Z), or null
+    const double *gbound;       //   the combine's per-voxel bound (k = grad_shift(*gbound, dxz))
+    float dxz;                  //   delta_x * delta_z (+1 each): per-add bound factor
 };
+
+// Fixed-point shift k of fast pass 2's gradient accumulation: one node-window add is at most
+// (delta_x + 1)(delta_z + 1) gbound in magnitude (the B-spline weights of a node sum to about
+// delta per axis); k keeps it below 2^40 so that the int32 (hi, lo) pair of the node window and
+// the int64 global sums are exact.
+__device__ __forceinline__ int grad_shift(double b1, float dxz) {
+    const double bnd = b1 * (double)dxz * 1.1;
+    if (!(bnd > 0.0) || !(bnd < 1e300)) return 40;
+    int e;
+    frexp(bnd, &e);   // bnd < 2^e
+    return max(-200, min(60, 40 - e));
+}
 
 __device__ __forceinline__ float f4(const float4 &v, int i) {
     return i == 0 ? v.x : i == 1 ? v.y : i == 2 ? v.z : v.w;
@@ -208,6 +223,17 @@ __device__ __forceinline__ void parzen_pair(float f, float &hlo, float &hhi) {
         hlo = w;
         hhi = 1.0f - w;
     }
+}
+
+// Parzen pair of the FIXED image with h_hi rounded to a multiple of 2^-23 (|error| <= 2^-24,
+// fp32-rounding size): the static record of the fast passes stores h_hi in 24 bits, and every
+// pass, the static counts N and the exact path use the same weights, so that S and N (whose
+// ratio is the conditional mean of Eq 10) are accumulated with identical h.
+__device__ __forceinline__ void parzen_pair_F(float f, float &hlo, float &hhi) {
+    float lo, hi;
+    parzen_pair(f, lo, hi);
+    hhi = rintf(hi * 8388608.f) * (1.f / 8388608.f);
+    hlo = 1.0f - hhi;
 }
 
 // recursive-halving warp reduction of 8 per-lane values: afterwards every lane holds
@@ -546,7 +572,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
                 a0[v] = min((int)Fv, g.L - 1);
                 slot[v] = smap[a0[v]];
                 float hlo, hhi;
-                parzen_pair(Fv - (float)a0[v], hlo, hhi);
+                parzen_pair_F(Fv - (float)a0[v], hlo, hhi);
                 if (STATIC) {
                     lo[v] = hlo;
                     hi[v] = hhi;
@@ -905,8 +931,9 @@ struct CombineArgs {
     const double *NQ;           // ORI 1: [R][B][2] dynamic counts N' (lo, hi halves)
     int gstride;                // ORI 1: row stride of gamma = 3 (B + 2)
     unsigned *ticket;           // last-CTA ticket (0 between launches)
-    double *part;               // [2 * gridDim] per-CTA partial sums of dterm, retained
+    double *part;               // [3 * gridDim] per-CTA partial sums of dterm, retained; max q_r
     double *Dout;               // [2] D, #retained regions
+    double *gbound;             // [1] bound on |dD/dm * dM/dy_c| * Z per voxel (fast pass 2's fixed point)
 };
 
 __device__ __forceinline__ double warp_sum_d(double v) {
@@ -918,33 +945,51 @@ __device__ __forceinline__ double warp_sum_d(double v) {
 // D = (1/Z) sum_r dterm[r], deterministic: each CTA sums its regions' dterm and retained
 // flags in warp order into part[2*blockIdx]; the last CTA (atomic ticket) sums the
 // partials in block order into Dout = {D, #retained} and re-arms the ticket.
-__device__ __forceinline__ void combine_tail(const CombineArgs &a, double dt, double rt) {
+// The third value is a max: q_r = (2L+1)|alpha_r| + 2|beta_r| + 2 max_a |gamma_ra| over the
+// regions, giving gbound = 1.9 L max_r q_r >= |Z dD/dm dM/dy_c| per voxel (|g1'| <= 1.9, the
+// spatial weights sum to 1, |dM/dy_c| <= L): the scale of fast pass 2's fixed point.
+__device__ __forceinline__ void combine_tail(const CombineArgs &a, double dt, double rt, double mq = 0.0) {
     __shared__ bool last;
-    __shared__ double sd[256], sc[256];
+    __shared__ double sd[256], sc[256], sq[256];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    if (lane == 0) { sd[warp] = dt; sc[warp] = rt; }
+    if (lane == 0) { sd[warp] = dt; sc[warp] = rt; sq[warp] = mq; }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double s = 0, c = 0;
-        for (int w = 0; w < nw; ++w) { s += sd[w]; c += sc[w]; }
-        a.part[2 * blockIdx.x] = s;
-        a.part[2 * blockIdx.x + 1] = c;
+        double s = 0, c = 0, q = 0;
+        for (int w = 0; w < nw; ++w) { s += sd[w]; c += sc[w]; q = fmax(q, sq[w]); }
+        a.part[3 * blockIdx.x] = s;
+        a.part[3 * blockIdx.x + 1] = c;
+        a.part[3 * blockIdx.x + 2] = q;
         __threadfence();
         last = atomicAdd(a.ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    double s = 0, c = 0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) { s += __ldcg(a.part + 2 * i); c += __ldcg(a.part + 2 * i + 1); }
+    double s = 0, c = 0, q = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        s += __ldcg(a.part + 3 * i);
+        c += __ldcg(a.part + 3 * i + 1);
+        q = fmax(q, __ldcg(a.part + 3 * i + 2));
+    }
     sd[threadIdx.x] = s;
     sc[threadIdx.x] = c;
+    sq[threadIdx.x] = q;
     __syncthreads();
     for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) { sd[threadIdx.x] += sd[threadIdx.x + o]; sc[threadIdx.x] += sc[threadIdx.x + o]; }
+        if (threadIdx.x < o) {
+            sd[threadIdx.x] += sd[threadIdx.x + o];
+            sc[threadIdx.x] += sc[threadIdx.x + o];
+            sq[threadIdx.x] = fmax(sq[threadIdx.x], sq[threadIdx.x + o]);
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) { a.Dout[0] = sd[0] / a.Z; a.Dout[1] = sc[0]; *a.ticket = 0u; }
+    if (threadIdx.x == 0) {
+        a.Dout[0] = sd[0] / a.Z;
+        a.Dout[1] = sc[0];
+        if (a.gbound) a.gbound[0] = 1.9 * (double)(a.B - 1) * sq[0];
+        *a.ticket = 0u;
+    }
 }
 
 __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, double &N, double &S) {
@@ -960,10 +1005,12 @@ __device__ __forceinline__ void bin_NS(const CombineArgs &a, int r, int b, doubl
     }
 }
 
-// returns (in dt, rt; lane 0 of the region's warp) the region's dterm and retained flag
-__device__ __forceinline__ void combine_region(const CombineArgs &a, int r, double &dt, double &rt) {
+// returns (in dt, rt; lane 0 of the region's warp) the region's dterm and retained flag, and
+// (every lane) the region's q_r of combine_tail
+__device__ __forceinline__ void combine_region(const CombineArgs &a, int r, double &dt, double &rt, double &mq) {
     const int lane = threadIdx.x & 31;
     dt = rt = 0.0;
+    mq = 0.0;
     if (r >= a.R) return;
     const int B = a.B;
     double Nv[4], Sv[4];    // this lane's bins b = lane + 32 k (B <= 128)
@@ -1008,11 +1055,16 @@ __device__ __forceinline__ void combine_region(const CombineArgs &a, int r, doub
         rg[0] = pr; rg[1] = sig2; rg[2] = mu; rg[3] = omcr; rg[4] = rt; rg[5] = a.Z;
     }
     const double is2 = ret ? 1.0 / sig2 : 0.0;
+    float gmax = 0.f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
         const int b = lane + 32 * k;
-        if (b < B) a.gamma[(long long)r * B + b] = (ret && Nv[k] > 0.0) ? (float)((Sv[k] / Nv[k]) * is2) : 0.f;
+        const float gv = (ret && Nv[k] > 0.0) ? (float)((Sv[k] / Nv[k]) * is2) : 0.f;
+        if (b < B) a.gamma[(long long)r * B + b] = gv;
+        gmax = fmaxf(gmax, b < B ? fabsf(gv) : 0.f);
     }
+    gmax = __uint_as_float(__reduce_max_sync(FULL, __float_as_uint(gmax)));
+    if (ret) mq = (2.0 * (B - 1) + 1.0) * fabs((1.0 - omcr) / sig2) + 2.0 * fabs(omcr * mu / sig2) + 2.0 * (double)gmax;
 }
 
 
@@ -1102,14 +1154,15 @@ __device__ __forceinline__ void combineA_region(const CombineArgs &a, int r, dou
 // a fixed grid: warp w of CTA b takes regions b*8 + w, then + 8*gridDim (fine lattices have
 // 10^5-10^6 regions; one CTA per 8 regions made the last-CTA ticket a serial hot spot)
 __global__ void __launch_bounds__(256) k_combine(CombineArgs a) {
-    double dt = 0, rt = 0;
+    double dt = 0, rt = 0, mq = 0;
     for (int r = blockIdx.x * 8 + (threadIdx.x >> 5); r < a.R; r += gridDim.x * 8) {
-        double d1, r1;
-        combine_region(a, r, d1, r1);
+        double d1, r1, q1;
+        combine_region(a, r, d1, r1, q1);
         dt += d1;
         rt += r1;
+        mq = fmax(mq, q1);
     }
-    combine_tail(a, dt, rt);
+    combine_tail(a, dt, rt, mq);
 }
 __global__ void __launch_bounds__(256) k_combineA(CombineArgs a) {
     double dt = 0, rt = 0;
@@ -1496,7 +1549,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 5) : 1) k_pass2(
             for (int v = 0; v < XV; ++v) {
                 const float Fv = Fl[v];
                 a0[v] = min((int)Fv, g.L - 1);
-                parzen_pair(Fv - (float)a0[v], hlo[v], hhi[v]);
+                parzen_pair_F(Fv - (float)a0[v], hlo[v], hhi[v]);
             }
             __syncwarp();
 #pragma unroll
@@ -1618,7 +1671,7 @@ __device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx
     const float Fv = a.F[(long long)z * g.nxy + (long long)y * g.nx + x];
     const int a0 = min((int)Fv, g.L - 1);
     float hlo, hhi;
-    parzen_pair(Fv - (float)a0, hlo, hhi);
+    parzen_pair_F(Fv - (float)a0, hlo, hhi);
     const int cx = a.t.sb[0][x], cy = a.t.sb[1][y], cz = a.t.sb[2][z];
     const float4 sx = a.t.sw[0][x], sy = a.t.sw[1][y], sz = a.t.sw[2][z];
     float al[4], be[4], ga[4];
@@ -1677,14 +1730,17 @@ __device__ __forceinline__ void exact_fix_voxel(const PassArgs &a, long long idx
     const float d = ORI == 0 ? e.g1p * a.invZ * fmaf(e.c2, At, 2.0f * (Bt - Gt)) : a.invZ * At;
     const float dc[3] = {d * e.gx, d * e.gy, d * e.gz};
     const float4 wx = a.t.cw[0][x], wy = a.t.cw[1][y], wz = a.t.cw[2][z];
+    const double unit = a.gradi ? ldexp(1.0, grad_shift(*a.gbound, a.dxz)) : 1.0;
 #pragma unroll
     for (int h = 0; h < 4; ++h) {
         const int tp = gl + 16 * h, nn = tp >> 4, mm = (tp >> 2) & 3, l = tp & 3;
         if (bz + nn >= g.GzExt || f4(wz, nn) == 0.f) continue;
         const float w = f4(wz, nn) * f4(wy, mm) * f4(wx, l);
-        for (int c = 0; c < g.ndim; ++c)
-            atomicAdd(a.grad + (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l,
-                      (double)(w * dc[c]));
+        for (int c = 0; c < g.ndim; ++c) {
+            const long long gi = (((long long)c * g.GzExt + bz + nn) * g.Gy + by + mm) * g.Gx + bx + l;
+            if (a.gradi) atomicAdd(a.gradi + gi, (unsigned long long)__double2ll_rn((double)(w * dc[c]) * unit));
+            else atomicAdd(a.grad + gi, (double)(w * dc[c]));
+        }
     }
     __syncwarp(gm);   // sp is reused by the group's next voxel
 }
