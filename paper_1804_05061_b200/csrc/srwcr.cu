@@ -31,6 +31,7 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*AllReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi &nccl() {
@@ -44,8 +45,9 @@ NcclApi &nccl() {
             api.CommInitRank = (decltype(api.CommInitRank))dlsym(h, "ncclCommInitRank");
             api.AllReduce = (decltype(api.AllReduce))dlsym(h, "ncclAllReduce");
             api.CommDestroy = (decltype(api.CommDestroy))dlsym(h, "ncclCommDestroy");
+            api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
-            api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString;
+            api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString && api.Broadcast;
         }
     }
     return api;
@@ -409,23 +411,31 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     if (g.nz == 1 || c->opt.orientation != 0 || c->MC || c->z1 <= c->z0) return SRWCR_OK;
     int XV = c->XV;
     if (const char *e = getenv("SRWCR_FXV")) XV = std::min(XV, std::max(1, atoi(e)));
+    // the split (rows and slices per item) is chosen on the WHOLE volume so that every rank of a
+    // z-slab decomposition whose slab boundaries fall on spatial z-cells runs exactly the items
+    // of the single-GPU decomposition that lie in its slab (bitwise-equal statistics sums)
     int ymax = 32, zmax = FZMAX;
-    std::vector<Item> its;
-    for (;;) {
-        its.clear();
+    auto make_items = [&](int zlo, int zhi) {
+        std::vector<Item> out;
         auto xr = runs(c->h_sb[0], 0, g.nx, 32 * XV);
         auto yr = runs(c->h_sb[1], 0, g.ny, ymax);
-        auto zr = runs(c->h_sb[2], (int)c->z0, (int)c->z1, zmax);
+        auto zr = runs(c->h_sb[2], zlo, zhi, zmax);
         for (auto &zz : zr)
             for (auto &yy : yr)
-                for (auto &xx : xr) its.push_back(Item{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second, 0, 0, 0.f, 0});
-        if ((long long)its.size() * 2 < 3LL * nsm && (ymax > 16 || zmax > 16)) {
+                for (auto &xx : xr) out.push_back(Item{xx.first, xx.second, yy.first, yy.second, zz.first, zz.second, 0, 0, 0.f, 0});
+        return out;
+    };
+    for (;;) {
+        const size_t nall = make_items(0, g.nz).size();
+        if ((long long)nall * 2 < 3LL * nsm && (ymax > 16 || zmax > 16)) {
             if (ymax > 16) ymax = 16;
             else zmax /= 2;
             continue;
         }
         break;
     }
+    std::vector<Item> its = make_items((int)c->z0, (int)c->z1);
+    if (its.empty()) return SRWCR_OK;
     for (const Item &it : its) {
         const int nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
         if (nxn > 32 || it.zlen > FZMAX) return SRWCR_OK;   // not eligible: round-1 passes
@@ -630,7 +640,7 @@ static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bo
         CKL();
     }
     if (convert) {
-        k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c));
+        k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c), (long long)c->R * c->g.B * 2);
         CKL();
     }
     return SRWCR_OK;
@@ -648,7 +658,7 @@ static srwcr_status launch_fast_prep(srwcr_ctx *c, const double *pd) {
 }
 
 // fast pass 2 (+ the fp64 exact-path voxels, + the int64 -> fp64 gradient conversion)
-static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad) {
+static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad, bool reduce_int64 = false) {
     F2Args A{};
     A.f = fast_args(c);
     A.MG = c->MG;
@@ -679,6 +689,9 @@ static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad) {
     pa.dxz = c->fdxz;
     k_exact_fix<0><<<1184, 128, 0, c->stream>>>(pa);
     CKL();
+    // z-slabs: the int64 gradient partials are summed across ranks before the conversion
+    // (exact: the same gradient bits for every rank count)
+    if (reduce_int64) NCK(nccl().AllReduce(c->gradi, c->gradi, (size_t)c->nparams, ncclInt64, ncclSum, c->comm, c->stream));
     k_grad_convert<<<592, 256, 0, c->stream>>>(c->gradi, grad, (long long)c->nparams, c->Dout + 2, c->fdxz, 1.0 / c->Z);
     CKL();
     return SRWCR_OK;
@@ -1170,6 +1183,23 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     }
     c->launches_per_eval = 6;  // prep (phi + x-max, y/z-max), pass 1, combine (+ D), pass 2, exact fix
     TRY(build_fast(c, nsm));
+    if (c->comm && c->nranks > 1) {
+        // z-slab ranks: every rank computed the whole-volume static counts and moment shifts
+        // (fp32 shared / fp64 global atomics: equal to rounding, not bitwise); rank 0's copy is
+        // broadcast so that the replicated combine -- and so D, the coefficient tables and the
+        // gradient -- are bitwise identical on every rank
+        const long long RBn = c->R * g.B;
+        NCK(nccl().Broadcast(c->Nlo, c->Nlo, (size_t)RBn, ncclFloat64, 0, c->comm, c->stream));
+        NCK(nccl().Broadcast(c->Nup, c->Nup, (size_t)RBn, ncclFloat64, 0, c->comm, c->stream));
+        NCK(nccl().Broadcast(c->shiftc, c->shiftc, (size_t)g.B, ncclFloat32, 0, c->comm, c->stream));
+        double *zb = nullptr;
+        CK(cudaMalloc(&zb, sizeof(double)));
+        CK(cudaMemcpy(zb, &c->Z, sizeof(double), cudaMemcpyHostToDevice));
+        NCK(nccl().Broadcast(zb, zb, 1, ncclFloat64, 0, c->comm, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        CK(cudaMemcpy(&c->Z, zb, sizeof(double), cudaMemcpyDeviceToHost));
+        cudaFree(zb);
+    }
     if (c->fast) c->launches_per_eval = 7;   // prep, pass 1, stats conversion, combine, pass 2, exact fix, gradient conversion
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
@@ -1238,7 +1268,14 @@ static srwcr_status eval_begin_impl(srwcr_ctx *c, const double *params, int pdev
     if (c->fast) {
         TRY(launch_fast_prep(c, pd));
         if (c->timing) CK(record_ev(c, 0));
-        TRY(launch_fast_pass1(c));
+        // with a communicator the int64 statistics are summed across ranks before the
+        // conversion: exact, so every rank count gives bitwise the same statistics
+        TRY(launch_fast_pass1(c, 0, -1, c->comm == nullptr));
+        if (c->comm) {
+            NCK(nccl().AllReduce(c->SQi, c->SQi, stats_count(c), ncclInt64, ncclSum, c->comm, c->stream));
+            k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c), (long long)c->R * c->g.B * 2);
+            CKL();
+        }
     } else {
         CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
         if (c->timing) CK(record_ev(c, 0));
@@ -1258,12 +1295,12 @@ static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_gra
     if (grad) {
         gd = grad_dev ? grad : c->grad64;
         if (c->fast) {
-            TRY(launch_fast_pass2(c, gd));
+            TRY(launch_fast_pass2(c, gd, reduce_grad && c->comm));
         } else {
             CK(cudaMemsetAsync(gd, 0, sizeof(double) * c->nparams, c->stream));
             TRY(launch_pass2(c, gd));
+            if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
         }
-        if (reduce_grad) TRY(allreduce(c, gd, (size_t)c->nparams));
     }
     if (c->timing) CK(record_ev(c, 3));
     CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1306,7 +1343,9 @@ static srwcr_status eval_graph(srwcr_ctx *c, const double *params, double *value
         const int64_t l0 = c->launches;
         CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
         srwcr_status st = eval_begin_impl(c, params, 1);
-        if (st == SRWCR_OK) st = eval_end_enqueue(c, grad, false, 1);
+        // z-slab ranks: the NCCL collectives are captured into the graph with the kernels
+        if (st == SRWCR_OK && c->comm && !c->fast) st = allreduce(c, c->SQ, stats_count(c));
+        if (st == SRWCR_OK) st = eval_end_enqueue(c, grad, c->comm != nullptr, 1);
         cudaGraph_t gr = nullptr;
         const cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
         c->g_kernels = c->launches - l0;
@@ -1425,14 +1464,14 @@ static srwcr_status eval_host_pipelined(srwcr_ctx *c, const double *params, doub
 extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
     if (!c) return SRWCR_EINVAL;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
-    if (c->opt.use_graph && !c->comm && !c->poisoned && params && is_device_ptr(params) &&
+    if (c->opt.use_graph && !c->poisoned && params && is_device_ptr(params) &&
         (!grad || is_device_ptr(grad)))
         return eval_graph(c, params, value, grad);
     if (!c->comm && !c->timing && !c->poisoned && !c->fast && params && (c->p1_split > 0 || c->p2_split > 0) &&
         !is_device_ptr(params) && (!grad || !is_device_ptr(grad)))
         return eval_host_pipelined(c, params, value, grad);
     TRY(eval_begin_impl(c, params));
-    TRY(allreduce(c, c->SQ, stats_count(c)));
+    if (!c->fast) TRY(allreduce(c, c->SQ, stats_count(c)));   // (fast: int64 sum inside eval_begin)
     return eval_end_impl(c, value, grad, true);
 }
 

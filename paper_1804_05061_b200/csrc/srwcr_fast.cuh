@@ -28,7 +28,8 @@ namespace srwcr {
 
 constexpr float MAGIC = 12582912.f;        // 1.5 * 2^23: float bits 0x4B400000 + round(x), |x| < 2^22
 constexpr int MAGIC_I = 0x4B400000;
-constexpr double STAT_UNIT = 65536.0;      // global statistics: int64 fixed point, units 2^-16
+constexpr double STAT_UNIT = 65536.0;      // binless second moments: int64 fixed point, units 2^-16
+constexpr double STAT_UNIT_S = 16777216.0; // binned first moments (shifted, small): units 2^-24
 constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
 constexpr int FZMAX = 128;                 // max slices per item
 
@@ -154,7 +155,8 @@ struct FArgs {
     P1Smem L1;                      // pass-1 shared-memory layout (host-computed: p1_smem(W, S))
     int ablate;                     // timing experiments only (SRWCR_ABLATE; wrong results): bit 0 no MG
                                     // store, bit 1 no line-table atomics / fold, bit 2 no M gathers;
-                                    // (correct results) bit 3 no uniform-line path, bit 4 no dither
+                                    // (correct results) bit 3 no uniform-line path, bit 4 no dither;
+                                    // pass 2 (wrong results): bit 5 no line tables, bit 6 no retire
 };
 
 // ------------------------------------------------------------------ create-time builders
@@ -304,16 +306,16 @@ __global__ void k_fprep(const double *__restrict__ p, float *__restrict__ phi, G
 
 // int64 statistics (units 2^-16) -> fp64 SQ / Q (exact below 2^53 units), zeroing the int64
 // buffer for the next evaluation
-__global__ void k_stats_convert(unsigned long long *__restrict__ si, double *__restrict__ sd, long long n) {
+__global__ void k_stats_convert(unsigned long long *__restrict__ si, double *__restrict__ sd, long long n, long long nS) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         const long long v = (long long)si[i];
-        sd[i] = (double)v * (1.0 / STAT_UNIT);
+        sd[i] = (double)v * (i < nS ? 1.0 / STAT_UNIT_S : 1.0 / STAT_UNIT);
         si[i] = 0ull;
     }
 }
 
-__device__ __forceinline__ void atomic_add_i64(unsigned long long *p, double v) {
-    atomicAdd(p, (unsigned long long)__double2ll_rn(v * STAT_UNIT));
+__device__ __forceinline__ void atomic_add_i64(unsigned long long *p, double v, double unit = STAT_UNIT) {
+    atomicAdd(p, (unsigned long long)__double2ll_rn(v * unit));
 }
 
 // ------------------------------------------------------------------ pass 1 (fast)
@@ -919,7 +921,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
         const int s = t >> 7, mm = (t >> 5) & 3, e = (t >> 2) & 7, n = t & 3;
         const int l = e >> 1, ch = e & 1;
         const long long r = ((long long)(cz + n) * g.Ky + (cy + mm)) * g.Kx + (cx + l);
-        atomic_add_i64(a.SQi + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val);
+        atomic_add_i64(a.SQi + (r * B + a.slotbins[it.slot_off + s]) * 2 + ch, (double)val, STAT_UNIT_S);
     }
     if (threadIdx.x < 64) {
         const int l = threadIdx.x >> 4, mm = (threadIdx.x >> 2) & 3, n = threadIdx.x & 3;
@@ -1173,7 +1175,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         // ---- retire the control layers this slice no longer reads
         const int bz = ZB[iz];
         while (gzl < bz) {
-            retire(gzl, Ad[0]);
+            if (!(a.ablate & 64)) retire(gzl, Ad[0]);
 #pragma unroll
             for (int n = 0; n < 3; ++n)
 #pragma unroll
@@ -1186,7 +1188,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         // their shared-memory latency overlaps the voxel work below): gamma of the touched slots
         // over z (GZ[s][b2].l), alpha / beta over z (GZ[ns][ab].l)
         __syncwarp();
-        if (iz + 1 < zlen) gz_line(iz + 1, GZw + ((iz + 1) & 1) * S * 2);
+        if (iz + 1 < zlen && !(a.ablate & 32)) gz_line(iz + 1, GZw + ((iz + 1) & 1) * S * 2);
         const float4 *GZc = GZw + (iz & 1) * S * 2;
         // ---- per voxel: Z dD/dm and the adjoint
         VF<XV> dx, dy, dzv;
@@ -1232,7 +1234,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         __syncwarp();
     }
 #pragma unroll
-    for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
+    if (!(a.ablate & 64))
+        for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
 }
 
 template <int XV, int MAXT>

@@ -232,7 +232,11 @@ __device__ __forceinline__ void parzen_pair(float f, float &hlo, float &hhi) {
 __device__ __forceinline__ void parzen_pair_F(float f, float &hlo, float &hhi) {
     float lo, hi;
     parzen_pair(f, lo, hi);
-    hhi = rintf(hi * 8388608.f) * (1.f / 8388608.f);
+    // the zero pattern is kept: a nonzero weight never rounds to 0 (nor its complement)
+    float k = rintf(hi * 8388608.f);
+    k = hi > 0.f ? fmaxf(k, 1.f) : k;
+    k = lo > 0.f ? fminf(k, 8388607.f) : k;
+    hhi = k * (1.f / 8388608.f);
     hlo = 1.0f - hhi;
 }
 

@@ -133,3 +133,31 @@ def test_dynamic_bin_mismatch_report():
     assert mism <= int(near.sum())                 # only next to an integer
     assert np.abs(m_g - m_o).max() < 1e-3           # fp32 sample of fp64 quality
     assert mism <= 1e-4 * m_o.size
+
+
+def test_fast_path_nccl_single_rank_graph():
+    """The library-driven z-slab exchange (int64 ncclAllReduce of the statistics and of the
+    gradient, captured into the per-rank CUDA graph with the kernels) on one rank: the result
+    of the context without a communicator (to the create-time static counts, which each
+    context computes itself), and bitwise reproducible across graph replays."""
+    torch = pytest.importorskip("torch")
+    import paper_1804_05061_b200 as S
+    import synth
+    g1, pb, Fn, Mn, params = _case("C5", 1, "small")
+    pt = torch.from_numpy(params).cuda()
+    gt1 = torch.empty_like(pt)
+    D1, _ = g1.eval(pt, grad=gt1)
+    cfg = synth.config("C5", FAST_DIMS["C5"])
+    F, M = synth.make_pair("C5", 1, cfg["dims"])
+    g2 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], nranks=1, rank=0,
+                 nccl_id=torch.cuda.nccl.unique_id())
+    assert g2.stats()["fast_path"] == 1
+    gt2 = torch.empty_like(pt)
+    D2, _ = g2.eval(pt, grad=gt2)      # captured
+    g2c = gt2.clone()
+    D3, _ = g2.eval(pt, grad=gt2)      # replayed
+    g1.close()
+    g2.close()
+    assert D3 == D2 and torch.equal(g2c, gt2)
+    assert abs(D2 - D1) / abs(D1) <= 1e-8
+    assert float((gt2 - gt1).norm() / gt1.norm()) <= 1e-6

@@ -1,0 +1,110 @@
+"""The z-slab decomposition run by the LIBRARY in two processes: each process
+is one rank (srwcr_options.nranks = 2, rank = k) on the one GPU of the box, the caller-driven
+exchange (srwcr_eval_begin -> statistics sum over gloo -> srwcr_eval_end -> gradient sum
+over gloo) replaces NCCL (nothing here makes one rank's kernels wait on the other's: the
+exchange happens on the host between the library calls).
+
+With slab boundaries on spatial z-cells, each rank runs exactly the work items of the
+single-GPU decomposition that lie in its slab, and the statistics are int64 fixed-point
+sums: the rank partials add up exactly.  Each context computes its whole-volume static
+counts N itself (create time, fp32 / fp64 atomics: equal to rounding, and the NCCL path
+broadcasts rank 0's copy), so D agrees to ~1e-9 here rather than bitwise.
+"""
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# C5-shaped, 8 spatial z-cells of 6 slices: the 2-rank split (24 / 24) falls on a cell boundary
+DIMS = (512, 34, 48)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _rank_main(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_05061_b200 as S
+    import synth
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.config("C5", DIMS)
+    F, M = synth.make_pair("C5", 1, cfg["dims"])
+    g = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], nranks=world, rank=rank)
+    params = synth.make_params(g.params_shape, "small", 1)
+    g.eval_begin(params)
+    p, n = g.stats_buffer()
+    h = torch.from_numpy(_d2h(p, n))
+    dist.all_reduce(h, op=dist.ReduceOp.SUM)
+    _h2d(p, h.numpy())
+    D, grad = g.eval_end()
+    gt = torch.from_numpy(np.ascontiguousarray(grad))
+    dist.all_reduce(gt, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "grad.npy"), gt.numpy())
+        np.save(os.path.join(out_dir, "D.npy"), np.array([D]))
+    g.close()
+    dist.destroy_process_group()
+
+
+def _cudart():
+    import ctypes
+    import glob
+    for cand in ["libcudart.so", *glob.glob("/usr/local/cuda/lib64/libcudart.so*")]:
+        try:
+            return ctypes.CDLL(cand)
+        except OSError:
+            continue
+    raise RuntimeError("libcudart not found")
+
+
+def _d2h(p, n):
+    import ctypes
+    h = np.empty(n, np.float64)
+    assert _cudart().cudaMemcpy(h.ctypes.data_as(ctypes.c_void_p), ctypes.c_void_p(p), ctypes.c_size_t(8 * n), 2) == 0
+    return h
+
+
+def _h2d(p, h):
+    import ctypes
+    h = np.ascontiguousarray(h)
+    assert _cudart().cudaMemcpy(ctypes.c_void_p(p), h.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(h.nbytes), 1) == 0
+
+
+def test_two_rank_library_gloo_exchange():
+    import torch.multiprocessing as mp
+
+    import oracle as O
+    import paper_1804_05061_b200 as S
+    import synth
+    cfg = synth.config("C5", DIMS)
+    F, M = synth.make_pair("C5", 1, cfg["dims"])
+    g1 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"])
+    assert g1.stats()["fast_path"] == 1
+    params = synth.make_params(g1.params_shape, "small", 1)
+    D1, grad1 = g1.eval(params)
+    g1.close()
+    with tempfile.TemporaryDirectory() as td:
+        mp.start_processes(_rank_main, args=(2, _free_port(), td), nprocs=2, join=True, start_method="spawn")
+        D2 = float(np.load(os.path.join(td, "D.npy"))[0])
+        grad2 = np.load(os.path.join(td, "grad.npy")).reshape(grad1.shape)
+    assert abs(D2 - D1) / abs(D1) <= 1e-8, (D2, D1)
+    assert np.linalg.norm(grad2 - grad1) / np.linalg.norm(grad1) <= 1e-6
+    L = cfg["bins"] - 1
+    pb = O.Problem(dims=cfg["dims"], L=L, delta=tuple(c / s for c, s in zip(cfg["control_mm"], cfg["spacing"])),
+                   kcells=cfg["cells"])
+    Do, go = O.eval_moments(pb, O.normalize(F, L), O.normalize(M, L), params)
+    assert abs(D2 - Do) / abs(Do) <= 1e-5
+    assert np.linalg.norm(grad2 - go) / np.linalg.norm(go) <= 1e-4
