@@ -145,6 +145,13 @@ struct srwcr_ctx {
     size_t fsmem2 = 0;
     float fdxz = 1.f;
     std::vector<FItem> h_fitems;
+    // split pass 1: sample half (k_p1w) -> plain m (fMv) -> moment half (k_p1f MODE 2)
+    bool fsplit = false;
+    float *fMv = nullptr;
+    cudaArray_t fMarr = nullptr;            // M as a 2-D layered array (pass 1 textureGather)
+    cudaTextureObject_t ftexM = 0;
+    int fWw = 8, fMinbW = 3;
+    size_t fsmemw = 0;
 };
 
 static srwcr_status fail(srwcr_ctx *c, srwcr_status s, const char *fmt, ...) {
@@ -440,6 +447,26 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
         const int nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
         if (nxn > 32 || it.zlen > FZMAX) return SRWCR_OK;   // not eligible: round-1 passes
     }
+    if (P1_TEX) {   // the layered copy of M (2-D layered limits: 32768 x 32768 x 2048)
+        if (g.nx > 32768 || g.ny > 32768 || g.nz > 2048) return SRWCR_OK;
+        cudaChannelFormatDesc cd = cudaCreateChannelDesc<float>();
+        CK(cudaMalloc3DArray(&c->fMarr, &cd, make_cudaExtent(g.nx, g.ny, g.nz), cudaArrayLayered));
+        cudaMemcpy3DParms cp{};
+        cp.srcPtr = make_cudaPitchedPtr(c->M, sizeof(float) * g.nx, g.nx, g.ny);
+        cp.dstArray = c->fMarr;
+        cp.extent = make_cudaExtent(g.nx, g.ny, g.nz);
+        cp.kind = cudaMemcpyDeviceToDevice;
+        CK(cudaMemcpy3DAsync(&cp, c->stream));
+        cudaResourceDesc rd{};
+        rd.resType = cudaResourceTypeArray;
+        rd.res.array.array = c->fMarr;
+        cudaTextureDesc td{};
+        td.addressMode[0] = td.addressMode[1] = td.addressMode[2] = cudaAddressModeClamp;
+        td.filterMode = cudaFilterModePoint;
+        td.readMode = cudaReadModeElementType;
+        td.normalizedCoords = 0;
+        CK(cudaCreateTextureObject(&c->ftexM, &rd, &td, nullptr));
+    }
     const size_t n = its.size();
     // per item: fixed bins present, binless shift, spatial weight sums
     Item *d_it = nullptr;
@@ -553,6 +580,14 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     c->nfitems = (int)n;
     c->fsmem1 = p1_smem(W, S).total;
     c->h_fitems = fi;
+    // split pass 1 (SRWCR_SPLIT=0/1 overrides the default).  Measured on C5 (c18/c19): the
+    // halves take 0.82 ms (k_p1w) + 0.87 ms (k_p1f MODE 2) against 1.60 ms fused: off
+    c->fsplit = false;
+    if (const char *e = getenv("SRWCR_SPLIT")) c->fsplit = atoi(e) != 0;
+    if (const char *e = getenv("SRWCR_P1W_MINB")) c->fMinbW = atoi(e) == 2 ? 2 : 3;
+    if (const char *e = getenv("SRWCR_P1W_W")) c->fWw = std::min(16, std::max(1, atoi(e)));
+    CK(cudaMalloc(&c->fMv, sizeof(float) * slab));   // (also when fused: SRWCR_SPLIT is re-read per launch)
+    c->fsmemw = p1w_smem(c->fWw).total;
     // pass 2: node window and warps per CTA
     int npmax = 0;
     for (const FItem &f : fi) {
@@ -592,7 +627,13 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             CK(cudaFuncSetAttribute(k_p1f<2, 512>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<2, 384>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<2, 256>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<2, 512, 2>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<2, 384, 2>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<2, 256, 2>, attr, sm));
         } else {
+            CK(cudaFuncSetAttribute(k_p1f<1, 512, 2>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<1, 384, 2>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p1f<1, 256, 2>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 768>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 512>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 384>, attr, sm));
@@ -612,7 +653,8 @@ static FArgs fast_args(srwcr_ctx *c) {
     a.M = c->M; a.phi = c->phi; a.rec = c->frec; a.loff = c->floff; a.lent = c->flent; a.rmask = c->frmask;
     a.items = c->fitems; a.itemw = c->fitemw; a.slotbins = c->fslotbins; a.iflag = c->fiflag; a.shiftc = c->shiftc;
     a.SQi = c->SQi; a.Qi = c->SQi + (size_t)c->R * c->g.B * 2;
-    a.MG = c->MG; a.mgz0 = (int)c->z0;
+    a.MG = c->MG; a.Mv = c->fMv; a.mgz0 = (int)c->z0;
+    a.texM = (unsigned long long)c->ftexM;
     a.S = c->fS; a.W = c->fW; a.i0 = 0;
     a.L1 = p1_smem(c->fW, c->fS);
     a.ablate = 0;
@@ -625,7 +667,34 @@ static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bo
     FArgs a = fast_args(c);
     a.i0 = i0;
     const int n = cnt >= 0 ? cnt : c->nfitems - i0;
-    if (n > 0) {
+    bool split = c->fsplit;
+    if (const char *e = getenv("SRWCR_SPLIT")) split = atoi(e) != 0;   // experiments / the fused-vs-split test
+    if (n > 0 && split) {
+        // sample half, then the moment half (same items)
+        FArgs aw = a;
+        aw.W = c->fWw;
+        aw.L1 = p1w_smem(c->fWw);
+        const int Tw = 32 * c->fWw, T = 32 * c->fW;
+        const size_t smw = c->fsmemw;
+        if (c->fXV == 2) {
+            if (Tw <= 256 && c->fMinbW == 3) k_p1w<2, 256, 3><<<n, Tw, smw, c->stream>>>(aw);
+            else if (Tw <= 256) k_p1w<2, 256, 2><<<n, Tw, smw, c->stream>>>(aw);
+            else k_p1w<2, 512, 1><<<n, Tw, smw, c->stream>>>(aw);
+            CKL();
+            if (T > 384) k_p1f<2, 512, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            else if (T > 256) k_p1f<2, 384, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            else k_p1f<2, 256, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+        } else {
+            if (Tw <= 256 && c->fMinbW == 3) k_p1w<1, 256, 3><<<n, Tw, smw, c->stream>>>(aw);
+            else if (Tw <= 256) k_p1w<1, 256, 2><<<n, Tw, smw, c->stream>>>(aw);
+            else k_p1w<1, 512, 1><<<n, Tw, smw, c->stream>>>(aw);
+            CKL();
+            if (T > 384) k_p1f<1, 512, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            else if (T > 256) k_p1f<1, 384, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            else k_p1f<1, 256, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+        }
+        CKL();
+    } else if (n > 0) {
         const int T = 32 * c->fW;
         if (c->fXV == 2) {
             if (T > 384) k_p1f<2, 512><<<n, T, c->fsmem1, c->stream>>>(a);
@@ -834,6 +903,11 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         auto xr = runs(c->h_sb[0], 0, g.nx, 1 << 30);
         for (auto &r : xr) minw = std::min(minw, r.second);
         c->XV = minw >= 48 ? 2 : 1;
+        // ... and every 64-voxel x-chunk reads at most 32 control x-nodes (the FFD layer
+        // loads are one node per lane): otherwise 32-voxel chunks (delta_x <= ~2.25 voxels)
+        if (c->XV == 2)
+            for (auto &r : runs(c->h_sb[0], 0, g.nx, 64))
+                if (c->h_cb[0][r.first + r.second - 1] + 4 - c->h_cb[0][r.first] > 32) c->XV = 1;
         if (const char *e = getenv("SRWCR_XV")) c->XV = std::min(c->XV, std::max(1, atoi(e)));
         c->XV2 = c->XV;  // pass 2 amortises its per-line gamma/alpha/beta contractions over XV2 x 32 voxels
         if (const char *e = getenv("SRWCR_XV2")) c->XV2 = std::min(c->XV, std::max(1, atoi(e)));
@@ -907,6 +981,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         }
         break;
     }
+    if (npmax == SIZE_MAX)
+        return fail(c, SRWCR_EINVAL, "control lattice too fine along x: a voxel line reads more than 32 control x-nodes");
     build_items(0, g.nz, items_full, xmax);
     // pass 2 has its own (narrower) x-chunks, hence more items: keep its z-marches as
     // long as the load balance allows (fewer FFD-layer loads and retires per voxel)
@@ -1200,7 +1276,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         CK(cudaMemcpy(&c->Z, zb, sizeof(double), cudaMemcpyDeviceToHost));
         cudaFree(zb);
     }
-    if (c->fast) c->launches_per_eval = 7;   // prep, pass 1, stats conversion, combine, pass 2, exact fix, gradient conversion
+    if (c->fast) c->launches_per_eval = c->fsplit ? 8 : 7;   // prep, pass 1 (split: 2 kernels), stats conversion, combine, pass 2, exact fix, gradient conversion
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -1619,13 +1695,15 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     if (c->comm && nccl().ok) nccl().CommDestroy(c->comm);
     if (c->gexec) cudaGraphExecDestroy(c->gexec);
     if (c->cstream) cudaStreamSynchronize(c->cstream);
+    if (c->ftexM) cudaDestroyTextureObject(c->ftexM);
+    if (c->fMarr) cudaFreeArray(c->fMarr);
     for (int i = 0; i < 4; ++i)
         if (c->pev[i]) cudaEventDestroy(c->pev[i]);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma, c->ticket, c->dpart, c->xbeg, c->fitems, c->fitemw, c->fslotbins,
-                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi};
+                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

@@ -98,6 +98,19 @@ template <int XV> __device__ __forceinline__ VF<XV> vlerp(VF<XV> a, VF<XV> b, VF
     return vfma(t, vsub(b, a), a);
 }
 
+// pass 1 gathers the 8 corners of M with 2 textureGather (TLD4) instead of 8 LDG (c20 / c21)
+#ifndef SRWCR_P1_TEX
+#define SRWCR_P1_TEX 0
+#endif
+constexpr bool P1_TEX = SRWCR_P1_TEX != 0;
+__device__ __forceinline__ float4 tex_gather(unsigned long long t, int layer, float x, float y) {
+    float4 r;
+    asm volatile("tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(t), "r"(layer), "f"(x), "f"(y));
+    return r;
+}
+
 // floor(u) as float and as int (|u| < 2^22), full-rate FADD.RM instead of FRND / F2I
 __device__ __forceinline__ float mfloor(float u, int &iu) {
     const float m = __fadd_rd(u, MAGIC);
@@ -107,7 +120,7 @@ __device__ __forceinline__ float mfloor(float u, int &iu) {
 
 // shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
 struct P1Smem {
-    int lt, k, ct, pl, lm, lo, wx, wy, rm, zs, zc, zb, sh, ts, total;
+    int lt, k, ct, pl, lm, lo, wx, wxr, wy, rm, zs, zc, zb, sh, ts, total;
 };
 __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     P1Smem o;
@@ -120,6 +133,7 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     o.lm = take(W * 4 * 4 * 4);          // float LM[W][4 layers][4]
     o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]  the row's line-list offsets
     o.wx = take(64 * 16);                // float4 WX[XV * 32]  the lane voxels' spatial x weights (0: padding)
+    o.wxr = take(64 * 16);               // float4 WXR[XV * 32] the same, rotated: component k = tap (k + lane) & 3
     o.wy = take(W * 16);                 // float4 WY[W]
     o.rm = take(W * 16);                 // uint4 RM[W]
     o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
@@ -136,6 +150,7 @@ struct FArgs {
     Tables t;
     const float *M;
     const float *phi;               // fp32 [3][Gz][Gy][Gx]
+    unsigned long long texM;        // texture object: M as a 2-D layered array (layer = z), point sampling
     const unsigned *rec;            // [slab voxels] slot << 24 | round(h_hi 2^23)
     const unsigned *loff;           // [lines + 1] offsets of the per-line entry lists
     const unsigned *lent;           // entries: slot | n_lo << 8 | n_hi << 16 (adds per entry)
@@ -148,6 +163,7 @@ struct FArgs {
     unsigned long long *SQi;        // [R][B][2] int64, units 2^-16 (shifted, as SQ)
     unsigned long long *Qi;         // [R] binless second moments, int64 units 2^-16
     float4 *MG;                     // pass 1 out: (m, dM/dy) per slab voxel, m < 0 flags exact
+    float *Mv;                      // split pass 1: plain m per slab voxel (sample half -> moment half)
     int mgz0;
     int S;                          // table stride in slots (max slots + binless + dummy)
     int W;                          // warps per CTA
@@ -335,7 +351,6 @@ struct P1Lane {
     // per-lane constants of the item
     int xv[XV], relx[XV];
     bool valid[XV];
-    VF<XV> wr[4];        // rotated spatial x weights: entry k holds tap (k + q) & 3, q = lane & 3
     unsigned lts[4];     // shared address of the rotated tap-k entry pair of slot 0 in the warp's line table
 };
 
@@ -361,9 +376,14 @@ template <int XV> __device__ __forceinline__ VF<XV> vfloor_rd(VF<XV> u) {   // u
     return r;
 }
 
-template <int XV, bool INT>
+// MODE 0: the whole pass (fused); MODE 1: the sample half only (a3, a4: FFD, gathers,
+// trilinear value and gradient, exact-path flags -> MG and the plain m array Mv); MODE 2:
+// the moment half only (a5, a6: m from Mv, the records of F -> line tables / binless).
+// Both halves run the same per-voxel arithmetic as MODE 0, so the results are bitwise equal.
+template <int XV, bool INT, int MODE = 0>
 __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1Smem &L, unsigned char *smem, int y,
                                        int warp, int lane, const P1Lane<XV, INT> &pl) {
+    constexpr bool SAMPLE = MODE != 2, MOMENTS = MODE != 1;
     const Geo &g = a.g;
     const int S = a.S, ns = it.nslots, dummy = it.nslots + 1;
     int *LTw = reinterpret_cast<int *>(smem + L.lt) + warp * S * 9;
@@ -384,7 +404,8 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     const int z0 = it.z0, zlen = it.zlen;
     const long long line0 = (long long)it.line_off + (long long)r * zlen;
     // the row's line-list offsets, staged once per row
-    for (int k = lane; k <= zlen; k += 32) LOw[k] = __ldg(a.loff + line0 + k);
+    if constexpr (MOMENTS)
+        for (int k = lane; k <= zlen; k += 32) LOw[k] = __ldg(a.loff + line0 + k);
 
     // ---- FFD layers (a3): U[n][c] = sum_{l,m} cwx_l cwy_m phi[c][gz_n][cby+m][cbx+l]
     VF<XV> U[4][3];
@@ -428,12 +449,14 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         __syncwarp();
     };
     int gzl = ZB[0];
+    if constexpr (SAMPLE) {
 #pragma unroll
-    for (int n = 0; n < 4; ++n) load_layer(gzl + n, U[n], (gzl + n) & 3);
+        for (int n = 0; n < 4; ++n) load_layer(gzl + n, U[n], (gzl + n) & 3);
+    }
     // rounding bound of u (any component): |u32 - u64| <= gamma_16 max_taps |phi| ~ 9.5e-7 max|phi|
     // (16 roundings on any path: fp32 phi and 3 weights, 3 x 4 fma levels; weights >= 0 sum to 1);
     // 2e-6 of the max over the line's 4 active layers (all x-nodes of the item, 4 y-taps, 3 comps)
-    float tol = 2e-6f * fmaxf(fmaxf(LMw[0], LMw[1]), fmaxf(LMw[2], LMw[3]));
+    float tol = SAMPLE ? 2e-6f * fmaxf(fmaxf(LMw[0], LMw[1]), fmaxf(LMw[2], LMw[3])) : 0.f;
 
     // ---- binless accumulators (per lane, over the z-march): 4 z-taps x {q', g1 - cI}
     VF<XV> accq[4], acca[4];
@@ -447,8 +470,12 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     // ---- software pipeline: the records, gathers and coordinate flags of slice z+1 are in
     // flight while slice z is processed
     unsigned recn[XV];
+    float mvn[XV];   // MODE 2: m of slice z+1
 #pragma unroll
-    for (int v = 0; v < XV; ++v) recn[v] = __ldg(a.rec + (vb + 32 * v));
+    for (int v = 0; v < XV; ++v) {
+        recn[v] = MOMENTS ? __ldg(a.rec + (vb + 32 * v)) : 0u;
+        mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + 32 * v)) : 0.f;
+    }
     float C[XV][8];
     VF<XV> T[3];
     int fl[XV];   // bit 0-2: clamped x, y, z (reading c2); bit 3: near an integer (exact path); bit 4: at rest
@@ -496,20 +523,30 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 }
             }
             fl[v] = f;
-            const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[2] * nxy + ci[1] * nx + ci[0];
-            const float *b0 = a.M + o0, *b1 = a.M + (o0 + nx), *b2 = a.M + (o0 + dzo), *b3 = a.M + (o0 + dzo + nx);
-            C[v][0] = __ldg(b0); C[v][1] = __ldg(b0 + 1);
-            C[v][2] = __ldg(b1); C[v][3] = __ldg(b1 + 1);
-            C[v][4] = __ldg(b2); C[v][5] = __ldg(b2 + 1);
-            C[v][6] = __ldg(b3); C[v][7] = __ldg(b3 + 1);
+            if constexpr (P1_TEX) {
+                // two 2x2 footprints (textureGather of the layered copy of M, layer = z): the
+                // footprint around the texel corner (cx + 1, cy + 1) is exactly texels cx..cx+1,
+                // cy..cy+1 (integer coordinates: no filtering, no rounding of the position)
+                const float fx = (float)(ci[0] + 1), fy = (float)(ci[1] + 1);
+                const float4 q0 = tex_gather(a.texM, ci[2], fx, fy), q1 = tex_gather(a.texM, ci[2] + 1, fx, fy);
+                C[v][0] = q0.w; C[v][1] = q0.z; C[v][2] = q0.x; C[v][3] = q0.y;
+                C[v][4] = q1.w; C[v][5] = q1.z; C[v][6] = q1.x; C[v][7] = q1.y;
+            } else {
+                const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[2] * nxy + ci[1] * nx + ci[0];
+                const float *b0 = a.M + o0, *b1 = a.M + (o0 + nx), *b2 = a.M + (o0 + dzo), *b3 = a.M + (o0 + dzo + nx);
+                C[v][0] = __ldg(b0); C[v][1] = __ldg(b0 + 1);
+                C[v][2] = __ldg(b1); C[v][3] = __ldg(b1 + 1);
+                C[v][4] = __ldg(b2); C[v][5] = __ldg(b2 + 1);
+                C[v][6] = __ldg(b3); C[v][7] = __ldg(b3 + 1);
+            }
         }
     };
-    gather(z0);
+    if constexpr (SAMPLE) gather(z0);
     // first list entries of the next line, prefetched one slice ahead (lane's passes 0, 1)
     __syncwarp();
     // the next line's list entries, one per lane (a line touches <= 32 slots but rarely)
-    unsigned entn;
-    {
+    unsigned entn = 0u;
+    if constexpr (MOMENTS) {
         const unsigned o = LOw[0], o1 = LOw[1];
         entn = o + lane < o1 ? __ldg(a.lent + o + lane) : 0u;
     }
@@ -521,30 +558,39 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         const int izn = min(iz + 1, zlen - 1);   // the last slice re-issues its own loads (no branch)
         // ---- this slice's inputs
         unsigned rc[XV];
+        float mvc[XV];
 #pragma unroll
         for (int v = 0; v < XV; ++v) {
             rc[v] = recn[v];
-            recn[v] = __ldg(a.rec + (vb + izn * nxy + 32 * v));
+            mvc[v] = mvn[v];
+            if constexpr (MOMENTS) recn[v] = __ldg(a.rec + (vb + izn * nxy + 32 * v));
+            if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + 32 * v));
         }
-        VF<XV> c000, c100, c010, c110, c001, c101, c011, c111;
-#pragma unroll
-        for (int v = 0; v < XV; ++v) {
-            c000.v[v] = C[v][0]; c100.v[v] = C[v][1]; c010.v[v] = C[v][2]; c110.v[v] = C[v][3];
-            c001.v[v] = C[v][4]; c101.v[v] = C[v][5]; c011.v[v] = C[v][6]; c111.v[v] = C[v][7];
-        }
-        const VF<XV> tx = T[0], ty = T[1], tz = T[2];
         int flc[XV];
+        VF<XV> m, dgx, dgy, dgz;
+        if constexpr (SAMPLE) {
+            VF<XV> c000, c100, c010, c110, c001, c101, c011, c111;
 #pragma unroll
-        for (int v = 0; v < XV; ++v) flc[v] = fl[v];
-        // ---- trilinear value and gradient (a4, nested lerps; readings c1, c3)
-        const VF<XV> d00 = vsub(c100, c000), d10 = vsub(c110, c010), d01 = vsub(c101, c001), d11 = vsub(c111, c011);
-        const VF<XV> e00 = vfma(tx, d00, c000), e10 = vfma(tx, d10, c010);
-        const VF<XV> e01 = vfma(tx, d01, c001), e11 = vfma(tx, d11, c011);
-        const VF<XV> f0 = vlerp(e00, e10, ty), f1 = vlerp(e01, e11, ty);
-        const VF<XV> m = vlerp(f0, f1, tz);
-        VF<XV> dgx = vlerp(vlerp(d00, d10, ty), vlerp(d01, d11, ty), tz);
-        VF<XV> dgy = vlerp(vsub(e10, e00), vsub(e11, e01), tz);
-        VF<XV> dgz = vsub(f1, f0);
+            for (int v = 0; v < XV; ++v) {
+                c000.v[v] = C[v][0]; c100.v[v] = C[v][1]; c010.v[v] = C[v][2]; c110.v[v] = C[v][3];
+                c001.v[v] = C[v][4]; c101.v[v] = C[v][5]; c011.v[v] = C[v][6]; c111.v[v] = C[v][7];
+            }
+            const VF<XV> tx = T[0], ty = T[1], tz = T[2];
+#pragma unroll
+            for (int v = 0; v < XV; ++v) flc[v] = fl[v];
+            // ---- trilinear value and gradient (a4, nested lerps; readings c1, c3)
+            const VF<XV> d00 = vsub(c100, c000), d10 = vsub(c110, c010), d01 = vsub(c101, c001), d11 = vsub(c111, c011);
+            const VF<XV> e00 = vfma(tx, d00, c000), e10 = vfma(tx, d10, c010);
+            const VF<XV> e01 = vfma(tx, d01, c001), e11 = vfma(tx, d11, c011);
+            const VF<XV> f0 = vlerp(e00, e10, ty), f1 = vlerp(e01, e11, ty);
+            m = vlerp(f0, f1, tz);
+            dgx = vlerp(vlerp(d00, d10, ty), vlerp(d01, d11, ty), tz);
+            dgy = vlerp(vsub(e10, e00), vsub(e11, e01), tz);
+            dgz = vsub(f1, f0);
+        } else {
+#pragma unroll
+            for (int v = 0; v < XV; ++v) m.v[v] = mvc[v];
+        }
         // ---- Parzen moments of m (a5, Eq 5): n = min(floor m, L-1), f = m - n
         const VF<XV> mfm = vfloor_rd(m);
         VF<XV> nf;
@@ -552,17 +598,19 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         for (int v = 0; v < XV; ++v) nf.v[v] = fminf(mfm.v[v] - MAGIC, Lm1);
         const VF<XV> fm = vsub(m, nf);
         const VF<XV> omf = vsub(vone, fm);
-        VF<XV> sfold;
-#pragma unroll
-        for (int v = 0; v < XV; ++v) sfold.v[v] = fm.v[v] < 0.5f ? fm.v[v] : omf.v[v];
-        const VF<XV> wq = vmul(sfold, vfma(vsplat<XV>(1.8f), sfold, vsplat<XV>(0.1f)));   // s (0.1 + 1.8 s)
-        const VF<XV> owq = vsub(vone, wq);
         VF<XV> w1, w1l;
+        if constexpr (MOMENTS) {
+            VF<XV> sfold;
 #pragma unroll
-        for (int v = 0; v < XV; ++v) {
-            const bool lowh = fm.v[v] < 0.5f;
-            w1.v[v] = lowh ? wq.v[v] : owq.v[v];
-            w1l.v[v] = lowh ? owq.v[v] : wq.v[v];
+            for (int v = 0; v < XV; ++v) sfold.v[v] = fm.v[v] < 0.5f ? fm.v[v] : omf.v[v];
+            const VF<XV> wq = vmul(sfold, vfma(vsplat<XV>(1.8f), sfold, vsplat<XV>(0.1f)));   // s (0.1 + 1.8 s)
+            const VF<XV> owq = vsub(vone, wq);
+#pragma unroll
+            for (int v = 0; v < XV; ++v) {
+                const bool lowh = fm.v[v] < 0.5f;
+                w1.v[v] = lowh ? wq.v[v] : owq.v[v];
+                w1l.v[v] = lowh ? owq.v[v] : wq.v[v];
+            }
         }
         // (g1 itself is never formed: n + w1 in fp32 would round w1 to the ulp of n; the shifted
         // moments are (n - c) + w1 with the small difference first)
@@ -573,11 +621,11 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         int kink[XV], anyk = 0;
 #pragma unroll
         for (int v = 0; v < XV; ++v) {
-            ex[v] = (flc[v] >> 3) & 1;
-            kink[v] = (int)(fminf(fm.v[v], omf.v[v]) < 5e-5f) & (int)((flc[v] & 24) == 0);
+            ex[v] = SAMPLE ? (flc[v] >> 3) & 1 : 0;
+            kink[v] = SAMPLE ? (int)(fminf(fm.v[v], omf.v[v]) < 5e-5f) & (int)((flc[v] & 24) == 0) : 0;
             anyk |= kink[v];
         }
-        if (__any_sync(FULL, anyk)) {   // rare: the flatness test (8 equal corners: m exact)
+        if (SAMPLE && __any_sync(FULL, anyk)) {   // rare: the flatness test (8 equal corners: m exact)
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 const float c0 = C[v][0];
@@ -588,7 +636,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         }
         // ---- next slice: slide the layer window, issue its gathers (the last slice re-issues);
         // slice z's corners are dead from here on: the loads of z+1 overlap the rest of slice z
-        {
+        if constexpr (SAMPLE) {
             const int bz1 = ZB[izn];
             if (gzl < bz1) {
                 while (gzl < bz1) {
@@ -606,23 +654,27 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         // ---- record: slot and Parzen weights of F (static); the shifted first moment A
         int slot[XV];
         VF<XV> hhi, A;
+        float lsc = 1.f, lisc = 1.f;
+        if constexpr (MOMENTS) {
 #pragma unroll
-        for (int v = 0; v < XV; ++v) {
-            slot[v] = pl.valid[v] ? (int)(rc[v] >> 24) : dummy;
-            hhi.v[v] = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu));
-            A.v[v] = SH[slot[v]];
+            for (int v = 0; v < XV; ++v) {
+                slot[v] = pl.valid[v] ? (int)(rc[v] >> 24) : dummy;
+                hhi.v[v] = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu));
+                A.v[v] = SH[slot[v]];
+            }
+            hhi = vsub(hhi, vone);
+            A = vadd(vsub(nf, A), w1);                                // g1 - c_a0 = (n - c_a0) + w1
+            // line fixed-point scale from the line's max |A|: one add (w <= 2/3) stays below 2^22
+            // (exact magic-number conversion), a line entry's sum below 2^28
+            float am = fabsf(A.v[0]);
+#pragma unroll
+            for (int v = 1; v < XV; ++v) am = fmaxf(am, fabsf(A.v[v]));
+            const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(am)) >> 23);
+            const int ksc = min(148 - EA, 126);
+            lsc = __int_as_float((ksc + 127) << 23);
+            lisc = __int_as_float((127 - ksc) << 23);
         }
-        hhi = vsub(hhi, vone);
-        A = vadd(vsub(nf, A), w1);                                // g1 - c_a0 = (n - c_a0) + w1
-        // line fixed-point scale from the line's max |A|: one add (w <= 2/3) stays below 2^22
-        // (exact magic-number conversion), a line entry's sum below 2^28
-        float am = fabsf(A.v[0]);
-#pragma unroll
-        for (int v = 1; v < XV; ++v) am = fmaxf(am, fabsf(A.v[v]));
-        const int EA = (int)(__reduce_max_sync(FULL, __float_as_uint(am)) >> 23);
-        const int ksc = min(148 - EA, 126);
-        const float lsc = __int_as_float((ksc + 127) << 23), lisc = __int_as_float((127 - ksc) << 23);
-        if (!INT) {
+        if (SAMPLE && !INT) {
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 dgx.v[v] = (flc[v] & 1) ? 0.f : dgx.v[v];
@@ -630,10 +682,15 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 dgz.v[v] = (flc[v] & 4) ? 0.f : dgz.v[v];
             }
         }
+        if constexpr (SAMPLE) {
 #pragma unroll
-        for (int v = 0; v < XV; ++v)   // (a padding lane samples its clamped neighbour: identical values)
-            if (!(a.ablate & 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
-                       make_float4(ex[v] ? -1.0f - m.v[v] : m.v[v], dgx.v[v], dgy.v[v], dgz.v[v]));
+            for (int v = 0; v < XV; ++v) {   // (a padding lane samples its clamped neighbour: identical values)
+                if (!(a.ablate & 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
+                           make_float4(ex[v] ? -1.0f - m.v[v] : m.v[v], dgx.v[v], dgy.v[v], dgz.v[v]));
+                if (MODE == 1) __stcs(a.Mv + (vb + iz * nxy + 32 * v), m.v[v]);
+            }
+        }
+        if constexpr (!MOMENTS) continue;
         // ---- binless (z-taps folded in registers)
         {
             const float4 wz = ZS[iz];
@@ -705,9 +762,16 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                     vb.v[v] = chA ? lov.v[v] : hiv.v[v];
                 }
                 const int db = chA ? -4 : 4;
+                // rotated spatial x weights (shared, per lane): entry k holds tap (k + q) & 3, q = lane & 3
+                VF<XV> wr[4];
+#pragma unroll
+                for (int v = 0; v < XV; ++v) {
+                    const float4 w = reinterpret_cast<const float4 *>(smem + L.wxr)[v * 32 + lane];
+                    wr[0].v[v] = w.x; wr[1].v[v] = w.y; wr[2].v[v] = w.z; wr[3].v[v] = w.w;
+                }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const VF<XV> xa = vadd(vfma(va, pl.wr[k], dith), vmagic), xb = vadd(vfma(vb, pl.wr[k], dith), vmagic);
+                    const VF<XV> xa = vadd(vfma(va, wr[k], dith), vmagic), xb = vadd(vfma(vb, wr[k], dith), vmagic);
 #pragma unroll
                     for (int v = 0; v < XV; ++v) {
                         const unsigned ad = pl.lts[k] + (unsigned)slot[v] * 36u;
@@ -753,17 +817,16 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         __syncwarp();
     }
     // ---- row end: binless -> K[ns]; lane j of the reduction holds value j = (l, ch, n)
-    {
+    if constexpr (MOMENTS) {
         float vals[32];
-        const int q4 = lane & 3;
-        // un-rotate the x weights: true tap l is rotated index (l - q) & 3
+        float4 wxl[XV];   // the lane voxels' spatial x weights (unrotated; 0 for padding lanes)
+#pragma unroll
+        for (int v = 0; v < XV; ++v) wxl[v] = reinterpret_cast<const float4 *>(smem + L.wx)[v * 32 + lane];
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
-            const int k = (l - q4) & 3;
             VF<XV> wl;
 #pragma unroll
-            for (int v = 0; v < XV; ++v)
-                wl.v[v] = k == 0 ? pl.wr[0].v[v] : k == 1 ? pl.wr[1].v[v] : k == 2 ? pl.wr[2].v[v] : pl.wr[3].v[v];
+            for (int v = 0; v < XV; ++v) wl.v[v] = f4(wxl[v], l);
 #pragma unroll
             for (int n = 0; n < 4; ++n) {
                 float sq = 0.f, sa = 0.f;
@@ -791,7 +854,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     }
 }
 
-template <int XV, int MAXT>
+template <int XV, int MAXT, int MODE = 0>
 __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int W = a.W, S = a.S;
@@ -821,8 +884,12 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
         ZB[i] = a.t.cb[2][it.z0 + i];
     }
     for (int s = threadIdx.x; s < S; s += blockDim.x) SH[s] = s < ns ? a.shiftc[a.slotbins[it.slot_off + s]] : 0.f;
-    for (int i = threadIdx.x; i < 32 * XV; i += blockDim.x)
-        reinterpret_cast<float4 *>(smem + L.wx)[i] = i < it.xlen ? a.t.sw[0][it.x0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int i = threadIdx.x; i < 32 * XV; i += blockDim.x) {
+        const float4 w = i < it.xlen ? a.t.sw[0][it.x0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        reinterpret_cast<float4 *>(smem + L.wx)[i] = w;
+        const int q = i & 3;   // the lane's rotation (lane = i mod 32)
+        reinterpret_cast<float4 *>(smem + L.wxr)[i] = make_float4(f4(w, q), f4(w, (q + 1) & 3), f4(w, (q + 2) & 3), f4(w, (q + 3) & 3));
+    }
 
     // per-lane constants
     const int q4 = lane & 3;
@@ -839,8 +906,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int l = (k + q4) & 3;
-#pragma unroll
-            for (int v = 0; v < XV; ++v) pl.wr[k].v[v] = pl.valid[v] ? f4(a.t.sw[0][pl.xv[v]], l) : 0.f;
             pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * 9) + 8u * (unsigned)l + 4u * ((lane >> 2) & 1);
         }
     };
@@ -858,11 +923,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
             if (interior) {
                 P1Lane<XV, true> pl;
                 setup(pl);
-                p1_row<XV, true>(a, it, L, smem, y, warp, lane, pl);
+                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl);
+            } else if (MODE == 2) {   // (the moment half has no clamping: one variant)
+                P1Lane<XV, true> pl;
+                setup(pl);
+                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl);
             } else {
                 P1Lane<XV, false> pl;
                 setup(pl);
-                p1_row<XV, false>(a, it, L, smem, y, warp, lane, pl);
+                p1_row<XV, false, MODE>(a, it, L, smem, y, warp, lane, pl);
             }
         }
         __syncthreads();
@@ -937,6 +1006,59 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
     }
 }
 
+// The sample half of a split pass 1 (MODE 1): same items, rows dealt to the warps with no
+// CTA barrier in the loop and only the FFD / z-weight shared state, so the kernel runs at
+// MINB CTAs per SM (more resident warps to cover the gathers' latency than the fused pass).
+__host__ __device__ inline P1Smem p1w_smem(int W) {
+    P1Smem o{};
+    int off = 0;
+    auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
+    o.pl = take(W * 32 * 16);
+    o.lm = take(W * 4 * 4 * 4);
+    o.zc = take(FZMAX * 16);
+    o.zb = take(FZMAX * 4);
+    o.total = off;
+    return o;
+}
+
+template <int XV, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) k_p1w(FArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int W = a.W;
+    const P1Smem &L = a.L1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int ii = a.i0 + blockIdx.x;
+    const FItem it = a.items[ii];
+    float4 *ZC = reinterpret_cast<float4 *>(smem + L.zc);
+    int *ZB = reinterpret_cast<int *>(smem + L.zb);
+    for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {
+        ZC[i] = a.t.cw[2][it.z0 + i];
+        ZB[i] = a.t.cb[2][it.z0 + i];
+    }
+    const int xn0 = a.t.cb[0][it.x0];
+    const bool interior = a.iflag[ii] != 0;
+    auto setup = [&](auto &pl) {
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            pl.valid[v] = lane + 32 * v < it.xlen;
+            pl.xv[v] = pl.valid[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
+            pl.relx[v] = a.t.cb[0][pl.xv[v]] - xn0;
+        }
+    };
+    __syncthreads();
+    for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
+        if (interior) {
+            P1Lane<XV, true> pl;
+            setup(pl);
+            p1_row<XV, true, 1>(a, it, L, smem, y, warp, lane, pl);
+        } else {
+            P1Lane<XV, false> pl;
+            setup(pl);
+            p1_row<XV, false, 1>(a, it, L, smem, y, warp, lane, pl);
+        }
+    }
+}
+
 }  // namespace srwcr
 
 namespace srwcr {
@@ -956,7 +1078,7 @@ namespace srwcr {
 // y-contracted into the CTA node window (exact int32 (hi, lo) pairs in units 2^-k, k from the
 // combine's bound), flushed once per item into the int64 global gradient: deterministic.
 struct P2Smem {
-    int gam, ab, gy, gz, rb, nph, npl, lo, zc, zb, zs, cx, total;
+    int gam, ab, gy, gz, rb, nph, npl, lo, zc, zb, zs, cx, ws, cr, total;
 };
 __host__ __device__ inline P2Smem p2_smem(int W, int S, int npn) {
     P2Smem o;
@@ -974,6 +1096,8 @@ __host__ __device__ inline P2Smem p2_smem(int W, int S, int npn) {
     o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
     o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
     o.cx = take(32 * 4);                 // int    CX[32] adds per x-node of a retire (magic offsets)
+    o.ws = take(64 * 16);                // float4 WS[XV * 32] the lane voxels' spatial x weights (0: padding)
+    o.cr = take(64 * 16);                // float4 CR[XV * 32] rotated control x weights: component k = tap (k + lane) & 3
     o.total = off;
     return o;
 }
@@ -995,8 +1119,6 @@ template <int XV>
 struct P2Lane {
     int xv[XV], relx[XV];
     bool valid[XV];
-    VF<XV> ws[4];        // spatial x weights (tap l)
-    VF<XV> cr[4];        // rotated control x weights: entry k holds tap (k + q) & 3
 };
 
 template <int XV>
@@ -1018,6 +1140,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
     const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
     const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
     const int *CX = reinterpret_cast<const int *>(smem + L.cx);
+    const float4 *WS = reinterpret_cast<const float4 *>(smem + L.ws);
+    const float4 *CR = reinterpret_cast<const float4 *>(smem + L.cr);
 
     const int r = y - it.y0;
     const int cby = a.t.cb[1][y];
@@ -1063,6 +1187,9 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
     // retire layer gzr with adjoints R (Z dD/dphi partials of this row): x-contract into RB
     // (int32, warp exponent), then y-contract into the node window (exact (hi, lo) pairs)
     auto retire = [&](int gzr, const VF<XV>(&R)[3]) {
+        float4 crv[XV];
+#pragma unroll
+        for (int v = 0; v < XV; ++v) crv[v] = CR[v * 32 + lane];
         float mx = 0.f;
 #pragma unroll
         for (int c = 0; c < 3; ++c)
@@ -1078,7 +1205,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const int nd = pl.relx[v] + ((k + q4) & 3);
-                const float w = pl.cr[k].v[v];
+                const float w = f4(crv[v], k);
                 red_shared(RBw + nd, __float_as_int(fmaf(w, R0, MAGIC)));
                 red_shared(RBw + 32 + nd, __float_as_int(fmaf(w, R1, MAGIC)));
                 red_shared(RBw + 64 + nd, __float_as_int(fmaf(w, R2, MAGIC)));
@@ -1207,7 +1334,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             const float g1p = integral ? 0.1f : (fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f));
             const float c2 = integral ? 2.0f * m : fmaf(2.0f, nf, 1.0f);
             const float4 G0 = GZc[slot * 2], G1 = GZc[slot * 2 + 1], AY = GZc[ns * 2], BY = GZc[ns * 2 + 1];
-            const float w0 = pl.ws[0].v[v], w1 = pl.ws[1].v[v], w2 = pl.ws[2].v[v], w3 = pl.ws[3].v[v];
+            const float4 wsv = WS[v * 32 + lane];
+            const float w0 = wsv.x, w1 = wsv.y, w2 = wsv.z, w3 = wsv.w;
             const float At = fmaf(w3, AY.w, fmaf(w2, AY.z, fmaf(w1, AY.y, w0 * AY.x)));
             const float Bt = fmaf(w3, BY.w, fmaf(w2, BY.z, fmaf(w1, BY.y, w0 * BY.x)));
             const float g0 = fmaf(w3, G0.w, fmaf(w2, G0.z, fmaf(w1, G0.y, w0 * G0.x)));
@@ -1302,13 +1430,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_p2f(F2Args A2) {
         pl.xv[v] = pl.valid[v] ? it.x0 + lane + 32 * v : it.x0 + it.xlen - 1;
         pl.relx[v] = a.t.cb[0][pl.xv[v]] - xn0;
     }
-#pragma unroll
-    for (int l = 0; l < 4; ++l)
-#pragma unroll
-        for (int v = 0; v < XV; ++v) {
-            pl.ws[l].v[v] = pl.valid[v] ? f4(a.t.sw[0][pl.xv[v]], l) : 0.f;
-            pl.cr[l].v[v] = pl.valid[v] ? f4(a.t.cw[0][pl.xv[v]], (l + q4) & 3) : 0.f;
-        }
+    (void)q4;
+    for (int i = threadIdx.x; i < 32 * XV; i += blockDim.x) {
+        const bool ok = i < it.xlen;
+        const float4 w = ok ? a.t.sw[0][it.x0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 c = ok ? a.t.cw[0][it.x0 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const int q = i & 3;   // the lane's rotation (lane = i mod 32)
+        reinterpret_cast<float4 *>(smem + L.ws)[i] = w;
+        reinterpret_cast<float4 *>(smem + L.cr)[i] = make_float4(f4(c, q), f4(c, (q + 1) & 3), f4(c, (q + 2) & 3), f4(c, (q + 3) & 3));
+    }
     __syncthreads();
     for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W)
         p2_row<XV>(A2, it, L, smem, y, warp, lane, pl, gunit, zn0, yn0, nxn, nyn);

@@ -38,3 +38,13 @@ def rel(a, b):
 
 def rel_l2(a, b):
     return float(np.linalg.norm(np.asarray(a) - np.asarray(b)) / max(np.linalg.norm(b), 1e-300))
+
+
+G_COMP = 1e-3   # per-component gradient bound: max |g - g_o| <= 1e-3 max |g_o|
+
+
+def comp(a, b):
+    """max-norm gradient error relative to the oracle gradient's max (catches a localised
+    error on boundary / halo nodes that a relative L2 can hide)."""
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))

@@ -161,3 +161,22 @@ def test_fast_path_nccl_single_rank_graph():
     assert D3 == D2 and torch.equal(g2c, gt2)
     assert abs(D2 - D1) / abs(D1) <= 1e-8
     assert float((gt2 - gt1).norm() / gt1.norm()) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["C3", "C5"])
+def test_split_pass1_bitwise_equals_fused(name, monkeypatch):
+    """Pass 1 split into its sample half (k_p1w: FFD, gathers, trilinear, exact flags -> MG
+    and m) and its moment half (k_p1f MODE 2: m -> line tables) runs the same per-voxel
+    arithmetic as the fused kernel: bitwise-equal statistics, D and gradient (one context;
+    SRWCR_SPLIT is read at each launch)."""
+    g, pb, Fn, Mn, params = _case(name, 1, "small")
+    res = []
+    for split in ("0", "1", "0"):
+        monkeypatch.setenv("SRWCR_SPLIT", split)
+        D, grad = g.eval(params)
+        res.append((D, grad, g.debug_dump("SQ"), g.debug_dump("warped")))
+    g.close()
+    for r in res[1:]:
+        assert r[0] == res[0][0]
+        for k in (1, 2, 3):
+            assert np.array_equal(r[k], res[0][k])

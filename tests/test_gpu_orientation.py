@@ -7,7 +7,7 @@ import pytest
 import oracle as O
 import synth
 import paper_1804_05061_b200 as S
-from gpu_common import problem, rel, rel_l2
+from gpu_common import problem, rel, rel_l2, comp, G_COMP
 
 pytestmark = pytest.mark.gpu
 
@@ -27,6 +27,7 @@ def test_orientation1_value_and_gradient(name, bins, kind):
     assert rel(D, Do) <= D_TOL, (D, Do)
     if np.linalg.norm(go) > 0:
         assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+        assert comp(grad, go) <= G_COMP, comp(grad, go)
     g.close()
 
 

@@ -8,7 +8,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from gpu_common import REDUCED, problem, rel, rel_l2
+from gpu_common import REDUCED, problem, rel, rel_l2, comp, G_COMP
 
 pytestmark = pytest.mark.gpu
 
@@ -31,6 +31,7 @@ def test_value_and_gradient(name, kind):
     assert rel(D, Do) <= D_TOL, (D, Do)
     if np.linalg.norm(go) > 0:
         assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+        assert comp(grad, go) <= G_COMP, comp(grad, go)
     g.close()
 
 
@@ -42,6 +43,7 @@ def test_more_seeds(name, seed):
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     assert rel(D, Do) <= D_TOL
     assert rel_l2(grad, go) <= G_TOL
+    assert comp(grad, go) <= G_COMP, comp(grad, go)
     g.close()
 
 
@@ -183,6 +185,7 @@ def test_exact_path_voxels_and_scan_fallback(monkeypatch):
     assert rel_l2(g2r, g1) <= 1e-5
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     assert rel_l2(g2r, go) <= G_TOL
+    assert comp(g2r, go) <= G_COMP, comp(g2r, go)
 
 
 def test_nccl_exchange_path_single_rank():
@@ -231,6 +234,7 @@ def test_fine_spatial_lattice(orientation):
     assert pb.nregions == 5440
     assert rel(D, Do) <= D_TOL
     assert rel_l2(grad, go) <= G_TOL
+    assert comp(grad, go) <= G_COMP, comp(grad, go)
     g.close()
 
 
@@ -261,6 +265,7 @@ def test_edge_geometries(dims, L, delta, kcells, orientation):
     assert rel(D, Do) <= D_TOL, (D, Do)
     if np.linalg.norm(go) > 1e-12:
         assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+        assert comp(grad, go) <= G_COMP, comp(grad, go)
     g.close()
 
 
@@ -330,6 +335,7 @@ def test_pipelined_host_buffers_match_device_path(monkeypatch, xcap, orientation
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     assert rel(D1, Do) <= D_TOL
     assert rel_l2(hg.numpy(), go) <= G_TOL
+    assert comp(hg.numpy(), go) <= G_COMP, comp(hg.numpy(), go)
 
 
 def test_debug_dump_statistics_match_oracle_moments():

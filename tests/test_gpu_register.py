@@ -121,3 +121,37 @@ def test_register_argument_errors():
     with pytest.raises(TypeError):
         g.register(None, bogus=1)
     g.close()
+
+
+def _oracle_iterates(pb, Fn, Mn, x0, w_p, k):
+    from oracle.lbfgs import lbfgs
+
+    def fun(x):
+        D, gD = O.eval_moments(pb, Fn, Mn, x)
+        E, gE = O.bending(pb, x)
+        return D + w_p * E, gD + w_p * gE
+    _, _, its = lbfgs(fun, x0, max_iter=k, stable_window=1000)
+    return its
+
+
+@pytest.mark.parametrize("name,dims,k", [("C1", None, 6), ("C5", (512, 66, 42), 3)])
+def test_register_iterates_match_oracle_lbfgs(name, dims, k):
+    """F1 against an independent optimizer: the fp64 CPU L-BFGS of reading c20
+    (oracle/lbfgs.py) driven by the oracle's D + w_p C_p.  After each of the first k
+    iterations srwcr_register (run with max_iter = 1..k from the same start) has taken the
+    same line-search decisions (equal cost-evaluation counts) and reached the same iterate
+    and cost within what the value / gradient parity allows.  C5 at this size runs the
+    fast passes."""
+    w_p = 0.1
+    g, pb, Fn, Mn, params = problem(name, 1, dims=dims)
+    x0 = 0.5 * params
+    its = _oracle_iterates(pb, Fn, Mn, x0, w_p, k)
+    assert len(its) == k
+    for j in range(1, k + 1):
+        x, rep = g.register(x0.copy(), w_p=w_p, max_iter=j, stable_window=1000)
+        xo, fo, _, evo = its[j - 1]
+        assert rep["iterations"] == j
+        assert rep["evaluations"] == evo, (j, rep["evaluations"], evo)
+        assert rel(rep["final_cost"], fo) <= 1e-5, (j, rep["final_cost"], fo)
+        assert rel_l2(x - x0, xo - x0) <= 1e-3, (j, rel_l2(x - x0, xo - x0))
+    g.close()

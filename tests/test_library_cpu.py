@@ -3,11 +3,12 @@
 * libsrwcr.so builds for sm_100a, loads without a GPU, and exports every function
   declared in include/srwcr.h (no compute call is made here).
 * srwcr_plan_slab (host-only) partitions the slices.
-* The z-slab decomposition used by nranks > 1 -- rank-partial bin statistics summed
-  across ranks, then a rank-partial gradient summed across ranks -- reproduces the
-  single-process result, run as 2 gloo processes with the oracle standing in for the
-  kernels (the kernels themselves are covered on one GPU by
-  tests/test_gpu_parity.py::test_slab_decomposition_on_one_gpu).
+* The ALGEBRA of the z-slab decomposition used by nranks > 1 -- rank-partial bin
+  statistics summed across ranks, then a rank-partial gradient summed across ranks --
+  reproduces the single-process result: 2 gloo processes each running the ORACLE on its
+  slab (no library context here).  The library's own nranks = 2 path runs as 2 processes
+  on one GPU in tests/test_gpu_multirank.py (caller-driven exchange over gloo) and its
+  slab kernels in tests/test_gpu_parity.py::test_slab_decomposition_on_one_gpu.
 """
 import ctypes
 import os
@@ -148,7 +149,7 @@ def _rank_main(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_zslab_decomposition_gloo_two_ranks():
+def test_oracle_zslab_algebra_gloo_two_ranks():
     import torch.multiprocessing as mp
 
     ctx = mp.get_context("spawn")

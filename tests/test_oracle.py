@@ -547,3 +547,88 @@ def test_orientation1_identical_images_and_slabs():
     g_parts = sum(O.grad_moments_A(pb, F, M, params, N, ga, reg, Z, a, b) for a, b in zip(cuts[:-1], cuts[1:]))
     assert np.linalg.norm(g_parts - g_full) <= 1e-13 * np.linalg.norm(g_full)
     assert np.linalg.norm(g_full - O.eval_moments(pb, F, M, params)[1]) <= 1e-13 * np.linalg.norm(g_full)
+
+
+# ------------------------------------------------------------ L-BFGS (F1, reading c20)
+
+def test_lbfgs_quadratic_closed_form():
+    """A strictly convex quadratic 1/2 x.Ax - b.x: the minimiser A^-1 b (closed form)."""
+    from oracle.lbfgs import lbfgs
+    rng = np.random.default_rng(7)
+    Q = rng.standard_normal((12, 12))
+    A = Q @ Q.T + 12 * np.eye(12)
+    b = rng.standard_normal(12)
+    x, rep, its = lbfgs(lambda x: (0.5 * x @ A @ x - b @ x, A @ x - b), np.zeros(12), max_iter=200,
+                        epsilon=1e-8)
+    assert rep["status_name"] == "converged"
+    assert np.allclose(x, np.linalg.solve(A, b), rtol=0, atol=1e-8)
+
+
+def test_lbfgs_rosenbrock_minimum():
+    from oracle.lbfgs import lbfgs
+
+    def rosen(x):
+        f = (1 - x[0]) ** 2 + 100 * (x[1] - x[0] ** 2) ** 2
+        g = np.array([-2 * (1 - x[0]) - 400 * x[0] * (x[1] - x[0] ** 2), 200 * (x[1] - x[0] ** 2)])
+        return f, g
+    x, rep, _ = lbfgs(rosen, np.array([-1.2, 1.0]), max_iter=500, epsilon=1e-9, stable_window=1000)
+    assert np.allclose(x, [1.0, 1.0], atol=1e-6), (x, rep)
+
+
+def test_lbfgs_first_step_and_wolfe_invariants():
+    """First trial step 1/||g0|| along -g0; every accepted step satisfies the Armijo test
+    and the regular Wolfe curvature test (c20) and is 1/||g0|| or 1 times 0.5^i 2.1^j."""
+    from oracle.lbfgs import lbfgs
+    rng = np.random.default_rng(3)
+    A = np.diag(rng.uniform(1, 50, 8))
+
+    calls = []
+
+    def fun(x):
+        calls.append(x.copy())
+        return 0.25 * np.sum((A @ x) ** 2) ** 1.0 + np.sum(np.cos(x)), 0.5 * A @ (A @ x) - np.sin(x)
+    x0 = rng.standard_normal(8)
+    f0, g0 = fun(x0)
+    calls.clear()
+    _, rep, its = lbfgs(fun, x0, max_iter=15, stable_window=1000)
+    assert np.allclose(calls[1], x0 - g0 / np.linalg.norm(g0), rtol=0, atol=1e-15)
+    xprev, fprev, gprev = x0, f0, g0
+    d = -g0
+    for k, (xk, fk, st, _) in enumerate(its):
+        s = xk - xprev
+        dd = s / st
+        fk2, gk = fun(xk)
+        assert fk2 == fk
+        assert fk <= fprev + 1e-4 * st * (gprev @ dd) + 1e-15
+        assert gk @ dd >= 0.9 * (gprev @ dd) - 1e-15
+        base = 1 / np.linalg.norm(g0) if k == 0 else 1.0
+        ok = any(abs(st - base * 0.5 ** i * 2.1 ** j) <= 1e-12 * st for i in range(25) for j in range(25))
+        assert ok, st
+        xprev, fprev, gprev = xk, fk, gk
+
+
+def test_lbfgs_one_dimensional_quadratic_second_step_is_newton():
+    """1-D f = a x^2 / 2: after the first pair, H0 = y.s / y.y = 1/a makes the second
+    direction the Newton step, accepted at step 1: x_2 = 0 (up to rounding)."""
+    from oracle.lbfgs import lbfgs
+    a = 3.7
+    x, rep, its = lbfgs(lambda x: (0.5 * a * x @ x, a * x), np.array([2.0]), max_iter=2, stable_window=1000)
+    assert len(its) == 2 and its[1][2] == 1.0
+    assert abs(its[1][0][0]) < 1e-14
+
+
+def test_lbfgs_stable_stop_and_line_search_failure():
+    """A cost whose variation is far below 1e-5 of its size: the run stops 'stable' once
+    stable_window costs (the start included) are within the tolerance.  A cost that is
+    infeasible everywhere but the start: the line search fails."""
+    from oracle.lbfgs import Infeasible, lbfgs
+    x, rep, its = lbfgs(lambda x: (1e6 + np.sum(np.cos(x)), -np.sin(x)), np.array([3.0, 2.5, 2.0]),
+                        stable_window=20)
+    assert rep["status_name"] == "stable" and rep["iterations"] == 19
+
+    def fun(x):
+        if np.any(x != 1.0):
+            raise Infeasible
+        return 1.0, np.ones_like(x)
+    x, rep, its = lbfgs(fun, np.ones(3), max_linesearch=7)
+    assert rep["status_name"] == "line_search_failed" and rep["evaluations"] == 8 and np.all(x == 1.0)

@@ -1,5 +1,6 @@
+import os
 import sys, numpy as np
-sys.path.insert(0, '/root/repo')
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1804_05061_b200 as S, oracle as O
 rng = np.random.default_rng(6)
 A = rng.integers(0, 16, size=(20, 24, 26)).astype(np.float32)

@@ -1,6 +1,6 @@
 """Fine spatial lattice (F3, spatial bins = control cells) at a full config: eval time."""
-import sys, time, json
-sys.path.insert(0, "/root/repo")
+import os, sys, time, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
 import synth, paper_1804_05061_b200 as S
 name = sys.argv[1] if len(sys.argv) > 1 else "C5"

@@ -1,7 +1,7 @@
 """Fine spatial lattice (spatial bins = control nodes) on a reduced
 CT-like volume: GPU vs oracle, and the eval time against the coarse 8^3 lattice."""
-import sys, time, json
-sys.path.insert(0, "/root/repo"); sys.path.insert(0, "/root/repo/tests")
+import os, sys, time, json
+_R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, 'tests'))
 import numpy as np
 import oracle as O, synth, paper_1804_05061_b200 as S
 from gpu_common import rel, rel_l2

@@ -1,6 +1,6 @@
 """Debug: where does the GPU-vs-oracle gradient error concentrate?"""
-import sys, numpy as np
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+import os, sys, numpy as np
+_R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, 'tests'))
 import oracle as O
 from gpu_common import problem, rel_l2
 name, kind = sys.argv[1], sys.argv[2]

@@ -1,5 +1,6 @@
+import os
 import sys, time, numpy as np
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+_R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, 'tests'))
 import oracle as O
 from gpu_common import problem, rel, rel_l2
 for name in sys.argv[1:]:

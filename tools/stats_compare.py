@@ -1,7 +1,7 @@
 """Debug: compare the GPU's static counts N and unshifted moments S, Q (debug dumps)
 with the oracle's moment tables, per region/bin, for one config."""
-import sys, numpy as np
-sys.path.insert(0, '/root/repo'); sys.path.insert(0, '/root/repo/tests')
+import os, sys, numpy as np
+_R = os.path.dirname(os.path.dirname(os.path.abspath(__file__))); sys.path.insert(0, _R); sys.path.insert(0, os.path.join(_R, 'tests'))
 import oracle as O
 from gpu_common import problem, rel, rel_l2
 name = sys.argv[1]; kind = sys.argv[2] if len(sys.argv) > 2 else "small"
