@@ -18,7 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _ROOT = os.path.dirname(_HERE)
-_LIB = os.path.join(_HERE, "libsrwcr.so")
+_LIB = os.environ.get("SRWCR_LIB") or os.path.join(_HERE, "libsrwcr.so")   # (SRWCR_LIB: another build of csrc/, experiments)
 _SRCS = [os.path.join(_HERE, "csrc", f) for f in ("srwcr.cu", "srwcr_kernels.cuh", "srwcr_fast.cuh", "srwcr_register.inc",
                                                   "srwcr_fields.inc")]
 _HDR = os.path.join(_ROOT, "include", "srwcr.h")

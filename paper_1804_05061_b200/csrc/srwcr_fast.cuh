@@ -103,6 +103,14 @@ template <int XV> __device__ __forceinline__ VF<XV> vlerp(VF<XV> a, VF<XV> b, VF
 #define SRWCR_P1_TEX 0
 #endif
 constexpr bool P1_TEX = SRWCR_P1_TEX != 0;
+// where the z-march issues slice z+1's gathers: 0 after the layer slide, 1 after the line
+// scale (REDUX), 3 before the binless sums, 4 before the line-table atomics, 2 at the end of
+// the slice.  Measured on C5 (pass 1 ms): 1.531 / 1.423 / 1.445 / 1.460 / 1.589.  Issued before
+// a warp-synchronous instruction, the loads' destination registers are copied or spilled at
+// the divergence check that precedes it, which waits for the loads (long-scoreboard stalls).
+#ifndef SRWCR_GATHER_POS
+#define SRWCR_GATHER_POS 1
+#endif
 __device__ __forceinline__ float4 tex_gather(unsigned long long t, int layer, float x, float y) {
     float4 r;
     asm volatile("tld4.r.a2d.v4.f32.f32 {%0, %1, %2, %3}, [%4, {%5, %6, %7, %7}];"
@@ -469,11 +477,14 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
 
     // ---- software pipeline: the records, gathers and coordinate flags of slice z+1 are in
     // flight while slice z is processed
-    unsigned recn[XV];
+    // (the records two slices ahead: a load consumed one slice later is moved / spilled by
+    // the register allocator at the loop edge, which waited on it)
+    unsigned recn[XV], recn2[XV];
     float mvn[XV];   // MODE 2: m of slice z+1
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
         recn[v] = MOMENTS ? __ldg(a.rec + (vb + 32 * v)) : 0u;
+        recn2[v] = MOMENTS ? __ldg(a.rec + (vb + min(1, zlen - 1) * nxy + 32 * v)) : 0u;
         mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + 32 * v)) : 0.f;
     }
     float C[XV][8];
@@ -563,7 +574,10 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         for (int v = 0; v < XV; ++v) {
             rc[v] = recn[v];
             mvc[v] = mvn[v];
-            if constexpr (MOMENTS) recn[v] = __ldg(a.rec + (vb + izn * nxy + 32 * v));
+            if constexpr (MOMENTS) {
+                recn[v] = recn2[v];
+                recn2[v] = __ldg(a.rec + (vb + min(iz + 2, zlen - 1) * nxy + 32 * v));
+            }
             if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + 32 * v));
         }
         int flc[XV];
@@ -649,7 +663,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 }
                 tol = 2e-6f * fmaxf(fmaxf(LMw[0], LMw[1]), fmaxf(LMw[2], LMw[3]));
             }
-            gather(z0 + izn);
+            if (SRWCR_GATHER_POS == 0) gather(z0 + izn);
         }
         // ---- record: slot and Parzen weights of F (static); the shifted first moment A
         int slot[XV];
@@ -674,6 +688,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             lsc = __int_as_float((ksc + 127) << 23);
             lisc = __int_as_float((127 - ksc) << 23);
         }
+        if constexpr (SAMPLE && SRWCR_GATHER_POS == 1) gather(z0 + izn);
         if (SAMPLE && !INT) {
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
@@ -690,7 +705,11 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 if (MODE == 1) __stcs(a.Mv + (vb + iz * nxy + 32 * v), m.v[v]);
             }
         }
-        if constexpr (!MOMENTS) continue;
+        if constexpr (!MOMENTS) {
+            if constexpr (SRWCR_GATHER_POS >= 2) gather(z0 + izn);
+            continue;
+        }
+        if constexpr (SAMPLE && SRWCR_GATHER_POS == 3) gather(z0 + izn);
         // ---- binless (z-taps folded in registers)
         {
             const float4 wz = ZS[iz];
@@ -705,6 +724,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             acca[2] = vfma(vsplat<XV>(wz.z), Ab, acca[2]);
             acca[3] = vfma(vsplat<XV>(wz.w), Ab, acca[3]);
         }
+        if constexpr (SAMPLE && SRWCR_GATHER_POS == 4) gather(z0 + izn);
         // ---- binned: int32 line table (magic-number fixed point at the line scale lsc; the
         // fold subtracts the per-entry offset count); every voxel adds its 8 values.  A line whose
         // voxels all share one slot (static list count 1) reduces across the warp instead
@@ -815,6 +835,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             }
         }
         __syncwarp();
+        if constexpr (SAMPLE && SRWCR_GATHER_POS == 2) gather(z0 + izn);
     }
     // ---- row end: binless -> K[ns]; lane j of the reduction holds value j = (l, ch, n)
     if constexpr (MOMENTS) {
