@@ -31,7 +31,13 @@ def lbfgs(fun, x0, m=5, max_iter=200, max_linesearch=20, ftol=1e-4, wolfe=0.9, s
           stable_tol=1e-5, epsilon=0.0):
     """Minimise ``fun(x) -> (f, g)``.  Returns (x, report, iterates) with iterates the list
     of accepted (x_k, f_k, step_k, cost evaluations so far) for k = 1.. (x_0 excluded)."""
-    x = np.array(x0, dtype=np.float64, copy=True)
+    shape = np.shape(x0)
+    fun0 = fun
+
+    def fun(v):   # flat fp64 vectors inside; the caller's shape outside
+        f, g = fun0(v.reshape(shape))
+        return f, np.asarray(g, dtype=np.float64).ravel()
+    x = np.array(x0, dtype=np.float64, copy=True).ravel()
     f, g = fun(x)
     f0 = f
     evals = 1
@@ -76,7 +82,7 @@ def lbfgs(fun, x0, m=5, max_iter=200, max_linesearch=20, ftol=1e-4, wolfe=0.9, s
         s, y = xp - x, gp - g
         x, g, f = xp, gp, fp
         hist.append(f)
-        its.append((x.copy(), f, step, evals))
+        its.append((x.reshape(shape).copy(), f, step, evals))
         if np.sqrt(g @ g) <= epsilon * max(1.0, np.sqrt(x @ x)):
             status = 0
             break
@@ -108,4 +114,4 @@ def lbfgs(fun, x0, m=5, max_iter=200, max_linesearch=20, ftol=1e-4, wolfe=0.9, s
         step = 1.0
     rep = {"iterations": it, "evaluations": evals, "status": status, "status_name": STATUS[status],
            "initial_cost": f0, "final_cost": f, "grad_norm": float(np.sqrt(g @ g))}
-    return x, rep, its
+    return x.reshape(shape), rep, its

@@ -16,8 +16,11 @@
 //    (quarter-rate conversion pipe, measured in tools/microbench/micro3.cu);
 //  * packed fp32x2 arithmetic (FFMA2 / FADD2 / FMUL2) over the lane's two voxels;
 //  * deterministic accumulation: int32 line tables, per-warp fp32 column tables folded
-//    into the CTA cell table in a fixed order (one barrier per round of rows), and int64
-//    fixed-point global statistics (units 2^-16) -- two evaluations are bitwise identical;
+//    into the CTA cell table in a fixed order (one barrier per round of rows), int64
+//    fixed-point global statistics (binned shifted first moments in units 2^-24, binless
+//    second moments in 2^-16) and an int64 fixed-point gradient (units 2^-k, k from the
+//    combine's bound) -- two evaluations are bitwise identical, and rank partials of a
+//    z-slab decomposition add up exactly;
 //  * per-item interior flag (convex-hull bound of the displacement: u is a convex
 //    combination of the supporting node values): items whose samples can never clamp
 //    run a variant without the clamp logic of reading c2.
@@ -97,6 +100,21 @@ template <int XV> __device__ __forceinline__ VF<XV> vmul(VF<XV> a, VF<XV> b) {
 template <int XV> __device__ __forceinline__ VF<XV> vlerp(VF<XV> a, VF<XV> b, VF<XV> t) {
     return vfma(t, vsub(b, a), a);
 }
+
+// Bounds checks of the shared-memory tables (build with -DSRWCR_CHECK: the checked library
+// tools/sanitize_run.py runs; compute-sanitizer is not available on the GPU pool)
+#ifdef SRWCR_CHECK
+#define FCHECK(cond)                                                                                  \
+    do {                                                                                              \
+        if (!(cond)) {                                                                                \
+            printf("srwcr check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__, __LINE__,  \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define FCHECK(cond) do { } while (0)
+#endif
 
 // pass 1 gathers the 8 corners of M with 2 textureGather (TLD4) instead of 8 LDG (c20 / c21)
 #ifndef SRWCR_P1_TEX
@@ -444,6 +462,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             VF<XV> w, q0, q1, q2;
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
+                FCHECK(pl.relx[v] + l < 32 && pl.relx[v] >= 0);
                 const float4 P = PLw[pl.relx[v] + l];
                 w.v[v] = __ldg(reinterpret_cast<const float *>(a.t.cw[0] + pl.xv[v]) + l);
                 q0.v[v] = P.x;
@@ -612,7 +631,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         for (int v = 0; v < XV; ++v) nf.v[v] = fminf(mfm.v[v] - MAGIC, Lm1);
         const VF<XV> fm = vsub(m, nf);
         const VF<XV> omf = vsub(vone, fm);
-        VF<XV> w1, w1l;
+        VF<XV> w1{}, w1l{};
         if constexpr (MOMENTS) {
             VF<XV> sfold;
 #pragma unroll
@@ -666,13 +685,14 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             if (SRWCR_GATHER_POS == 0) gather(z0 + izn);
         }
         // ---- record: slot and Parzen weights of F (static); the shifted first moment A
-        int slot[XV];
-        VF<XV> hhi, A;
+        int slot[XV] = {};
+        VF<XV> hhi{}, A{};
         float lsc = 1.f, lisc = 1.f;
         if constexpr (MOMENTS) {
 #pragma unroll
             for (int v = 0; v < XV; ++v) {
                 slot[v] = pl.valid[v] ? (int)(rc[v] >> 24) : dummy;
+                FCHECK(slot[v] < ns || slot[v] == dummy);
                 hhi.v[v] = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu));
                 A.v[v] = SH[slot[v]];
             }
@@ -819,6 +839,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 if (j < cnt) {
                     const int s = (int)(ent & 0xFFu);
                     const int nadd = (int)((ent >> nsh) & 0xFFu);
+                    FCHECK(s < ns && nadd <= 32 * XV);
                     const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
                     int raw;
                     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
@@ -981,6 +1002,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
         const int nts = TS[159];
         for (int pidx = threadIdx.x; pidx < nts * 32; pidx += blockDim.x) {
             const int s = TS[pidx >> 5], j = pidx & 31;
+            FCHECK(s <= ns && s < S);
             float acc0 = 0.f, acc1 = 0.f, acc2 = 0.f, acc3 = 0.f;
             for (int w = 0; w < W; ++w) {
                 float *kp = K + (w * S + s) * 32 + j;
@@ -1227,6 +1249,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             for (int k = 0; k < 4; ++k) {
                 const int nd = pl.relx[v] + ((k + q4) & 3);
                 const float w = f4(crv[v], k);
+                FCHECK(nd >= 0 && nd < 32);
                 red_shared(RBw + nd, __float_as_int(fmaf(w, R0, MAGIC)));
                 red_shared(RBw + 32 + nd, __float_as_int(fmaf(w, R1, MAGIC)));
                 red_shared(RBw + 64 + nd, __float_as_int(fmaf(w, R2, MAGIC)));
@@ -1240,6 +1263,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             RBw[c * 32 + j] = 0;
             const float rv = (float)(raw - CX[j] * MAGIC_I) * isc * gunit;
             if (rv != 0.f) {
+                FCHECK(lz >= 0 && (((lz * 3 + c) * nyn + (cby - yn0 + 3)) * nxn + j) < A2.npmax);
                 int *nh = NPH + ((lz * 3 + c) * nyn + (cby - yn0)) * nxn + j;
                 int *nl = NPL + ((lz * 3 + c) * nyn + (cby - yn0)) * nxn + j;
 #pragma unroll
@@ -1346,6 +1370,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             const bool ex = m < 0.f;
             m = ex ? -1.0f - m : m;
             const int slot = (int)(rc[v] >> 24);
+            FCHECK(!pl.valid[v] || slot < ns);
             const float hhi = __int_as_float(0x3F800000 + (int)(rc[v] & 0xFFFFFFu)) - 1.0f;
             int im;
             const float fl = mfloor(m, im);
@@ -1382,8 +1407,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         }
         __syncwarp();
     }
-#pragma unroll
     if (!(a.ablate & 64))
+#pragma unroll
         for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
 }
 
@@ -1391,7 +1416,7 @@ template <int XV, int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_p2f(F2Args A2) {
     extern __shared__ __align__(16) unsigned char smem[];
     const FArgs &a = A2.f;
-    const int W = a.W, S = a.S;
+    const int W = a.W;
     const Geo &g = a.g;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int ii = a.i0 + blockIdx.x;

@@ -180,3 +180,26 @@ def test_split_pass1_bitwise_equals_fused(name, monkeypatch):
         assert r[0] == res[0][0]
         for k in (1, 2, 3):
             assert np.array_equal(r[k], res[0][k])
+
+
+def test_checked_build_small_cases():
+    """The library built with -DSRWCR_CHECK (device-side bounds checks of every shared-memory
+    table index of the fast passes; a failed check traps) runs tools/sanitize_run.py: both
+    orientations, round-1 and fast passes (XV 1 and 2, fused and split pass 1), bending,
+    L-BFGS and field utilities.  (compute-sanitizer is closed on the GPU pool.)"""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    lib = os.path.join(root, "build_variants", "libsrwcr_check.so")
+    src = os.path.join(root, "paper_1804_05061_b200", "csrc", "srwcr.cu")
+    if not os.path.exists(lib) or os.path.getmtime(lib) < max(
+            os.path.getmtime(os.path.join(os.path.dirname(src), f)) for f in os.listdir(os.path.dirname(src))):
+        os.makedirs(os.path.dirname(lib), exist_ok=True)
+        import paper_1804_05061_b200 as S
+        subprocess.check_call([os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc"), *S.NVCC_FLAGS, "-DSRWCR_CHECK",
+                               "-o", lib, src, "-ldl"])
+    env = dict(os.environ, SRWCR_LIB=lib)
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "sanitize_run.py")], env=env,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "sanitize_run: ok" in out.stdout
