@@ -528,41 +528,53 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             T[c] = vsub(u[c], vsub(mf[c], vmagic));
             om[c] = vsub(vone, T[c]);
         }
+        int ci[XV][3], fv[XV];
+        bool out = false;
 #pragma unroll
         for (int v = 0; v < XV; ++v) {
-            int ci[3];
-            ci[0] = __float_as_int(mf[0].v[v]) - MAGIC_I + pl.xv[v];
-            ci[1] = __float_as_int(mf[1].v[v]) - MAGIC_I + y;
-            ci[2] = __float_as_int(mf[2].v[v]) - MAGIC_I + zz;
+            ci[v][0] = __float_as_int(mf[0].v[v]) - MAGIC_I + pl.xv[v];
+            ci[v][1] = __float_as_int(mf[1].v[v]) - MAGIC_I + y;
+            ci[v][2] = __float_as_int(mf[2].v[v]) - MAGIC_I + zz;
             // near an integer (a cell / clamp boundary: the derivative of the interpolant jumps)
             // unless u is exactly 0 (tap window at rest: identical in fp32 and fp64)
             const float emin = fminf(fminf(fminf(T[0].v[v], om[0].v[v]), fminf(T[1].v[v], om[1].v[v])),
                                      fminf(T[2].v[v], om[2].v[v]));
             const float umax = fmaxf(fmaxf(fabsf(u[0].v[v]), fabsf(u[1].v[v])), fabsf(u[2].v[v]));
             const bool rest = umax == 0.f;
-            int f = (emin < tol && !rest ? 8 : 0) | (rest ? 16 : 0);
-            if (!INT) {   // reading c2: clamp to [0, N-1], cell = min(floor y, N-2)
-                const int nm2[3] = {g.nxm2, g.nym2, g.nzm2};
+            fv[v] = (emin < tol && !rest ? 8 : 0) | (rest ? 16 : 0);
+            if (!INT)
+                out = out || (unsigned)ci[v][0] > (unsigned)g.nxm2 || (unsigned)ci[v][1] > (unsigned)g.nym2 ||
+                      (unsigned)ci[v][2] > (unsigned)g.nzm2;
+        }
+        // reading c2: clamp to [0, N-1], cell = min(floor y, N-2) -- only for the warps that
+        // have a sample outside [0, N-2] (the items of the general variant touch a face, but
+        // most of their samples stay inside)
+        if (!INT && __any_sync(FULL, out)) {
+            const int nm2[3] = {g.nxm2, g.nym2, g.nzm2};
+#pragma unroll
+            for (int v = 0; v < XV; ++v)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const bool lo = ci[c] < 0, hi = ci[c] > nm2[c];
+                    const bool lo = ci[v][c] < 0, hi = ci[v][c] > nm2[c];
                     const float tt = T[c].v[v];
                     T[c].v[v] = lo ? 0.f : (hi ? 1.f : tt);
-                    f |= (lo || (hi && !(ci[c] == nm2[c] + 1 && tt == 0.f))) ? (1 << c) : 0;
-                    ci[c] = min(max(ci[c], 0), nm2[c]);
+                    fv[v] |= (lo || (hi && !(ci[v][c] == nm2[c] + 1 && tt == 0.f))) ? (1 << c) : 0;
+                    ci[v][c] = min(max(ci[v][c], 0), nm2[c]);
                 }
-            }
-            fl[v] = f;
+        }
+#pragma unroll
+        for (int v = 0; v < XV; ++v) {
+            fl[v] = fv[v];
             if constexpr (P1_TEX) {
                 // two 2x2 footprints (textureGather of the layered copy of M, layer = z): the
                 // footprint around the texel corner (cx + 1, cy + 1) is exactly texels cx..cx+1,
                 // cy..cy+1 (integer coordinates: no filtering, no rounding of the position)
-                const float fx = (float)(ci[0] + 1), fy = (float)(ci[1] + 1);
-                const float4 q0 = tex_gather(a.texM, ci[2], fx, fy), q1 = tex_gather(a.texM, ci[2] + 1, fx, fy);
+                const float fx = (float)(ci[v][0] + 1), fy = (float)(ci[v][1] + 1);
+                const float4 q0 = tex_gather(a.texM, ci[v][2], fx, fy), q1 = tex_gather(a.texM, ci[v][2] + 1, fx, fy);
                 C[v][0] = q0.w; C[v][1] = q0.z; C[v][2] = q0.x; C[v][3] = q0.y;
                 C[v][4] = q1.w; C[v][5] = q1.z; C[v][6] = q1.x; C[v][7] = q1.y;
             } else {
-                const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[2] * nxy + ci[1] * nx + ci[0];
+                const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[v][2] * nxy + ci[v][1] * nx + ci[v][0];
                 const float *b0 = a.M + o0, *b1 = a.M + (o0 + nx), *b2 = a.M + (o0 + dzo), *b3 = a.M + (o0 + dzo + nx);
                 C[v][0] = __ldg(b0); C[v][1] = __ldg(b0 + 1);
                 C[v][2] = __ldg(b1); C[v][3] = __ldg(b1 + 1);
@@ -832,28 +844,32 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             const float2 wzs01 = make_float2(wz.x * lisc, wz.y * lisc), wzs23 = make_float2(wz.z * lisc, wz.w * lisc);
             const int e = lane & 7;
             const int nsh = (e & 1) ? 16 : 8;
-            for (int p = 0; 4 * p < cnt; ++p) {
+            auto fold_entry = [&](unsigned ent) {
+                const int s = (int)(ent & 0xFFu);
+                const int nadd = (int)((ent >> nsh) & 0xFFu);
+                FCHECK(s < ns && nadd <= 32 * XV);
+                const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
+                int raw;
+                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
+                asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(0) : "memory");
+                const float val = (float)(raw - nadd * MAGIC_I);
+                const unsigned ka = kw_s + (unsigned)(s * 128 + e * 16);
+                float4 k4;
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(k4.x), "=f"(k4.y), "=f"(k4.z), "=f"(k4.w) : "r"(ka));
+                const float2 vv = make_float2(val, val);
+                const float2 r01 = __ffma2_rn(wzs01, vv, make_float2(k4.x, k4.y));
+                const float2 r23 = __ffma2_rn(wzs23, vv, make_float2(k4.z, k4.w));
+                asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(ka), "f"(r01.x), "f"(r01.y), "f"(r23.x), "f"(r23.y) : "memory");
+            };
+            // entries 0..31 come from the prefetched register (one per lane), 4 slots per pass
+            const int c32 = min(cnt, 32);
+            for (int p = 0; 4 * p < c32; ++p) {
                 const int j = 4 * p + (lane >> 3);
-                unsigned ent = __shfl_sync(FULL, ecur, j & 31);
-                if (j >= 32) ent = j < cnt ? __ldg(a.lent + o + j) : 0u;   // > 32 slots in one line
-                if (j < cnt) {
-                    const int s = (int)(ent & 0xFFu);
-                    const int nadd = (int)((ent >> nsh) & 0xFFu);
-                    FCHECK(s < ns && nadd <= 32 * XV);
-                    const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
-                    int raw;
-                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
-                    asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(0) : "memory");
-                    const float val = (float)(raw - nadd * MAGIC_I);
-                    const unsigned ka = kw_s + (unsigned)(s * 128 + e * 16);
-                    float4 k4;
-                    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(k4.x), "=f"(k4.y), "=f"(k4.z), "=f"(k4.w) : "r"(ka));
-                    const float2 vv = make_float2(val, val);
-                    const float2 r01 = __ffma2_rn(wzs01, vv, make_float2(k4.x, k4.y));
-                    const float2 r23 = __ffma2_rn(wzs23, vv, make_float2(k4.z, k4.w));
-                    asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(ka), "f"(r01.x), "f"(r01.y), "f"(r23.x), "f"(r23.y) : "memory");
-                }
+                const unsigned ent = __shfl_sync(FULL, ecur, j & 31);
+                if (j < c32) fold_entry(ent);
             }
+            for (int j = 32 + (lane >> 3); j - (lane >> 3) < cnt; j += 4)   // > 32 slots in one line (rare)
+                if (j < cnt) fold_entry(__ldg(a.lent + o + j));
         }
         __syncwarp();
         if constexpr (SAMPLE && SRWCR_GATHER_POS == 2) gather(z0 + izn);

@@ -19,10 +19,13 @@ from . import Srwcr, compose, downsample2, resample, upsample2_field
 
 
 def register_multires(fixed, moving, spacing_mm, bins, spatial_bins, control_vox=5.0, levels=3,
-                      iters=(200, 200, 120), w_p=0.1, verbose=False, **lbfgs):
+                      iters=(200, 200, 120), w_p=0.1, verbose=False, orientation=0, **lbfgs):
     """Register moving onto fixed (fp32 CUDA tensors [Nz, Ny, Nx], raw intensities).
 
     control_vox: control spacing in voxels at every level (paper: 5 at the finest).
+    spatial_bins: k cells per axis at every level, or "control": spatial bins = control
+    cells at each level (k = round(N_level / control_vox) per axis; the paper's setting,
+    P:91).  orientation: 0 = moving as the estimated image B, 1 = moving as the model A.
     Returns (U, reports): U = total displacement field [3, Nz, Ny, Nx] (full resolution,
     voxels) such that moving(x + U(x)) ~ fixed(x); reports = per-level L-BFGS reports."""
     import torch
@@ -43,7 +46,11 @@ def register_multires(fixed, moving, spacing_mm, bins, spatial_bins, control_vox
             Fk, Mk = downsample2(Fk), downsample2(Mk)
         scale = np.array([2.0 ** down, 2.0 ** down, 2.0 ** down if shape[0] > 1 else 1.0])
         sp = np.asarray(spacing_mm, dtype=np.float64) * scale
-        g = Srwcr(Fk, Mk, tuple(sp), bins, spatial_bins, tuple(control_vox * sp))
+        if isinstance(spatial_bins, str):   # "control": one spatial cell per control cell
+            sb = tuple(max(1, int(round(n / control_vox))) if n > 1 else 0 for n in tuple(Fk.shape)[::-1])
+        else:
+            sb = spatial_bins
+        g = Srwcr(Fk, Mk, tuple(sp), bins, sb, tuple(control_vox * sp), orientation=orientation)
         try:
             x, rep = g.register(None, w_p=w_p, max_iter=int(iters[k]), verbose=int(verbose), **lbfgs)
             uk = torch.from_numpy(g.field(x)).to(fixed.device)
