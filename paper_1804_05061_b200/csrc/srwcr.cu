@@ -149,6 +149,7 @@ struct srwcr_ctx {
     bool fsplit = false;
     float *fMv = nullptr;
     cudaArray_t fMarr = nullptr;            // M as a 2-D layered array (pass 1 textureGather)
+    float4 *fphi4 = nullptr;                // fp32 phi, one float4 (x, y, z, 0) per node
     cudaTextureObject_t ftexM = 0;
     int fWw = 8, fMinbW = 3;
     size_t fsmemw = 0;
@@ -587,6 +588,8 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     if (const char *e = getenv("SRWCR_P1W_MINB")) c->fMinbW = atoi(e) == 2 ? 2 : 3;
     if (const char *e = getenv("SRWCR_P1W_W")) c->fWw = std::min(16, std::max(1, atoi(e)));
     CK(cudaMalloc(&c->fMv, sizeof(float) * slab));   // (also when fused: SRWCR_SPLIT is re-read per launch)
+    CK(cudaMalloc(&c->fphi4, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
+    CK(cudaMemset(c->fphi4, 0, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
     c->fsmemw = p1w_smem(c->fWw).total;
     // pass 2: node window and warps per CTA
     int npmax = 0;
@@ -650,7 +653,7 @@ static FArgs fast_args(srwcr_ctx *c) {
     for (int i = 0; i < 3; ++i) {
         a.t.cb[i] = c->cb[i]; a.t.cw[i] = c->cw[i]; a.t.cw64[i] = c->cw64[i]; a.t.sb[i] = c->sb[i]; a.t.sw[i] = c->sw[i];
     }
-    a.M = c->M; a.phi = c->phi; a.rec = c->frec; a.loff = c->floff; a.lent = c->flent; a.rmask = c->frmask;
+    a.M = c->M; a.phi = c->phi; a.phi4 = c->fphi4; a.rec = c->frec; a.loff = c->floff; a.lent = c->flent; a.rmask = c->frmask;
     a.items = c->fitems; a.itemw = c->fitemw; a.slotbins = c->fslotbins; a.iflag = c->fiflag; a.shiftc = c->shiftc;
     a.SQi = c->SQi; a.Qi = c->SQi + (size_t)c->R * c->g.B * 2;
     a.MG = c->MG; a.Mv = c->fMv; a.mgz0 = (int)c->z0;
@@ -720,7 +723,7 @@ static srwcr_status launch_fast_prep(srwcr_ctx *c, const double *pd) {
     Tables t{};
     for (int i = 0; i < 3; ++i) { t.cb[i] = c->cb[i]; t.cw[i] = c->cw[i]; t.sb[i] = c->sb[i]; t.sw[i] = c->sw[i]; }
     const int nconv = 296;   // blocks converting the params layers [pz0, pz1) to fp32; then one per item
-    k_fprep<<<(unsigned)(nconv + c->nfitems), 256, 0, c->stream>>>(pd, c->phi, c->g, c->pz0, c->pz1, nconv, c->fitems,
+    k_fprep<<<(unsigned)(nconv + c->nfitems), 256, 0, c->stream>>>(pd, c->fphi4, c->g, c->pz0, c->pz1, nconv, c->fitems,
                                                                     c->nfitems, t, c->fiflag);
     CKL();
     return SRWCR_OK;
@@ -1703,7 +1706,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma, c->ticket, c->dpart, c->xbeg, c->fitems, c->fitemw, c->fslotbins,
-                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv};
+                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv, c->fphi4};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

@@ -116,6 +116,14 @@ template <int XV> __device__ __forceinline__ VF<XV> vlerp(VF<XV> a, VF<XV> b, VF
 #define FCHECK(cond) do { } while (0)
 #endif
 
+// Timing ablations (SRWCR_ABLATE bits, wrong results) exist only in a build with
+// -DSRWCR_ABLATE_BUILD: the production kernels carry no ablation branches.
+#ifdef SRWCR_ABLATE_BUILD
+#define ABL(a, bit) (((a).ablate & (bit)) != 0)
+#else
+#define ABL(a, bit) false
+#endif
+
 // pass 1 gathers the 8 corners of M with 2 textureGather (TLD4) instead of 8 LDG (c20 / c21)
 #ifndef SRWCR_P1_TEX
 #define SRWCR_P1_TEX 0
@@ -146,7 +154,7 @@ __device__ __forceinline__ float mfloor(float u, int &iu) {
 
 // shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
 struct P1Smem {
-    int lt, k, ct, pl, lm, lo, wx, wxr, wy, rm, zs, zc, zb, sh, ts, total;
+    int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, total;
 };
 __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     P1Smem o;
@@ -160,6 +168,7 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]  the row's line-list offsets
     o.wx = take(64 * 16);                // float4 WX[XV * 32]  the lane voxels' spatial x weights (0: padding)
     o.wxr = take(64 * 16);               // float4 WXR[XV * 32] the same, rotated: component k = tap (k + lane) & 3
+    o.wcx = take(64 * 16);               // float4 WCX[XV * 32] the lane voxels' control x weights
     o.wy = take(W * 16);                 // float4 WY[W]
     o.rm = take(W * 16);                 // uint4 RM[W]
     o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
@@ -175,7 +184,8 @@ struct FArgs {
     Geo g;
     Tables t;
     const float *M;
-    const float *phi;               // fp32 [3][Gz][Gy][Gx]
+    const float *phi;               // fp32 [3][Gz][Gy][Gx] (round-1 layout; unused by the fast passes)
+    const float4 *phi4;             // fast passes: fp32 (phi_x, phi_y, phi_z, 0) per node [Gz][Gy][Gx]
     unsigned long long texM;        // texture object: M as a 2-D layered array (layer = z), point sampling
     const unsigned *rec;            // [slab voxels] slot << 24 | round(h_hi 2^23)
     const unsigned *loff;           // [lines + 1] offsets of the per-line entry lists
@@ -286,20 +296,22 @@ __global__ void k_lists(const unsigned *__restrict__ rec, const FItem *items, in
 // warp per item, the interior flag: with umax_c = max |phi_c| over the item's node box
 // (u_c is a convex combination of those values: B-spline weights >= 0, sum 1, P:51/Eq 8),
 // no sample of the item leaves [0, N-2] along any axis.
-__global__ void k_fprep(const double *__restrict__ p, float *__restrict__ phi, Geo g, int zlo, int zhi, int nconv,
+__global__ void k_fprep(const double *__restrict__ p, float4 *__restrict__ phi4, Geo g, int zlo, int zhi, int nconv,
                         const FItem *items, int nitems, Tables t, int *iflag) {
     if ((int)blockIdx.x < nconv) {
         const long long plane = (long long)g.Gx * g.Gy;
-        const long long cs = (long long)g.Gz * plane, span = (long long)(zhi - zlo) * plane;
+        const long long span = (long long)(zhi - zlo) * plane;
         for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < span; j += (long long)nconv * blockDim.x) {
             const long long i = (long long)zlo * plane + j;
             const long long gz = i / plane, xy = i - gz * plane;
+            float v[3];
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                double v = 0.0;
-                if (c < g.ndim && gz < g.GzExt) v = p[(c * g.GzExt + gz) * plane + xy];
-                phi[c * cs + i] = (float)v;
+                double d = 0.0;
+                if (c < g.ndim && gz < g.GzExt) d = p[(c * g.GzExt + gz) * plane + xy];
+                v[c] = (float)d;
             }
+            phi4[i] = make_float4(v[0], v[1], v[2], 0.f);
         }
         return;
     }
@@ -435,20 +447,23 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
 
     // ---- FFD layers (a3): U[n][c] = sum_{l,m} cwx_l cwy_m phi[c][gz_n][cby+m][cbx+l]
     VF<XV> U[4][3];
-    const int Gx = g.Gx, plane = g.Gx * g.Gy, cs = plane * g.Gz;
+    const int Gx = g.Gx, plane = g.Gx * g.Gy;
     const int pbase = cby * Gx + xn0 + lane;
+    const float4 *WCX = reinterpret_cast<const float4 *>(smem + L.wcx);
     auto load_layer = [&](int gz, VF<XV>(&Un)[3], int slotn) {
         float p0 = 0.f, p1 = 0.f, p2 = 0.f, mx = 0.f;
         if (lane < nxn) {
-            const float *q = a.phi + (gz * plane + pbase);
+            const float4 *q = a.phi4 + (gz * plane + pbase);
+            float4 f[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) f[m] = __ldg(q + m * Gx);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const float w = f4(cwy, m);
-                const float f0 = __ldg(q + m * Gx), f1 = __ldg(q + (cs + m * Gx)), f2 = __ldg(q + (2 * cs + m * Gx));
-                p0 = fmaf(w, f0, p0);
-                p1 = fmaf(w, f1, p1);
-                p2 = fmaf(w, f2, p2);
-                mx = fmaxf(mx, fmaxf(fabsf(f0), fmaxf(fabsf(f1), fabsf(f2))));
+                p0 = fmaf(w, f[m].x, p0);
+                p1 = fmaf(w, f[m].y, p1);
+                p2 = fmaf(w, f[m].z, p2);
+                mx = fmaxf(mx, fmaxf(fabsf(f[m].x), fmaxf(fabsf(f[m].y), fabsf(f[m].z))));
             }
             PLw[lane] = make_float4(p0, p1, p2, 0.f);
         }
@@ -457,6 +472,9 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         __syncwarp();
 #pragma unroll
         for (int c = 0; c < 3; ++c) Un[c] = vsplat<XV>(0.f);
+        float4 wcx[XV];   // the lane voxels' control x weights
+#pragma unroll
+        for (int v = 0; v < XV; ++v) wcx[v] = WCX[v * 32 + lane];
 #pragma unroll
         for (int l = 0; l < 4; ++l) {
             VF<XV> w, q0, q1, q2;
@@ -464,7 +482,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             for (int v = 0; v < XV; ++v) {
                 FCHECK(pl.relx[v] + l < 32 && pl.relx[v] >= 0);
                 const float4 P = PLw[pl.relx[v] + l];
-                w.v[v] = __ldg(reinterpret_cast<const float *>(a.t.cw[0] + pl.xv[v]) + l);
+                w.v[v] = f4(wcx[v], l);
                 q0.v[v] = P.x;
                 q1.v[v] = P.y;
                 q2.v[v] = P.z;
@@ -574,7 +592,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 C[v][0] = q0.w; C[v][1] = q0.z; C[v][2] = q0.x; C[v][3] = q0.y;
                 C[v][4] = q1.w; C[v][5] = q1.z; C[v][6] = q1.x; C[v][7] = q1.y;
             } else {
-                const int o0 = (a.ablate & 4) ? (pl.xv[v] + y * nx) : ci[v][2] * nxy + ci[v][1] * nx + ci[v][0];
+                const int o0 = ABL(a, 4) ? (pl.xv[v] + y * nx) : ci[v][2] * nxy + ci[v][1] * nx + ci[v][0];
                 const float *b0 = a.M + o0, *b1 = a.M + (o0 + nx), *b2 = a.M + (o0 + dzo), *b3 = a.M + (o0 + dzo + nx);
                 C[v][0] = __ldg(b0); C[v][1] = __ldg(b0 + 1);
                 C[v][2] = __ldg(b1); C[v][3] = __ldg(b1 + 1);
@@ -594,6 +612,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     }
     const float cI = it.cI;
     const float Lm1 = (float)(g.L - 1);
+    const float hrow = fmaf((float)lane, 0.7548776662f, (float)y * 0.41421356f);   // dither base of the row
     const unsigned kw_s = (unsigned)__cvta_generic_to_shared(Kw), lt_s = (unsigned)__cvta_generic_to_shared(LTw);
 
     for (int iz = 0; iz < zlen; ++iz) {
@@ -732,7 +751,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         if constexpr (SAMPLE) {
 #pragma unroll
             for (int v = 0; v < XV; ++v) {   // (a padding lane samples its clamped neighbour: identical values)
-                if (!(a.ablate & 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
+                if (!ABL(a, 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
                            make_float4(ex[v] ? -1.0f - m.v[v] : m.v[v], dgx.v[v], dgy.v[v], dgz.v[v]));
                 if (MODE == 1) __stcs(a.Mv + (vb + iz * nxy + 32 * v), m.v[v]);
             }
@@ -762,8 +781,8 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         // voxels all share one slot (static list count 1) reduces across the warp instead
         // (REDUX: a 32-lane same-address atomic serialises), and its lane 0 adds the 8 totals.
         const unsigned lo_o = LOw[iz], lo_o1 = LOw[iz + 1];
-        const bool uni = lo_o1 - lo_o == 1u && !(a.ablate & 8);
-        if (!(a.ablate & 2)) {
+        const bool uni = lo_o1 - lo_o == 1u && !ABL(a, 8);
+        if (!ABL(a, 2)) {
             const VF<XV> As = vmul(A, vsplat<XV>(lsc));
             const VF<XV> hiv = vmul(hhi, As), lov = vsub(As, hiv);   // h_hi A, h_lo A (scaled)
             // deterministic dither in (-1/2, 1/2) before the round to integer: identical values
@@ -771,10 +790,10 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             // the dither the rounding is unbiased (R2 low-discrepancy sequence over lane, slice, row)
             VF<XV> dith;
             {
-                const float h = fmaf((float)lane, 0.7548776662f, fmaf((float)iz, 0.5698402910f, (float)y * 0.41421356f));
-                const float d0 = (a.ablate & 16) ? 0.f : h - floorf(h) - 0.5f;
+                const float h = fmaf((float)iz, 0.5698402910f, hrow);   // h >= 0
+                const float d0 = ABL(a, 16) ? 0.f : h - (__fadd_rd(h, MAGIC) - MAGIC) - 0.5f;
                 dith.v[0] = d0;
-                if (XV == 2) dith.v[XV - 1] = (a.ablate & 16) ? 0.f : (d0 < 0.f ? d0 + 0.5f : d0 - 0.5f);
+                if (XV == 2) dith.v[XV - 1] = ABL(a, 16) ? 0.f : (d0 < 0.f ? d0 + 0.5f : d0 - 0.5f);
             }
             if (uni) {
                 const float4 *WXw = reinterpret_cast<const float4 *>(smem + L.wx);
@@ -835,7 +854,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         }
         // ---- fold the line into the column table K (touched entries only, from the static list)
         __syncwarp();
-        if (!(a.ablate & 2)) {
+        if (!ABL(a, 2)) {
             const unsigned o = LOw[iz], o1 = LOw[iz + 1], o2 = LOw[iz + 2 <= zlen ? iz + 2 : zlen];
             const int cnt = (int)(o1 - o);
             const unsigned ecur = entn;
@@ -847,7 +866,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             auto fold_entry = [&](unsigned ent) {
                 const int s = (int)(ent & 0xFFu);
                 const int nadd = (int)((ent >> nsh) & 0xFFu);
-                FCHECK(s < ns && nadd <= 32 * XV);
+                FCHECK((s < ns || s == dummy) && nadd <= 32 * XV);
                 const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
                 int raw;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
@@ -863,10 +882,11 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
             };
             // entries 0..31 come from the prefetched register (one per lane), 4 slots per pass
             const int c32 = min(cnt, 32);
+            // (lanes past the list fold the dummy slot, which no flush reads: no branch)
             for (int p = 0; 4 * p < c32; ++p) {
                 const int j = 4 * p + (lane >> 3);
                 const unsigned ent = __shfl_sync(FULL, ecur, j & 31);
-                if (j < c32) fold_entry(ent);
+                fold_entry(j < c32 ? ent : (unsigned)dummy);
             }
             for (int j = 32 + (lane >> 3); j - (lane >> 3) < cnt; j += 4)   // > 32 slots in one line (rare)
                 if (j < cnt) fold_entry(__ldg(a.lent + o + j));
@@ -947,6 +967,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
         reinterpret_cast<float4 *>(smem + L.wx)[i] = w;
         const int q = i & 3;   // the lane's rotation (lane = i mod 32)
         reinterpret_cast<float4 *>(smem + L.wxr)[i] = make_float4(f4(w, q), f4(w, (q + 1) & 3), f4(w, (q + 2) & 3), f4(w, (q + 3) & 3));
+        reinterpret_cast<float4 *>(smem + L.wcx)[i] = a.t.cw[0][min(it.x0 + i, it.x0 + it.xlen - 1)];
     }
 
     // per-lane constants
@@ -1074,6 +1095,7 @@ __host__ __device__ inline P1Smem p1w_smem(int W) {
     auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
     o.pl = take(W * 32 * 16);
     o.lm = take(W * 4 * 4 * 4);
+    o.wcx = take(64 * 16);
     o.zc = take(FZMAX * 16);
     o.zb = take(FZMAX * 4);
     o.total = off;
@@ -1094,6 +1116,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k_p1w(FArgs a) {
         ZC[i] = a.t.cw[2][it.z0 + i];
         ZB[i] = a.t.cb[2][it.z0 + i];
     }
+    for (int i = threadIdx.x; i < 32 * XV; i += blockDim.x)
+        reinterpret_cast<float4 *>(smem + L.wcx)[i] = a.t.cw[0][min(it.x0 + i, it.x0 + it.xlen - 1)];
     const int xn0 = a.t.cb[0][it.x0];
     const bool interior = a.iflag[ii] != 0;
     auto setup = [&](auto &pl) {
@@ -1363,7 +1387,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         // ---- retire the control layers this slice no longer reads
         const int bz = ZB[iz];
         while (gzl < bz) {
-            if (!(a.ablate & 64)) retire(gzl, Ad[0]);
+            if (!ABL(a, 64)) retire(gzl, Ad[0]);
 #pragma unroll
             for (int n = 0; n < 3; ++n)
 #pragma unroll
@@ -1376,7 +1400,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         // their shared-memory latency overlaps the voxel work below): gamma of the touched slots
         // over z (GZ[s][b2].l), alpha / beta over z (GZ[ns][ab].l)
         __syncwarp();
-        if (iz + 1 < zlen && !(a.ablate & 32)) gz_line(iz + 1, GZw + ((iz + 1) & 1) * S * 2);
+        if (iz + 1 < zlen && !ABL(a, 32)) gz_line(iz + 1, GZw + ((iz + 1) & 1) * S * 2);
         const float4 *GZc = GZw + (iz & 1) * S * 2;
         // ---- per voxel: Z dD/dm and the adjoint
         VF<XV> dx, dy, dzv;
@@ -1423,7 +1447,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         }
         __syncwarp();
     }
-    if (!(a.ablate & 64))
+    if (!ABL(a, 64))
 #pragma unroll
         for (int n = 0; n < 4; ++n) retire(gzl + n, Ad[n]);
 }
