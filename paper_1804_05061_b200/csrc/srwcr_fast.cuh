@@ -145,6 +145,13 @@ __device__ __forceinline__ float4 tex_gather(unsigned long long t, int layer, fl
     return r;
 }
 
+// a select the compiler keeps as one instruction (no branch around a rare condition)
+__device__ __forceinline__ float selp(bool c, float a, float b) {
+    float r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.f32 %0, %2, %3, p;\n\t}" : "=f"(r) : "r"((unsigned)c), "f"(a), "f"(b));
+    return r;
+}
+
 // floor(u) as float and as int (|u| < 2^22), full-rate FADD.RM instead of FRND / F2I
 __device__ __forceinline__ float mfloor(float u, int &iu) {
     const float m = __fadd_rd(u, MAGIC);
@@ -1347,14 +1354,14 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         entn = o1 + lane < o2 ? __ldg(a.lent + o1 + lane) : 0u;
         // lane = (slot j of the pass, b2): the four x-taps of GZ[s][b2] from four independent loads
         const int b2 = lane & 1;
-        {   // first pass (<= 16 slots: nearly every line) straight-line
+        {   // first pass (<= 16 slots: nearly every line) straight-line; lanes past the list
+            // write the dummy slot's entry, which no voxel reads (no branch)
             const int j = lane >> 1;
-            const int s = (int)(__shfl_sync(FULL, ecur, j) & 0xFFu);
-            if (j < cnt) {
-                const float4 *gy = GYw + (s * 2 + b2) * 4;
-                const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
-                GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
-            }
+            const unsigned ent = __shfl_sync(FULL, ecur, j);
+            const int s = j < cnt ? (int)(ent & 0xFFu) : ns + 1;
+            const float4 *gy = GYw + (s * 2 + b2) * 4;
+            const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
+            GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
         }
         for (int p = 1; 16 * p < cnt; ++p) {
             const int j = 16 * p + (lane >> 1);
@@ -1367,10 +1374,11 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
                 GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
             }
         }
-        float t = f4(wz, lane & 3) * abY;
+        float t = reinterpret_cast<const float *>(ZS + jz)[lane & 3] * abY;
         t += __shfl_xor_sync(FULL, t, 1);
         t += __shfl_xor_sync(FULL, t, 2);
-        if ((lane & 3) == 0) reinterpret_cast<float *>(GZb + ns * 2 + (lane >> 4))[(lane >> 2) & 3] = t;
+        // (the 4 lanes of a group hold the same sum: all store it, no branch)
+        reinterpret_cast<float *>(GZb + ns * 2 + (lane >> 4))[(lane >> 2) & 3] = t;
     };
     gz_line(0, GZw);
     for (int iz = 0; iz < zlen; ++iz) {
@@ -1417,8 +1425,9 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             const float nf = fminf(fl, Lm1);
             const float fm = m - nf;
             const bool integral = m == fl;
-            const float g1p = integral ? 0.1f : (fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f));
-            const float c2 = integral ? 2.0f * m : fmaf(2.0f, nf, 1.0f);
+            // g1' = 3.6 f + 0.1 below the fold, 3.7 - 3.6 f above; 0.1 at an integer m (c4)
+            const float g1p = selp(integral, 0.1f, fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f));
+            const float c2 = selp(integral, 2.0f * m, fmaf(2.0f, nf, 1.0f));
             const float4 G0 = GZc[slot * 2], G1 = GZc[slot * 2 + 1], AY = GZc[ns * 2], BY = GZc[ns * 2 + 1];
             const float4 wsv = WS[v * 32 + lane];
             const float w0 = wsv.x, w1 = wsv.y, w2 = wsv.z, w3 = wsv.w;
