@@ -150,6 +150,7 @@ struct srwcr_ctx {
     float *fMv = nullptr;
     cudaArray_t fMarr = nullptr;            // M as a 2-D layered array (pass 1 textureGather)
     float4 *fphi4 = nullptr;                // fp32 phi, one float4 (x, y, z, 0) per node
+    std::vector<NBox> h_nboxes;             // whole-volume boxes of the deterministic static counts
     cudaTextureObject_t ftexM = 0;
     int fWw = 8, fMinbW = 3;
     size_t fsmemw = 0;
@@ -444,6 +445,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     }
     std::vector<Item> its = make_items((int)c->z0, (int)c->z1);
     if (its.empty()) return SRWCR_OK;
+    for (const Item &it : make_items(0, g.nz)) c->h_nboxes.push_back(NBox{it.x0, it.xlen, it.y0, it.ylen, it.z0, it.zlen});
     for (const Item &it : its) {
         const int nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
         if (nxn > 32 || it.zlen > FZMAX) return SRWCR_OK;   // not eligible: round-1 passes
@@ -1262,6 +1264,37 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     }
     c->launches_per_eval = 6;  // prep (phi + x-max, y/z-max), pass 1, combine (+ D), pass 2, exact fix
     TRY(build_fast(c, nsm));
+    if (c->fast && !c->h_nboxes.empty() && !getenv("SRWCR_NONDET_N")) {
+        // the fast contexts replace N, Z and the moment shifts by the deterministic whole-volume
+        // computation (k_static_N): bitwise the same in every context, rank count and run
+        const size_t nb = c->h_nboxes.size();
+        NBox *d_nb = nullptr;
+        unsigned long long *Ni = nullptr, *Ci = nullptr;
+        CK(cudaMalloc(&d_nb, sizeof(NBox) * nb));
+        CK(cudaMemcpy(d_nb, c->h_nboxes.data(), sizeof(NBox) * nb, cudaMemcpyHostToDevice));
+        CK(cudaMalloc(&Ni, sizeof(unsigned long long) * 2 * RB));
+        CK(cudaMalloc(&Ci, sizeof(unsigned long long) * 4 * g.B));
+        CK(cudaMemsetAsync(Ni, 0, sizeof(unsigned long long) * 2 * RB, c->stream));
+        CK(cudaMemsetAsync(Ci, 0, sizeof(unsigned long long) * 4 * g.B, c->stream));
+        Tables t{};
+        for (int i = 0; i < 3; ++i) { t.cb[i] = c->cb[i]; t.cw[i] = c->cw[i]; t.sb[i] = c->sb[i]; t.sw[i] = c->sw[i]; }
+        const int sm = (int)(sizeof(double) * 132 * (size_t)g.B);
+        CK(cudaFuncSetAttribute(k_static_N, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        k_static_N<<<(unsigned)nb, 32, sm, c->stream>>>(c->F, c->M, d_nb, t, g, Ni, Ci);
+        CKL();
+        k_static_N_convert<<<296, 256, 0, c->stream>>>(Ni, Ci, c->Nlo, c->Nup, c->shiftc, RB, g.B);
+        CKL();
+        std::vector<double> nl(RB), nu(RB);
+        CK(cudaMemcpyAsync(nl.data(), c->Nlo, sizeof(double) * RB, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(nu.data(), c->Nup, sizeof(double) * RB, cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        double Z = 0;
+        for (long long i = 0; i < RB; ++i) Z += nl[i] + nu[i];
+        c->Z = Z;
+        cudaFree(d_nb);
+        cudaFree(Ni);
+        cudaFree(Ci);
+    }
     if (c->comm && c->nranks > 1) {
         // z-slab ranks: every rank computed the whole-volume static counts and moment shifts
         // (fp32 shared / fp64 global atomics: equal to rounding, not bitwise); rank 0's copy is

@@ -298,6 +298,153 @@ __global__ void k_lists(const unsigned *__restrict__ rec, const FItem *items, in
     }
 }
 
+// ------------------------------------------------------------------ create-time static counts
+// Deterministic whole-volume N_ra = sum_x w_r h_a(F) (Eq 5 / Eq 7; the quantised h of reading
+// c24) and the per-bin moment shifts c_b (conditional mean of g1(M) over bin b's mass at
+// Phi = 0, c28): one warp per box of one spatial cell, lines in a fixed order, per-line sums
+// over the warp by fixed-order shuffles in fp64, folded into an fp64 table per box in a
+// fixed order; per box an int64 flush (order-independent).  N rounds UP to units 2^-30, so a
+// positive N stays positive (the zero pattern, c13); the shift sums round to 2^-24.  Every
+// context, rank count and run gets bitwise the same N, Z and shifts.
+constexpr double N_UNIT = 1073741824.0;   // 2^30
+constexpr double C_UNIT = 16777216.0;     // 2^24
+
+struct NBox { int x0, xlen, y0, ylen, z0, zlen; };
+constexpr int NOBIN = 0x7fffffff;
+
+__device__ __forceinline__ double halving8d(const double (&v)[8], int lane) {   // value (lane >> 2)
+    double r4[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double send = (lane & 16) ? v[i] : v[i + 4], keep = (lane & 16) ? v[i + 4] : v[i];
+        r4[i] = keep + __shfl_xor_sync(FULL, send, 16);
+    }
+    double r2[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double send = (lane & 8) ? r4[i] : r4[i + 2], keep = (lane & 8) ? r4[i + 2] : r4[i];
+        r2[i] = keep + __shfl_xor_sync(FULL, send, 8);
+    }
+    const double send = (lane & 4) ? r2[0] : r2[1], keep = (lane & 4) ? r2[1] : r2[0];
+    double r = keep + __shfl_xor_sync(FULL, send, 4);
+    r += __shfl_xor_sync(FULL, r, 2);
+    r += __shfl_xor_sync(FULL, r, 1);
+    return r;
+}
+
+// smem: double T[B][8 (l ch)][16 (m n)], double C[B][4] (sum h_lo, h_lo g1, h_hi, h_hi g1)
+__global__ void __launch_bounds__(32) k_static_N(const float *__restrict__ F, const float *__restrict__ M,
+                                                 const NBox *boxes, Tables t, Geo g, unsigned long long *Ni,
+                                                 unsigned long long *Ci) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    double *T = reinterpret_cast<double *>(smem);
+    double *C = T + (size_t)g.B * 128;
+    const int lane = threadIdx.x;
+    const NBox bx = boxes[blockIdx.x];
+    const int B = g.B;
+    for (int i = lane; i < B * 132; i += 32) T[i] = 0.0;
+    __syncwarp();
+    const float Lm1 = (float)(g.L - 1);
+    for (int y = bx.y0; y < bx.y0 + bx.ylen; ++y) {
+        const float4 wy = t.sw[1][y];
+        for (int z = bx.z0; z < bx.z0 + bx.zlen; ++z) {
+            const float4 wz = t.sw[2][z];
+            // this lane's voxels of the line (x-chunks of 32)
+            int bin[4];
+            double hl[4], hh[4], gm[4];
+            float4 wx[4];
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const int x = bx.x0 + 32 * v + lane;
+                bin[v] = NOBIN;
+                hl[v] = hh[v] = gm[v] = 0.0;
+                wx[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (32 * v < bx.xlen && x < bx.x0 + bx.xlen) {
+                    const long long o = (long long)z * g.nxy + (long long)y * g.nx + x;
+                    const float Fv = F[o], Mv = M[o];
+                    const int a0 = min((int)Fv, g.L - 1);
+                    float lo, hi;
+                    parzen_pair_F(Fv - (float)a0, lo, hi);
+                    const float nm = fminf(floorf(Mv), Lm1);   // g1(M) = n + h(1 - f) (Eq 5)
+                    float mlo, mhi;
+                    parzen_pair(Mv - nm, mlo, mhi);
+                    bin[v] = a0;
+                    hl[v] = lo;
+                    hh[v] = hi;
+                    gm[v] = (double)nm + (double)mhi;
+                    wx[v] = t.sw[0][x];
+                }
+            }
+            for (;;) {   // the line's fixed bins, ascending
+                const int mine = min(min(bin[0], bin[1]), min(bin[2], bin[3]));
+                const int b = (int)__reduce_min_sync(FULL, (unsigned)mine);
+                if (b == NOBIN) break;
+                double e[8], c4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+                for (int k = 0; k < 8; ++k) e[k] = 0.0;
+#pragma unroll
+                for (int v = 0; v < 4; ++v)
+                    if (bin[v] == b) {
+#pragma unroll
+                        for (int l = 0; l < 4; ++l) {
+                            e[2 * l] += (double)f4(wx[v], l) * hl[v];
+                            e[2 * l + 1] += (double)f4(wx[v], l) * hh[v];
+                        }
+                        c4[0] += hl[v];
+                        c4[1] += hl[v] * gm[v];
+                        c4[2] += hh[v];
+                        c4[3] += hh[v] * gm[v];
+                        bin[v] = NOBIN;
+                    }
+                const double s = halving8d(e, lane);   // e[lane >> 2] summed over the warp
+                // lane: entry (l ch) = lane >> 2, m = lane & 3, and the 4 n
+                const int m = lane & 3;
+                const double wym = (double)f4(wy, m) * s;
+                double *Tp = T + (size_t)b * 128 + (lane >> 2) * 16 + m * 4;
+                Tp[0] += wym * (double)wz.x;
+                Tp[1] += wym * (double)wz.y;
+                Tp[2] += wym * (double)wz.z;
+                Tp[3] += wym * (double)wz.w;
+                double cs[8] = {c4[0], c4[1], c4[2], c4[3], 0.0, 0.0, 0.0, 0.0};
+                const double cr = halving8d(cs, lane);
+                if (lane < 16 && (lane & 3) == 0) C[(size_t)b * 4 + (lane >> 2)] += cr;
+                __syncwarp();
+            }
+        }
+    }
+    __syncwarp();
+    const int cx = t.sb[0][bx.x0], cy = t.sb[1][bx.y0], cz = t.sb[2][bx.z0];
+    for (int i = lane; i < B * 128; i += 32) {
+        const double v = T[i];
+        if (v == 0.0) continue;
+        const int b = i >> 7, e = (i >> 4) & 7, m = (i >> 2) & 3, n = i & 3;
+        const long long r = ((long long)(cz + n) * g.Ky + (cy + m)) * g.Kx + (cx + (e >> 1));
+        atomicAdd(Ni + (r * B + b) * 2 + (e & 1), (unsigned long long)(long long)ceil(v * N_UNIT));
+    }
+    for (int i = lane; i < B * 4; i += 32) {
+        const double v = C[i];
+        if (v != 0.0) atomicAdd(Ci + i, (unsigned long long)__double2ll_rn(v * C_UNIT));
+    }
+}
+
+// int64 -> Nlo / Nup (fp64) and the per-bin shifts
+__global__ void k_static_N_convert(const unsigned long long *Ni, const unsigned long long *Ci, double *Nlo,
+                                   double *Nup, float *shiftc, long long RB, int B) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < RB; i += (long long)gridDim.x * blockDim.x) {
+        Nlo[i] = (double)(long long)Ni[2 * i] * (1.0 / N_UNIT);
+        Nup[i] = (double)(long long)Ni[2 * i + 1] * (1.0 / N_UNIT);
+    }
+    if (blockIdx.x == 0)
+        for (int b = threadIdx.x; b < B; b += blockDim.x) {
+            double n = (double)(long long)Ci[4 * b], s = (double)(long long)Ci[4 * b + 1];
+            if (b > 0) {
+                n += (double)(long long)Ci[4 * (b - 1) + 2];
+                s += (double)(long long)Ci[4 * (b - 1) + 3];
+            }
+            shiftc[b] = n > 0.0 ? (float)(s / n) : (float)b;
+        }
+}
+
 // ------------------------------------------------------------------ per-eval prep
 // Blocks [0, nconv): fp64 params -> fp32 phi (node layers [zlo, zhi)).  Blocks after: one
 // warp per item, the interior flag: with umax_c = max |phi_c| over the item's node box
