@@ -35,6 +35,7 @@ constexpr double STAT_UNIT = 65536.0;      // binless second moments: int64 fixe
 constexpr double STAT_UNIT_S = 16777216.0; // binned first moments (shifted, small): units 2^-24
 constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
 constexpr int FZMAX = 128;                 // max slices per item
+constexpr int RRING = 4;                   // pass 1: slices in the per-warp record ring (3 ahead)
 
 struct FItem {
     int x0, xlen, y0, ylen, z0, zlen;
@@ -161,7 +162,7 @@ __device__ __forceinline__ float mfloor(float u, int &iu) {
 
 // shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
 struct P1Smem {
-    int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, total;
+    int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, rr, total;
 };
 __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     P1Smem o;
@@ -183,6 +184,7 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
     o.sh = take(S * 4);                  // float  SH[S]  per-slot shift
     o.ts = take(160 * 4);                // int    TS[]   touched-slot list of a round
+    o.rr = take(W * RRING * 64 * 4);     // unsigned RR[W][RRING][XV * 32] record ring (cp.async)
     o.total = off;
     return o;
 }
@@ -668,16 +670,23 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
 
     // ---- software pipeline: the records, gathers and coordinate flags of slice z+1 are in
     // flight while slice z is processed
-    // (the records two slices ahead: a load consumed one slice later is moved / spilled by
-    // the register allocator at the loop edge, which waited on it)
-    unsigned recn[XV], recn2[XV];
+    // The records of F go through a per-warp shared ring (cp.async, RRING slices ahead): an
+    // asynchronous copy holds no register, so no register copy of an in-flight load can
+    // wait for it at a loop edge (as a register prefetch did).
+    unsigned *RRw = reinterpret_cast<unsigned *>(smem + L.rr) + warp * (RRING * 32 * XV);
+    const unsigned rr_s = (unsigned)__cvta_generic_to_shared(RRw);
+    auto rec_copy = [&](int jz) {   // slice jz's records -> ring slot jz % RRING, one commit group
+#pragma unroll
+        for (int v = 0; v < XV; ++v)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rr_s + 4u * (unsigned)((jz % RRING) * 32 * XV + 32 * v + lane)),
+                         "l"(a.rec + (vb + jz * nxy + 32 * v)) : "memory");
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if constexpr (MOMENTS)
+        for (int j = 0; j < RRING - 1; ++j) rec_copy(min(j, zlen - 1));
     float mvn[XV];   // MODE 2: m of slice z+1
 #pragma unroll
-    for (int v = 0; v < XV; ++v) {
-        recn[v] = MOMENTS ? __ldg(a.rec + (vb + 32 * v)) : 0u;
-        recn2[v] = MOMENTS ? __ldg(a.rec + (vb + min(1, zlen - 1) * nxy + 32 * v)) : 0u;
-        mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + 32 * v)) : 0.f;
-    }
+    for (int v = 0; v < XV; ++v) mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + 32 * v)) : 0.f;
     float C[XV][8];
     VF<XV> T[3];
     int fl[XV];   // bit 0-2: clamped x, y, z (reading c2); bit 3: near an integer (exact path); bit 4: at rest
@@ -774,14 +783,14 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         // ---- this slice's inputs
         unsigned rc[XV];
         float mvc[XV];
+        if constexpr (MOMENTS) {   // slice iz's group is complete once at most RRING - 2 newer are pending
+            asm volatile("cp.async.wait_group %0;" ::"n"(RRING - 2) : "memory");
+            rec_copy(min(iz + RRING - 1, zlen - 1));   // into the slot read one slice ago
+        }
 #pragma unroll
         for (int v = 0; v < XV; ++v) {
-            rc[v] = recn[v];
+            rc[v] = MOMENTS ? RRw[(iz % RRING) * 32 * XV + 32 * v + lane] : 0u;
             mvc[v] = mvn[v];
-            if constexpr (MOMENTS) {
-                recn[v] = recn2[v];
-                recn2[v] = __ldg(a.rec + (vb + min(iz + 2, zlen - 1) * nxy + 32 * v));
-            }
             if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + 32 * v));
         }
         int flc[XV];
@@ -1048,6 +1057,8 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         __syncwarp();
         if constexpr (SAMPLE && SRWCR_GATHER_POS == 2) gather(z0 + izn);
     }
+    // ---- row end: no record copy may still land in the ring the next row reuses
+    if constexpr (MOMENTS) asm volatile("cp.async.wait_group 0;" ::: "memory");
     // ---- row end: binless -> K[ns]; lane j of the reduction holds value j = (l, ch, n)
     if constexpr (MOMENTS) {
         float vals[32];
