@@ -679,14 +679,14 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
 #pragma unroll
         for (int v = 0; v < XV; ++v)
             asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rr_s + 4u * (unsigned)((jz % RRING) * 32 * XV + 32 * v + lane)),
-                         "l"(a.rec + (vb + jz * nxy + 32 * v)) : "memory");
+                         "l"(a.rec + (vb + jz * nxy + (pl.xv[v] - pl.xv[0]))) : "memory");
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if constexpr (MOMENTS)
         for (int j = 0; j < RRING - 1; ++j) rec_copy(min(j, zlen - 1));
     float mvn[XV];   // MODE 2: m of slice z+1
 #pragma unroll
-    for (int v = 0; v < XV; ++v) mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + 32 * v)) : 0.f;
+    for (int v = 0; v < XV; ++v) mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + (pl.xv[v] - pl.xv[0]))) : 0.f;
     float C[XV][8];
     VF<XV> T[3];
     int fl[XV];   // bit 0-2: clamped x, y, z (reading c2); bit 3: near an integer (exact path); bit 4: at rest
@@ -791,7 +791,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         for (int v = 0; v < XV; ++v) {
             rc[v] = MOMENTS ? RRw[(iz % RRING) * 32 * XV + 32 * v + lane] : 0u;
             mvc[v] = mvn[v];
-            if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + 32 * v));
+            if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + (pl.xv[v] - pl.xv[0])));
         }
         int flc[XV];
         VF<XV> m, dgx, dgy, dgz;
@@ -914,9 +914,11 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         if constexpr (SAMPLE) {
 #pragma unroll
             for (int v = 0; v < XV; ++v) {   // (a padding lane samples its clamped neighbour: identical values)
-                if (!ABL(a, 1)) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
+                // (padding lanes -- x past the item's chunk -- store nothing: their slab index
+                // would be another item's voxel)
+                if (!ABL(a, 1) && pl.valid[v]) st_stream4(a.MG + (vb + iz * nxy + 32 * v),
                            make_float4(ex[v] ? -1.0f - m.v[v] : m.v[v], dgx.v[v], dgy.v[v], dgz.v[v]));
-                if (MODE == 1) __stcs(a.Mv + (vb + iz * nxy + 32 * v), m.v[v]);
+                if (MODE == 1 && pl.valid[v]) __stcs(a.Mv + (vb + iz * nxy + 32 * v), m.v[v]);
             }
         }
         if constexpr (!MOMENTS) {
@@ -1493,8 +1495,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
     float4 mgn[XV];
 #pragma unroll
     for (int v = 0; v < XV; ++v) {
-        recn[v] = __ldg(a.rec + (vb + 32 * v));
-        mgn[v] = ld_stream4(A2.MG + (vb + 32 * v));
+        recn[v] = __ldg(a.rec + (vb + (pl.xv[v] - pl.xv[0])));   // (padding lanes: the clamped voxel)
+        mgn[v] = ld_stream4(A2.MG + (vb + (pl.xv[v] - pl.xv[0])));
     }
     unsigned entn;
     {
@@ -1547,8 +1549,8 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
         for (int v = 0; v < XV; ++v) {
             rc[v] = recn[v];
             mg[v] = mgn[v];
-            recn[v] = __ldg(a.rec + (vb + (unsigned)izn * (unsigned)nxy + 32 * v));
-            mgn[v] = ld_stream4(A2.MG + (vb + (unsigned)izn * (unsigned)nxy + 32 * v));
+            recn[v] = __ldg(a.rec + (vb + (unsigned)izn * (unsigned)nxy + (pl.xv[v] - pl.xv[0])));
+            mgn[v] = ld_stream4(A2.MG + (vb + (unsigned)izn * (unsigned)nxy + (pl.xv[v] - pl.xv[0])));
         }
         // ---- retire the control layers this slice no longer reads
         const int bz = ZB[iz];

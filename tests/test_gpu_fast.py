@@ -217,3 +217,51 @@ def test_contexts_are_bitwise_identical():
     assert res[0][0] == res[1][0]
     for k in (1, 2, 3):
         assert np.array_equal(res[0][k], res[1][k])
+
+
+def _custom(F, M, cells, control_vox, bins, phi, seed=1):
+    import oracle as O
+    import paper_1804_05061_b200 as S
+    import synth
+    dims = (F.shape[2], F.shape[1], F.shape[0])
+    L = bins - 1
+    pb = O.Problem(dims=dims, L=L, delta=tuple(float(c) for c in control_vox), kcells=cells)
+    g = S.Srwcr(F, M, (1.0, 1.0, 1.0), bins, cells, tuple(float(c) for c in control_vox))
+    params = synth.make_params(g.params_shape, phi, seed)
+    return g, pb, O.normalize(F, L), O.normalize(M, L), params
+
+
+@pytest.mark.parametrize("phi", ["small", "large"])
+def test_fast_path_noisy_fixed_image_many_bins_per_line(phi):
+    """Uniform-noise F with 128 bins: every 64-voxel line touches ~50 fixed bins, so the line
+    fold runs its > 32-slot path and items carry ~128 slots; M a smooth ramp plus noise."""
+    import oracle as O
+    rng = np.random.default_rng(11)
+    nz, ny, nx = 24, 20, 128
+    F = rng.uniform(0, 1000, size=(nz, ny, nx)).astype(np.float32)
+    z, y, x = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    M = (3.0 * x + 2.0 * y + rng.normal(0, 20, size=x.shape)).astype(np.float32)
+    g, pb, Fn, Mn, params = _custom(F, M, (2, 1, 1), (5, 5, 5), 128, phi)
+    st = g.stats()
+    assert st["fast_path"] == 1 and st["fast_slots"] > 34
+    D, grad = g.eval(params)
+    g.close()
+    Do, go = O.eval_moments(pb, Fn, Mn, params)
+    _check(D, grad, Do, go)
+
+
+@pytest.mark.parametrize("dims,cells", [((100, 22, 9), (2, 2, 1)), ((70, 17, 31), (2, 1, 3)), ((96, 40, 5), (3, 2, 1))])
+def test_fast_path_ragged_cells_and_thin_z(dims, cells):
+    """Ragged x-cells (50, 35, 32 voxels: padding lanes in every line), odd y / z extents and
+    a z-extent below the 4 control taps: the fast passes against the oracle at Phi large
+    (samples leave the volume: the clamp variant)."""
+    import oracle as O
+    import synth
+    cfg = synth.config("C5", dims)
+    F, M = synth.make_pair("C5", 2, cfg["dims"])
+    g, pb, Fn, Mn, params = _custom(F, M, cells, (5, 5, 5), 64, "large", seed=2)
+    assert g.stats()["fast_path"] == 1
+    D, grad = g.eval(params)
+    g.close()
+    Do, go = O.eval_moments(pb, Fn, Mn, params)
+    _check(D, grad, Do, go)
