@@ -613,22 +613,15 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     CK(cudaMalloc(&c->gradi, sizeof(unsigned long long) * c->nparams));
     CK(cudaMemset(c->gradi, 0, sizeof(unsigned long long) * c->nparams));
     {
-        const int sm = (int)c->fsmem2;
+        // the attribute is per function and process-wide: every context sets the device maximum
+        // (a context-sized value would break the launches of an earlier context with larger
+        // tables, e.g. several z-slab ranks in one process)
+        const int sm = maxsm;
         const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
         if (XV == 2) {
             CK(cudaFuncSetAttribute(k_p2f<2, 512>, attr, sm));
             CK(cudaFuncSetAttribute(k_p2f<2, 384>, attr, sm));
             CK(cudaFuncSetAttribute(k_p2f<2, 256>, attr, sm));
-        } else {
-            CK(cudaFuncSetAttribute(k_p2f<1, 512>, attr, sm));
-            CK(cudaFuncSetAttribute(k_p2f<1, 384>, attr, sm));
-            CK(cudaFuncSetAttribute(k_p2f<1, 256>, attr, sm));
-        }
-    }
-    {
-        const int sm = (int)c->fsmem1;
-        const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
-        if (XV == 2) {
             CK(cudaFuncSetAttribute(k_p1f<2, 512>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<2, 384>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<2, 256>, attr, sm));
@@ -636,6 +629,9 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             CK(cudaFuncSetAttribute(k_p1f<2, 384, 2>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<2, 256, 2>, attr, sm));
         } else {
+            CK(cudaFuncSetAttribute(k_p2f<1, 512>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<1, 384>, attr, sm));
+            CK(cudaFuncSetAttribute(k_p2f<1, 256>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 512, 2>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 384, 2>, attr, sm));
             CK(cudaFuncSetAttribute(k_p1f<1, 256, 2>, attr, sm));
@@ -1279,7 +1275,9 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         Tables t{};
         for (int i = 0; i < 3; ++i) { t.cb[i] = c->cb[i]; t.cw[i] = c->cw[i]; t.sb[i] = c->sb[i]; t.sw[i] = c->sw[i]; }
         const int sm = (int)(sizeof(double) * 132 * (size_t)g.B);
-        CK(cudaFuncSetAttribute(k_static_N, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        int maxsm = 0;
+        CK(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev));
+        CK(cudaFuncSetAttribute(k_static_N, cudaFuncAttributeMaxDynamicSharedMemorySize, maxsm));
         k_static_N<<<(unsigned)nb, 32, sm, c->stream>>>(c->F, c->M, d_nb, t, g, Ni, Ci);
         CKL();
         k_static_N_convert<<<296, 256, 0, c->stream>>>(Ni, Ci, c->Nlo, c->Nup, c->shiftc, RB, g.B);
