@@ -35,7 +35,11 @@ constexpr double STAT_UNIT = 65536.0;      // binless second moments: int64 fixe
 constexpr double STAT_UNIT_S = 16777216.0; // binned first moments (shifted, small): units 2^-24
 constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
 constexpr int FZMAX = 128;                 // max slices per item
-constexpr int RRING = 4;                   // pass 1: slices in the per-warp record ring (3 ahead)
+constexpr int RRING = 4;
+#ifndef SRWCR_LTW
+#define SRWCR_LTW 8
+#endif
+constexpr int LTW = SRWCR_LTW;             // pass 1: words per slot of the int32 line table (C5 pass 1: 8 words 1.213 ms, 9: 1.235, 12: 1.233)                   // pass 1: slices in the per-warp record ring (3 ahead)
 
 struct FItem {
     int x0, xlen, y0, ylen, z0, zlen;
@@ -168,7 +172,7 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     P1Smem o;
     int off = 0;
     auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
-    o.lt = take(W * S * 9 * 4);          // int   LT[W][S][9]
+    o.lt = take(W * S * LTW * 4);        // int   LT[W][S][LTW]
     o.k = take(W * S * 32 * 4);          // float K[W][S][8 e][4 n]
     o.ct = take(S * 128 * 4);            // float CT[S][4 m][8 e][4 n]
     o.pl = take(W * 32 * 16);            // float4 PL[W][32]   layer node buffer
@@ -580,7 +584,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     constexpr bool SAMPLE = MODE != 2, MOMENTS = MODE != 1;
     const Geo &g = a.g;
     const int S = a.S, ns = it.nslots, dummy = it.nslots + 1;
-    int *LTw = reinterpret_cast<int *>(smem + L.lt) + warp * S * 9;
+    int *LTw = reinterpret_cast<int *>(smem + L.lt) + warp * S * LTW;
     float *Kw = reinterpret_cast<float *>(smem + L.k) + warp * S * 32;
     float4 *PLw = reinterpret_cast<float4 *>(smem + L.pl) + warp * 32;
     float *LMw = reinterpret_cast<float *>(smem + L.lm) + warp * 16;
@@ -983,7 +987,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 if (lane == 0) {
                     // padding voxels added a bare offset each: the list counts valid voxels only
                     const int pad = (32 * XV - it.xlen) * MAGIC_I;
-                    const unsigned row = lt_s + (unsigned)slot[0] * 36u;
+                    const unsigned row = lt_s + (unsigned)slot[0] * (4u * LTW);
 #pragma unroll
                     for (int e = 0; e < 8; ++e) red_s32(row + 4u * e, red8[e] - pad);
                 }
@@ -1010,7 +1014,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                     const VF<XV> xa = vadd(vfma(va, wr[k], dith), vmagic), xb = vadd(vfma(vb, wr[k], dith), vmagic);
 #pragma unroll
                     for (int v = 0; v < XV; ++v) {
-                        const unsigned ad = pl.lts[k] + (unsigned)slot[v] * 36u;
+                        const unsigned ad = pl.lts[k] + (unsigned)slot[v] * (4u * LTW);
                         red_s32(ad, __float_as_int(xa.v[v]));
                         red_s32(ad + db, __float_as_int(xb.v[v]));
                     }
@@ -1032,7 +1036,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 const int s = (int)(ent & 0xFFu);
                 const int nadd = (int)((ent >> nsh) & 0xFFu);
                 FCHECK((s < ns || s == dummy) && nadd <= 32 * XV);
-                const unsigned la = lt_s + (unsigned)(s * 36 + e * 4);
+                const unsigned la = lt_s + (unsigned)(s * (4 * LTW) + e * 4);
                 int raw;
                 asm volatile("ld.shared.u32 %0, [%1];" : "=r"(raw) : "r"(la));
                 asm volatile("st.shared.u32 [%0], %1;" ::"r"(la), "r"(0) : "memory");
@@ -1120,7 +1124,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
     float *SH = reinterpret_cast<float *>(smem + L.sh);
     int *TS = reinterpret_cast<int *>(smem + L.ts);
 
-    for (int i = threadIdx.x; i < W * S * 9; i += blockDim.x) LT[i] = 0;
+    for (int i = threadIdx.x; i < W * S * LTW; i += blockDim.x) LT[i] = 0;
     for (int i = threadIdx.x; i < W * S * 32; i += blockDim.x) K[i] = 0.f;
     for (int i = threadIdx.x; i < (ns + 1) * 128; i += blockDim.x) CT[i] = 0.f;
     for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {
@@ -1152,7 +1156,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
             const int l = (k + q4) & 3;
-            pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * 9) + 8u * (unsigned)l + 4u * ((lane >> 2) & 1);
+            pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * LTW) + 8u * (unsigned)l + 4u * ((lane >> 2) & 1);
         }
     };
     __syncthreads();
