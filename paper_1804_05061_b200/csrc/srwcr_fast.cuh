@@ -35,11 +35,12 @@ constexpr double STAT_UNIT = 65536.0;      // binless second moments: int64 fixe
 constexpr double STAT_UNIT_S = 16777216.0; // binned first moments (shifted, small): units 2^-24
 constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
 constexpr int FZMAX = 128;                 // max slices per item
-constexpr int RRING = 4;
+constexpr int RRING = 4;                   // pass 1: slices in the per-warp record ring (3 ahead)
 #ifndef SRWCR_LTW
 #define SRWCR_LTW 8
 #endif
-constexpr int LTW = SRWCR_LTW;             // pass 1: words per slot of the int32 line table (C5 pass 1: 8 words 1.213 ms, 9: 1.235, 12: 1.233)                   // pass 1: slices in the per-warp record ring (3 ahead)
+// pass 1: words per slot of the int32 line table (C5 pass 1: 8 words 1.213 ms, 9: 1.235, 12: 1.233)
+constexpr int LTW = SRWCR_LTW;
 
 struct FItem {
     int x0, xlen, y0, ylen, z0, zlen;
