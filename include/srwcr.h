@@ -61,8 +61,9 @@ typedef struct {
     int32_t struct_size;       /* = sizeof(srwcr_options); set by srwcr_default_options */
     int32_t orientation;       /* 0 = moving image is the estimated image B (Eq 18-19/27).
                                   1 = moving image is the model image A (Eq 20-21, App. II Eq 31;
-                                  readings c4, c23): at most 83 intensity bins (SRWCR_ENOTSUP
-                                  above); other values SRWCR_EINVAL */
+                                  readings c4, c23); above ~64 bins its per-item slot
+                                  tables need fewer warps per CTA (slower); other values
+                                  SRWCR_EINVAL */
     int32_t inputs_normalized; /* 1: fixed/moving already in [0, L]; 0: min-max normalise */
     int32_t device;            /* CUDA device ordinal */
     int32_t nranks, rank;      /* z-slab decomposition: rank r owns slab srwcr_plan_slab(r) */
@@ -92,7 +93,7 @@ srwcr_status srwcr_default_options(srwcr_options *opt);
  * replayed as one CUDA graph when options.use_graph applies.)
  *   dims[3]            Nx, Ny, Nz (Nz = 1: 2-D); each >= 1, Nx, Ny >= 2, Nx Ny Nz < 2^31
  *   spacing_mm[3]      voxel spacing (> 0)
- *   intensity_bins     L + 1, in [2, 128] (paper: L = 31); orientation 1: <= 83
+ *   intensity_bins     L + 1, in [2, 128] (paper: L = 31), both orientations
  *   spatial_bins[3]    k cells per axis (>= 0; 0 = one region on that axis)
  *   control_spacing_mm[3]  control-node spacing (> 0); paper: delta = [5,5,5]
  *   opt                NULL = defaults

@@ -780,8 +780,6 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
                     (long long)(dims[0] * dims[1] * dims[2]));
     if (bins < 2 || bins > 128) return fail(c, SRWCR_EINVAL, "intensity_bins must be in [2, 128], got %d", bins);
     if (o.orientation != 0 && o.orientation != 1) return fail(c, SRWCR_EINVAL, "orientation must be 0 or 1");
-    if (o.orientation == 1 && bins > 83)
-        return fail(c, SRWCR_ENOTSUP, "orientation 1 (moving as model image) supports at most 83 intensity bins, got %d", bins);
     if (o.nranks < 1 || o.rank < 0 || o.rank >= o.nranks) return fail(c, SRWCR_EINVAL, "rank/nranks out of range");
     for (int i = 0; i < 3; ++i) {
         if (!(sp[i] > 0)) return fail(c, SRWCR_EINVAL, "spacing_mm[%d] must be > 0", i);
@@ -1173,7 +1171,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     // shared memory and warps per CTA of each pass: the largest W in {16, 12, 8, 6, 4} that fits
     int maxsm = 0;
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
-    const int Wc[8] = {32, 24, 20, 16, 12, 8, 6, 4};
+    // (2 and 1: orientation 1 at > 83 bins, whose 2 (L) slots per item fill the tables)
+    const int Wc[10] = {32, 24, 20, 16, 12, 8, 6, 4, 2, 1};
     // a CTA's warps own whole rows of its item: no more warps than the tallest item has
     // rows (fine spatial lattices -- small items -- then fit several CTAs per SM)
     auto wcap = [&](const std::vector<Item> &its) {
@@ -1196,7 +1195,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         const size_t xrn = c->MC ? MC_XRN : 4, zrn = c->MC ? c->zrn : 4, gys = c->MC ? MC_XRN + 1 : GYS;
         const size_t s2 = sizeof(float4) * (size_t)W * c->S2 * (gys + xrn / 4) +
                           sizeof(float) * (4 * zrn * xrn * (size_t)c->S2 + (c->S2 + 1) + 8 * zrn * xrn + W * 192 + (o.orientation ? g.B : 0)) +
-                          (((o.orientation ? 3 * (g.B + 2) : g.B) + 15) & ~15) +
+                          2 * (((o.orientation ? 3 * (g.B + 2) : g.B) + 7) & ~7) +
                           sizeof(float) * npmax;
         if (!c->W2 && W <= w2max && (int)s2 <= maxsm) { c->W2 = W; c->smem2 = s2; }
     }

@@ -276,11 +276,12 @@ __device__ __forceinline__ int select_bit(unsigned w, int r) {
     }
     return pos;
 }
-// the j-th set bit of a (<= 128-bit) mask, or -1
-__device__ __forceinline__ int mask_select(const unsigned (&bits)[4], int nw, int j) {
+// the j-th set bit of a (<= 32 NWD-bit) mask, or -1
+template <int NWD>
+__device__ __forceinline__ int mask_select(const unsigned (&bits)[NWD], int nw, int j) {
     int pos = -1, base = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < NWD; ++k) {
         if (k < nw) {
             const int c = __popc(bits[k]);
             if (pos < 0 && j >= base && j < base + c) pos = 32 * k + select_bit(bits[k], j - base);
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
     const int ns = it.nslots;                       // list entries (ORI 1: every bin)
     const int nsl = ORI ? 2 * ns : ns + (MC ? 1 : 0); // slots (ORI 1: two groups per bin; MC: + binless)
     const int nwords = (nsl + 31) >> 5;
+    constexpr int NW = ORI ? 8 : 4;                 // slot-mask words (ORI 1: 2 slots per bin, B <= 128)
 
     for (int i = threadIdx.x; i < ltsz; i += blockDim.x) LT[i] = 0;
     for (int i = threadIdx.x; i < W * S * KS; i += blockDim.x) K[i] = 0.f;
@@ -477,14 +479,16 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
             for (int n = 0; n < 4; ++n) ffd_layer<XV>(a.phi, g, gzl + n, cby, cwy, xn0, nxn, relx, cwx, lane, U[n]);
         }
         float bacc = 0.f;
-        unsigned wmask[4] = {0u, 0u, 0u, 0u};
+        unsigned wmask[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k) wmask[k] = 0u;
         // fold the column table with the row's y-weights into the cell table (MC: at z-region
         // offset lcz -- called at every crossed z-cell of a multi-cell item and at row end)
         // (MC only: a by-reference lambda in the coarse kernel costs it registers)
         auto foldK = [&](int lcz) {
           if constexpr (MC) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < NW; ++k) {
                 unsigned bw = k < nwords ? wmask[k] : 0u;
                 wmask[k] = 0u;
                 while (bw) {
@@ -769,13 +773,15 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
             }
             if (uniform && ORI) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < NW; ++k)
                     if (((slot[0] + gi) >> 5) == k) wmask[k] |= 1u << ((slot[0] + gi) & 31);
             }
             }
             // ---- fold the line into the warp's column table, 4 slots per instruction:
             //      K[slot][ent][n] += wz_n * LT[slot][ent]
-            unsigned bits[4] = {0u, 0u, 0u, 0u};
+            unsigned bits[NW];
+#pragma unroll
+            for (int k = 0; k < NW; ++k) bits[k] = 0u;
             int cnt = 0;
             if (MC && !STATIC) {   // the binless slot is touched by every line
                 bits[ns >> 5] |= 1u << (ns & 31);
@@ -784,11 +790,11 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
             }
             if (uniform && !ORI) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
+                for (int k = 0; k < NW; ++k)
                     if ((slot[0] >> 5) == k) wmask[k] |= 1u << (slot[0] & 31);
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < NW; ++k) {
                 if (k < nwords && !uniform) {
                     unsigned mine = 0u;
 #pragma unroll
@@ -803,7 +809,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
             if (!uniform) {
                 cnt = 0;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) cnt += __popc(bits[k]);
+                for (int k = 0; k < NW; ++k) cnt += __popc(bits[k]);
             }
             const int nwf = MC ? max(nwords, (ns >> 5) + 1) : nwords;
             __syncwarp();
@@ -839,7 +845,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 4) : 1) k_pass1(
             foldK(lczr);
         } else {
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < NW; ++k) {
                 unsigned bw = k < nwords ? wmask[k] : 0u;
                 while (bw) {
                     const int s = 32 * k + __ffs(bw) - 1;
@@ -1326,8 +1332,8 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 5) : 1) k_pass2(
     float4 *GZ = GY + W * GB * GYSV;                              // [W][GB] (MC: [W][GB][XRN] floats)
     float *gl = reinterpret_cast<float *>(GZ + W * GB * (XRN / 4)); // [4 ZRN XRN][GB] gamma of the regions
     int *gbins = reinterpret_cast<int *>(gl + 4 * ZRN * XRN * GB); // [GB+1] the bin list, count
-    unsigned char *gmap = reinterpret_cast<unsigned char *>(gbins + GB + 1);  // [B] bin -> list index
-    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 15) & ~15)); // [4 ZRN XRN]
+    unsigned short *gmap = reinterpret_cast<unsigned short *>(gbins + GB + 1);  // [B] bin -> list index
+    float *al = reinterpret_cast<float *>(gmap + (((ORI ? 3 * (B + 2) : B) + 7) & ~7)); // [4 ZRN XRN]
     float *bl = al + 4 * ZRN * XRN;                               // [4 ZRN XRN]
     float *shc2 = bl + 4 * ZRN * XRN;                             // [B] (ORI 1) the bins' moment shifts
     float *RB = shc2 + (ORI ? B : 0);                             // [W][3][64] retiring-layer row buffer
@@ -1339,7 +1345,7 @@ __global__ void __launch_bounds__(MAXT, MAXT <= 256 ? (MC ? 3 : 5) : 1) k_pass2(
     for (int i = threadIdx.x; i < nb2; i += blockDim.x) {
         const int b = a.slotbins[it.slot_off + i];
         gbins[i] = b;
-        gmap[b] = (unsigned char)i;
+        gmap[b] = (unsigned short)i;
     }
     __syncthreads();
     // region (n, m, l) of the item (l, n: relative x-, z-regions) at index (n * 4 + m) * XRN + l
