@@ -64,3 +64,25 @@ def test_orientation1_bin_counts_near_the_limit(bins):
     g.close()
     assert rel(D, Do) <= D_TOL, (D, Do)
     assert rel_l2(grad, go) <= G_TOL, rel_l2(grad, go)
+
+
+def test_orientation1_model_bin_assignment_contract():
+    """F2's bin-assignment contract (DESIGN c25): in orientation 1 the model bin of a voxel is
+    n(m) = min(floor m, L-1) of the fp32 sample m (Eq 5 applied to A = M(T(x))); where fp64 m
+    lies within fp32 rounding of an integer the voxel is decided by the fp64 exact path.  The
+    dumped per-voxel m (pass 1) against the oracle's fp64 warp: bins differ only next to an
+    integer, and only rarely."""
+    g, pb, Fn, Mn, params = problem("C3", 1, params_kind="small", orientation=1)
+    g.eval(params)
+    mg = g.debug_dump("warped").reshape(pb.dims[2], pb.dims[1], pb.dims[0], 4)
+    g.close()
+    m_o, _ = O.warp(pb, Mn, params)
+    L = pb.L
+    m_g = np.where(mg[..., 0] < 0, -1.0 - mg[..., 0], mg[..., 0])
+    n_g = np.minimum(np.floor(m_g), L - 1)
+    n_o = np.minimum(np.floor(m_o), L - 1)
+    mism = n_g != n_o
+    near = np.abs(m_o - np.round(m_o)) < 1e-4
+    assert not np.any(mism & ~near)
+    assert int(mism.sum()) <= 1e-4 * m_o.size
+    assert np.abs(m_g - m_o).max() < 1e-3
