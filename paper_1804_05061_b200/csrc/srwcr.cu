@@ -149,6 +149,10 @@ struct srwcr_ctx {
     bool fsplit = false;
     float *fMv = nullptr;
     cudaArray_t fMarr = nullptr;            // M as a 2-D layered array (pass 1 textureGather)
+    // pipelined host-buffer evaluation of the fast passes: pass 1 parts [fp1_b[j], fp1_b[j+1])
+    // need params layers [0, fp1_l[j]); after pass-2 part j the gradient layers [0, fp2_l[j])
+    // are final
+    std::vector<int> fp1_b, fp1_l, fp2_b, fp2_l;
     float4 *fphi4 = nullptr;                // fp32 phi, one float4 (x, y, z, 0) per node
     std::vector<NBox> h_nboxes;             // whole-volume boxes of the deterministic static counts
     cudaTextureObject_t ftexM = 0;
@@ -583,6 +587,36 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     c->nfitems = (int)n;
     c->fsmem1 = p1_smem(W, S).total;
     c->h_fitems = fi;
+    // pipelined host-buffer evaluation (one rank): pass 1 in parts of one wave, one wave, the
+    // rest (the first params upload part is as small as one wave's layers); pass 2 as all but
+    // three waves, then one wave at a time (the gradient layers final after each part go back
+    // while the next runs).  Items are ordered by z, so both boundaries are layer prefixes.
+    if (c->nranks == 1 && !getenv("SRWCR_NOPIPE")) {
+        int wave = nsm;
+        if (const char *e = getenv("SRWCR_PIPE_WAVE")) wave = std::max(1, atoi(e));   // tests: small volumes
+        const int nn = (int)n;
+        if (nn >= 5 * wave) {
+            std::vector<int> b = {0, wave, 2 * wave, nn}, l;
+            for (size_t j = 0; j + 1 < b.size(); ++j) {
+                int hi = 0;
+                for (int i = 0; i < b[j + 1]; ++i) hi = std::max(hi, c->h_cb[2][fi[i].z0 + fi[i].zlen - 1] + 4);
+                l.push_back(std::min(hi, g.GzExt));
+            }
+            l.back() = g.GzExt;
+            c->fp1_b = b;
+            c->fp1_l = l;
+            std::vector<int> b2 = {0, nn - 3 * wave, nn - 2 * wave, nn - wave, nn}, l2;
+            for (size_t j = 0; j + 1 < b2.size(); ++j) {
+                int lo = g.GzExt;
+                for (int i = b2[j + 1]; i < nn; ++i) lo = std::min(lo, c->h_cb[2][fi[i].z0]);
+                l2.push_back(lo);
+            }
+            l2.back() = g.GzExt;
+            for (size_t j = 1; j < l2.size(); ++j) l2[j] = std::max(l2[j], l2[j - 1]);
+            c->fp2_b = b2;
+            c->fp2_l = l2;
+        }
+    }
     // split pass 1 (SRWCR_SPLIT=0/1 overrides the default).  Measured on C5 (c18/c19): the
     // halves take 0.82 ms (k_p1w) + 0.87 ms (k_p1f MODE 2) against 1.60 ms fused: off
     c->fsplit = false;
@@ -728,6 +762,37 @@ static srwcr_status launch_fast_prep(srwcr_ctx *c, const double *pd) {
 }
 
 // fast pass 2 (+ the fp64 exact-path voxels, + the int64 -> fp64 gradient conversion)
+static F2Args fast_pass2_args(srwcr_ctx *c) {
+    F2Args A{};
+    A.f = fast_args(c);
+    A.MG = c->MG;
+    A.alpha = c->alpha; A.beta = c->beta; A.gamma = c->gamma;
+    A.gbound = c->Dout + 2;
+    A.dxz = c->fdxz;
+    A.gradi = c->gradi;
+    A.xlist = c->xlist; A.xcount = c->xcount; A.xcap = c->xcap;
+    A.npmax = c->fnpmax;
+    A.f.W = c->fW2;
+    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax);
+    return A;
+}
+static srwcr_status launch_fast_p2f(srwcr_ctx *c, const F2Args &A0, int i0, int n) {
+    if (n <= 0) return SRWCR_OK;
+    F2Args A = A0;
+    A.f.i0 = i0;
+    const int T = 32 * c->fW2;
+    if (c->fXV == 2) {
+        if (T > 384) k_p2f<2, 512><<<n, T, c->fsmem2, c->stream>>>(A);
+        else if (T > 256) k_p2f<2, 384><<<n, T, c->fsmem2, c->stream>>>(A);
+        else k_p2f<2, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+    } else {
+        if (T > 384) k_p2f<1, 512><<<n, T, c->fsmem2, c->stream>>>(A);
+        else if (T > 256) k_p2f<1, 384><<<n, T, c->fsmem2, c->stream>>>(A);
+        else k_p2f<1, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+    }
+    CKL();
+    return SRWCR_OK;
+}
 static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad, bool reduce_int64 = false) {
     F2Args A{};
     A.f = fast_args(c);
@@ -1570,6 +1635,100 @@ static srwcr_status eval_host_pipelined(srwcr_ctx *c, const double *params, doub
     return eval_finish(c, value);
 }
 
+// Host-buffer evaluation of the fast passes on one rank with the copies overlapped: params
+// go up in parts, each part's fp32 conversion, interior flags and pass-1 items starting as soon
+// as it has arrived; pass 2 runs in parts, and after each part the gradient layers no later
+// item touches (their deferred exact-path voxels fixed first) are converted and go back while
+// the next part runs.  The same kernels as srwcr_eval on device buffers, on item ranges.
+static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params, double *value, double *grad) {
+    if (c->poisoned) return fail(c, SRWCR_ESTATE, "context poisoned by an earlier CUDA error");
+    CK(cudaSetDevice(c->dev));
+    const Geo &g = c->g;
+    const size_t plane = (size_t)g.Gx * g.Gy, cs = plane * g.GzExt;
+    auto copy_layers = [&](double *dst, const double *src, int l0, int l1, cudaMemcpyKind kind, cudaStream_t st) {
+        for (int k = 0; k < g.ndim; ++k)
+            if (l1 > l0)
+                CK(cudaMemcpyAsync(dst + k * cs + l0 * plane, src + k * cs + l0 * plane, sizeof(double) * plane * (l1 - l0),
+                                   kind, st));
+        return SRWCR_OK;
+    };
+    Tables t{};
+    for (int i = 0; i < 3; ++i) { t.cb[i] = c->cb[i]; t.cw[i] = c->cw[i]; t.sb[i] = c->sb[i]; t.sw[i] = c->sw[i]; }
+    // ---- params in parts (copy stream), each followed by its prep and pass-1 items
+    CK(cudaEventRecord(c->pev[3], c->stream));
+    CK(cudaStreamWaitEvent(c->cstream, c->pev[3], 0));
+    c->cur_params = c->params64;
+    const int np1 = (int)c->fp1_l.size();
+    int lo = 0;
+    for (int j = 0; j < np1; ++j) {
+        const int hi = c->fp1_l[j];
+        TRY(copy_layers(c->params64, params, lo, hi, cudaMemcpyHostToDevice, c->cstream));
+        CK(cudaEventRecord(c->pev[0], c->cstream));
+        CK(cudaStreamWaitEvent(c->stream, c->pev[0], 0));
+        const int b0 = c->fp1_b[j], nb = c->fp1_b[j + 1] - b0;
+        const int zl = std::max(lo, c->pz0), zh = j + 1 == np1 ? c->pz1 : std::min(hi, c->pz1);
+        const int nconv = zh > zl ? 296 : 0;
+        k_fprep<<<(unsigned)(nconv + nb), 256, 0, c->stream>>>(c->params64, c->fphi4, g, zl, std::max(zl, zh), nconv,
+                                                             c->fitems + b0, nb, t, c->fiflag + b0);
+        CKL();
+        TRY(launch_fast_pass1(c, b0, nb, false));
+        lo = hi;
+    }
+    k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c), (long long)c->R * c->g.B * 2);
+    CKL();
+    TRY(run_combine(c));
+    CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    if (grad) {
+        const F2Args A = fast_pass2_args(c);
+        PassArgs pa = pass_args(c);
+        pa.invZ = 1.f;
+        pa.gradi = c->gradi;
+        pa.gbound = c->Dout + 2;
+        pa.dxz = c->fdxz;
+        pa.xbeg = c->xbeg;
+        CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
+        CK(cudaMemsetAsync(c->xbeg, 0, sizeof(int), c->stream));
+        const int np2 = (int)c->fp2_l.size();
+        int done = 0;
+        for (int j = 0; j < np2; ++j) {
+            const bool last = j + 1 == np2;
+            TRY(launch_fast_p2f(c, A, c->fp2_b[j], c->fp2_b[j + 1] - c->fp2_b[j]));
+            pa.xmode = last ? 0 : 1;   // a list overflow scans the slab in the last part only
+            k_exact_fix<0><<<1184, 128, 0, c->stream>>>(pa);
+            CKL();
+            const int hi = c->fp2_l[j];
+            if (hi > done) {
+                k_grad_convert_layers<<<592, 256, 0, c->stream>>>(c->gradi, c->grad64, (long long)plane, (long long)cs, g.ndim,
+                                                                  done, hi, c->Dout + 2, c->fdxz, 1.0 / c->Z);
+                CKL();
+            }
+            if (last) {
+                TRY(copy_layers(grad, c->grad64, done, hi, cudaMemcpyDeviceToHost, c->stream));
+            } else {
+                CK(cudaMemcpyAsync(c->xbeg, c->xcount, sizeof(int), cudaMemcpyDeviceToDevice, c->stream));
+                CK(cudaEventRecord(c->pev[2], c->stream));
+                CK(cudaStreamWaitEvent(c->cstream, c->pev[2], 0));
+                TRY(copy_layers(grad, c->grad64, done, hi, cudaMemcpyDeviceToHost, c->cstream));
+            }
+            done = std::max(done, hi);
+        }
+        CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->cstream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (grad) {
+        int xc = 0;
+        memcpy(&xc, c->pinned + 2, sizeof(int));
+        if (xc > c->xcap) {
+            // list overflow: voxels of layers already converted were fixed by the last part's
+            // scan after their conversion -- rare; evaluate again without the parts
+            TRY(eval_begin_impl(c, params));
+            return eval_end_impl(c, value, grad, true);
+        }
+    }
+    return eval_finish(c, value);
+}
+
 extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
     if (!c) return SRWCR_EINVAL;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
@@ -1579,6 +1738,9 @@ extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *v
     if (!c->comm && !c->timing && !c->poisoned && !c->fast && params && (c->p1_split > 0 || c->p2_split > 0) &&
         !is_device_ptr(params) && (!grad || !is_device_ptr(grad)))
         return eval_host_pipelined(c, params, value, grad);
+    if (!c->comm && !c->timing && !c->poisoned && c->fast && params && !c->fp1_b.empty() && !is_device_ptr(params) &&
+        (!grad || !is_device_ptr(grad)) && !getenv("SRWCR_NOPIPE"))
+        return eval_host_pipelined_fast(c, params, value, grad);
     TRY(eval_begin_impl(c, params));
     if (!c->fast) TRY(allreduce(c, c->SQ, stats_count(c)));   // (fast: int64 sum inside eval_begin)
     return eval_end_impl(c, value, grad, true);

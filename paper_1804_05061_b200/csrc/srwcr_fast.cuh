@@ -1730,4 +1730,18 @@ __global__ void k_grad_convert(unsigned long long *__restrict__ gi, double *__re
     }
 }
 
+// int64 -> fp64 gradient for the node layers [l0, l1) of every component (the pipelined
+// host-buffer evaluation converts and copies back the layers no later item touches)
+__global__ void k_grad_convert_layers(unsigned long long *__restrict__ gi, double *__restrict__ gd, long long plane,
+                                      long long cs, int ndim, int l0, int l1, const double *gbound, float dxz,
+                                      double invZ) {
+    const double s = ldexp(invZ, -grad_shift(*gbound, dxz));
+    const long long per = (long long)(l1 - l0) * plane, n = per * ndim;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const long long c = k / per, i = c * cs + (long long)l0 * plane + (k - c * per);
+        gd[i] = (double)(long long)gi[i] * s;
+        gi[i] = 0ull;
+    }
+}
+
 }  // namespace srwcr

@@ -310,3 +310,24 @@ def test_fast_path_slabs_on_one_gpu(P):
     assert np.linalg.norm(gsum - grad1) / np.linalg.norm(grad1) <= 1e-5
     Do, go = O.eval_moments(pb, Fn, Mn, params)
     _check(D, gsum, Do, go)
+
+
+@pytest.mark.parametrize("phi", ["small", "large"])
+def test_pipelined_host_evaluation_bitwise(phi, monkeypatch):
+    """Host params / gradient buffers: the parts-pipelined evaluation (params uploaded in parts
+    overlapped with pass 1, gradient layers converted and copied back while later pass-2 parts
+    run; parts forced small with SRWCR_PIPE_WAVE) runs the same kernels on item ranges, with
+    integer sums: bitwise the device-buffer evaluation."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("SRWCR_PIPE_WAVE", "16")
+    g, pb, Fn, Mn, params = _case("C5", 1, phi)
+    st = g.stats()
+    assert st["fast_path"] == 1
+    D1, g1 = g.eval(params)                      # host buffers: pipelined
+    pt = torch.from_numpy(params).cuda()
+    gt = torch.empty_like(pt)
+    D2, _ = g.eval(pt, grad=gt)                  # device buffers: one launch per kernel (graph)
+    D3, g3 = g.eval(params)
+    g.close()
+    assert D1 == D2 == D3
+    assert np.array_equal(g1, gt.cpu().numpy()) and np.array_equal(g1, g3)
