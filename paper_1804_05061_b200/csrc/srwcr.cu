@@ -595,8 +595,11 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
         int wave = nsm;
         if (const char *e = getenv("SRWCR_PIPE_WAVE")) wave = std::max(1, atoi(e));   // tests: small volumes
         const int nn = (int)n;
-        if (nn >= 5 * wave) {
-            std::vector<int> b = {0, wave, 2 * wave, nn}, l;
+        if (nn >= 6 * wave) {
+            const int np = std::min(4, std::max(2, atoi(getenv("SRWCR_PIPE_P1") ? getenv("SRWCR_PIPE_P1") : "3")));   // C5 e2e: 3 parts 371, 4 parts 364 evals/s
+            std::vector<int> b = {0}, l;
+            for (int k = 1; k < np; ++k) b.push_back(k * wave);
+            b.push_back(nn);
             for (size_t j = 0; j + 1 < b.size(); ++j) {
                 int hi = 0;
                 for (int i = 0; i < b[j + 1]; ++i) hi = std::max(hi, c->h_cb[2][fi[i].z0 + fi[i].zlen - 1] + 4);
@@ -605,7 +608,10 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             l.back() = g.GzExt;
             c->fp1_b = b;
             c->fp1_l = l;
-            std::vector<int> b2 = {0, nn - 3 * wave, nn - 2 * wave, nn - wave, nn}, l2;
+            const int np2 = std::min(5, std::max(2, atoi(getenv("SRWCR_PIPE_P2") ? getenv("SRWCR_PIPE_P2") : "4")));
+            std::vector<int> b2 = {0}, l2;
+            for (int k = np2 - 1; k >= 1; --k) b2.push_back(nn - k * wave);
+            b2.push_back(nn);
             for (size_t j = 0; j + 1 < b2.size(); ++j) {
                 int lo = g.GzExt;
                 for (int i = b2[j + 1]; i < nn; ++i) lo = std::min(lo, c->h_cb[2][fi[i].z0]);
