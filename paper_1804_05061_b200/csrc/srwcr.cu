@@ -1727,7 +1727,9 @@ static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params,
         memcpy(&xc, c->pinned + 2, sizeof(int));
         if (xc > c->xcap) {
             // list overflow: voxels of layers already converted were fixed by the last part's
-            // scan after their conversion -- rare; evaluate again without the parts
+            // scan after their conversion (their int64 adds are still in gradi) -- rare;
+            // clear the int64 gradient and evaluate again without the parts
+            CK(cudaMemsetAsync(c->gradi, 0, sizeof(unsigned long long) * c->nparams, c->stream));
             TRY(eval_begin_impl(c, params));
             return eval_end_impl(c, value, grad, true);
         }
