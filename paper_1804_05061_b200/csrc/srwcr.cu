@@ -428,6 +428,10 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     // z-slab decomposition whose slab boundaries fall on spatial z-cells runs exactly the items
     // of the single-GPU decomposition that lie in its slab (bitwise-equal statistics sums)
     int ymax = 32, zmax = FZMAX;
+    // at least 1.5 items per SM over the whole volume (times imul: SRWCR_FITEMS_MUL, experiments
+    // with the z-slab decomposition, where each rank gets 1/P of them)
+    int imul = 1;
+    if (const char *e = getenv("SRWCR_FITEMS_MUL")) imul = std::max(1, atoi(e));
     auto make_items = [&](int zlo, int zhi) {
         std::vector<Item> out;
         auto xr = runs(c->h_sb[0], 0, g.nx, 32 * XV);
@@ -440,7 +444,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     };
     for (;;) {
         const size_t nall = make_items(0, g.nz).size();
-        if ((long long)nall * 2 < 3LL * nsm && (ymax > 16 || zmax > 16)) {
+        if ((long long)nall * 2 < 3LL * nsm * imul && (ymax > 16 || zmax > 16)) {
             if (ymax > 16) ymax = 16;
             else zmax /= 2;
             continue;

@@ -30,6 +30,7 @@ for P in PS:
                 ts.append(g.stats())
         med = {k: float(np.median([t[k] for t in ts])) for k in ("ms_prep", "ms_pass1", "ms_combine", "ms_pass2", "ms_total")}
         med["items"], med["items2"] = ts[-1]["items"], ts[-1]["items2"]
+        med["fast_items"] = ts[-1]["fast_items"]
         per.append(med)
         g.close()
     worst = max(x["ms_total"] for x in per)
