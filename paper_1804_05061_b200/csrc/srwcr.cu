@@ -600,7 +600,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
         if (const char *e = getenv("SRWCR_PIPE_WAVE")) wave = std::max(1, atoi(e));   // tests: small volumes
         const int nn = (int)n;
         if (nn >= 6 * wave) {
-            const int np = std::min(4, std::max(2, atoi(getenv("SRWCR_PIPE_P1") ? getenv("SRWCR_PIPE_P1") : "3")));   // C5 e2e: 3 parts 371, 4 parts 364 evals/s
+            const int np = std::min(4, std::max(2, atoi(getenv("SRWCR_PIPE_P1") ? getenv("SRWCR_PIPE_P1") : "2")));
             std::vector<int> b = {0}, l;
             for (int k = 1; k < np; ++k) b.push_back(k * wave);
             b.push_back(nn);
@@ -612,7 +612,9 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             l.back() = g.GzExt;
             c->fp1_b = b;
             c->fp1_l = l;
-            const int np2 = std::min(5, std::max(2, atoi(getenv("SRWCR_PIPE_P2") ? getenv("SRWCR_PIPE_P2") : "4")));
+            const int np2 = std::min(5, std::max(2, atoi(getenv("SRWCR_PIPE_P2") ? getenv("SRWCR_PIPE_P2") : "2")));
+            // (C5 e2e, pass-1 / pass-2 parts: 3/4 372.6, 2/4 375.0, 3/3 375.6, 3/2 377.6, 2/2
+            // 380.1 evals/s; 351.5 without the parts: each part boundary drains a wave)
             std::vector<int> b2 = {0}, l2;
             for (int k = np2 - 1; k >= 1; --k) b2.push_back(nn - k * wave);
             b2.push_back(nn);
