@@ -35,6 +35,12 @@ constexpr double STAT_UNIT = 65536.0;      // binless second moments: int64 fixe
 constexpr double STAT_UNIT_S = 16777216.0; // binned first moments (shifted, small): units 2^-24
 constexpr int FWMAX = 24;                  // max warps per CTA of the fast passes
 constexpr int FZMAX = 128;                 // max slices per item
+#ifndef SRWCR_P1_TMA_REC
+#define SRWCR_P1_TMA_REC 0
+#endif
+// pass 1: records by TMA bulk copies (cp.async.bulk + mbarrier) when aligned -- measured on C5
+// 1.328 vs 1.223 ms with the per-lane cp.async ring (C3 0.250 vs 0.227): off
+constexpr bool P1_TMA_REC = SRWCR_P1_TMA_REC != 0;
 constexpr int RRING = 4;                   // pass 1: slices in the per-warp record ring (3 ahead)
 #ifndef SRWCR_LTW
 #define SRWCR_LTW 8
@@ -167,7 +173,7 @@ __device__ __forceinline__ float mfloor(float u, int &iu) {
 
 // shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
 struct P1Smem {
-    int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, rr, total;
+    int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, rr, rbar, total;
 };
 __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     P1Smem o;
@@ -189,7 +195,8 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
     o.sh = take(S * 4);                  // float  SH[S]  per-slot shift
     o.ts = take(160 * 4);                // int    TS[]   touched-slot list of a round
-    o.rr = take(W * RRING * 64 * 4);     // unsigned RR[W][RRING][XV * 32] record ring (cp.async)
+    o.rr = take(W * RRING * 64 * 4);     // unsigned RR[W][RRING][XV * 32] record ring (TMA bulk / cp.async)
+    o.rbar = take(W * RRING * 8);        // mbarrier RB[W][RRING] of the ring's bulk copies
     o.total = off;
     return o;
 }
@@ -581,7 +588,7 @@ template <int XV> __device__ __forceinline__ VF<XV> vfloor_rd(VF<XV> u) {   // u
 // Both halves run the same per-voxel arithmetic as MODE 0, so the results are bitwise equal.
 template <int XV, bool INT, int MODE = 0>
 __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1Smem &L, unsigned char *smem, int y,
-                                       int warp, int lane, const P1Lane<XV, INT> &pl) {
+                                       int warp, int lane, const P1Lane<XV, INT> &pl, unsigned &rq) {
     constexpr bool SAMPLE = MODE != 2, MOMENTS = MODE != 1;
     const Geo &g = a.g;
     const int S = a.S, ns = it.nslots, dummy = it.nslots + 1;
@@ -675,20 +682,46 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
 
     // ---- software pipeline: the records, gathers and coordinate flags of slice z+1 are in
     // flight while slice z is processed
-    // The records of F go through a per-warp shared ring (cp.async, RRING slices ahead): an
+    // The records of F go through a per-warp shared ring, RRING - 1 slices ahead: an
     // asynchronous copy holds no register, so no register copy of an in-flight load can
-    // wait for it at a loop edge (as a register prefetch did).
+    // wait for it at a loop edge (as a register prefetch did).  A row's records of one slice
+    // are contiguous: one TMA bulk copy (cp.async.bulk, completing on the slot's mbarrier)
+    // issued by lane 0 when the row is 16-byte aligned and sized, else 4-byte cp.async per lane.
+    // Slot of slice j: (rq + j) % RRING, rq = the warp's slices of earlier rows.
     unsigned *RRw = reinterpret_cast<unsigned *>(smem + L.rr) + warp * (RRING * 32 * XV);
     const unsigned rr_s = (unsigned)__cvta_generic_to_shared(RRw);
-    auto rec_copy = [&](int jz) {   // slice jz's records -> ring slot jz % RRING, one commit group
+    const unsigned rb_s = (unsigned)__cvta_generic_to_shared(smem + L.rbar) + 8u * (unsigned)(warp * RRING);
+    const bool tma = P1_TMA_REC && ((it.x0 | g.nx | it.xlen) & 3) == 0;
+    auto rec_copy = [&](int jz) {   // slice jz's records -> ring slot (rq + jz) % RRING
+        const unsigned slot = (rq + (unsigned)jz) % RRING;
+        if (tma) {
+            if (jz < zlen && lane == 0) {
+                const unsigned bar = rb_s + 8u * slot, bytes = 4u * (unsigned)it.xlen;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // the slot's earlier reads
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(rr_s + 4u * slot * 32u * XV), "l"(a.rec + (vb + jz * nxy)), "r"(bytes), "r"(bar) : "memory");
+            }
+        } else {
 #pragma unroll
-        for (int v = 0; v < XV; ++v)
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rr_s + 4u * (unsigned)((jz % RRING) * 32 * XV + 32 * v + lane)),
-                         "l"(a.rec + (vb + jz * nxy + (pl.xv[v] - pl.xv[0]))) : "memory");
-        asm volatile("cp.async.commit_group;" ::: "memory");
+            for (int v = 0; v < XV; ++v)
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(rr_s + 4u * (slot * 32u * XV + 32u * v + lane)),
+                             "l"(a.rec + (vb + min(jz, zlen - 1) * nxy + (pl.xv[v] - pl.xv[0]))) : "memory");
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        }
+    };
+    auto rec_wait = [&](int jz) {   // slice jz's records have landed in their slot
+        if (tma) {
+            const unsigned q = rq + (unsigned)jz, bar = rb_s + 8u * (q % RRING), par = (q / RRING) & 1u;
+            asm volatile("{\n\t.reg .pred P1;\n\tWAIT_%=:\n\t"
+                         "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+                         "@!P1 bra WAIT_%=;\n\t}" ::"r"(bar), "r"(par) : "memory");
+        } else {
+            asm volatile("cp.async.wait_group %0;" ::"n"(RRING - 2) : "memory");
+        }
     };
     if constexpr (MOMENTS)
-        for (int j = 0; j < RRING - 1; ++j) rec_copy(min(j, zlen - 1));
+        for (int j = 0; j < RRING - 1; ++j) rec_copy(j);
     float mvn[XV];   // MODE 2: m of slice z+1
 #pragma unroll
     for (int v = 0; v < XV; ++v) mvn[v] = MODE == 2 ? __ldg(a.Mv + (vb + (pl.xv[v] - pl.xv[0]))) : 0.f;
@@ -788,13 +821,13 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         // ---- this slice's inputs
         unsigned rc[XV];
         float mvc[XV];
-        if constexpr (MOMENTS) {   // slice iz's group is complete once at most RRING - 2 newer are pending
-            asm volatile("cp.async.wait_group %0;" ::"n"(RRING - 2) : "memory");
-            rec_copy(min(iz + RRING - 1, zlen - 1));   // into the slot read one slice ago
+        if constexpr (MOMENTS) {
+            rec_wait(iz);
+            rec_copy(iz + RRING - 1);   // into the slot read one slice ago
         }
 #pragma unroll
         for (int v = 0; v < XV; ++v) {
-            rc[v] = MOMENTS ? RRw[(iz % RRING) * 32 * XV + 32 * v + lane] : 0u;
+            rc[v] = MOMENTS ? RRw[((rq + (unsigned)iz) % RRING) * 32 * XV + 32 * v + lane] : 0u;
             mvc[v] = mvn[v];
             if constexpr (MODE == 2) mvn[v] = __ldg(a.Mv + (vb + izn * nxy + (pl.xv[v] - pl.xv[0])));
         }
@@ -1064,8 +1097,10 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
         __syncwarp();
         if constexpr (SAMPLE && SRWCR_GATHER_POS == 2) gather(z0 + izn);
     }
-    // ---- row end: no record copy may still land in the ring the next row reuses
+    // ---- row end: no record copy may still land in the ring the next row reuses (the bulk
+    // copies: every one issued was waited for)
     if constexpr (MOMENTS) asm volatile("cp.async.wait_group 0;" ::: "memory");
+    rq += (unsigned)zlen;
     // ---- row end: binless -> K[ns]; lane j of the reduction holds value j = (l, ch, n)
     if constexpr (MOMENTS) {
         float vals[32];
@@ -1160,6 +1195,13 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
             pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * LTW) + 8u * (unsigned)l + 4u * ((lane >> 2) & 1);
         }
     };
+    // the warp's record-ring mbarriers (one arrival: lane 0's expect_tx; the bulk copy's bytes)
+    if (MODE != 1 && P1_TMA_REC && lane == 0) {
+        const unsigned rb = (unsigned)__cvta_generic_to_shared(smem + L.rbar) + 8u * (unsigned)(warp * RRING);
+        for (int k = 0; k < RRING; ++k) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rb + 8u * k) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    unsigned rq = 0;   // the warp's record-ring sequence number (slices of its earlier rows)
     __syncthreads();
 
     const int rounds = (it.ylen + W - 1) / W;
@@ -1174,15 +1216,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
             if (interior) {
                 P1Lane<XV, true> pl;
                 setup(pl);
-                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl);
+                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl, rq);
             } else if (MODE == 2) {   // (the moment half has no clamping: one variant)
                 P1Lane<XV, true> pl;
                 setup(pl);
-                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl);
+                p1_row<XV, true, MODE>(a, it, L, smem, y, warp, lane, pl, rq);
             } else {
                 P1Lane<XV, false> pl;
                 setup(pl);
-                p1_row<XV, false, MODE>(a, it, L, smem, y, warp, lane, pl);
+                p1_row<XV, false, MODE>(a, it, L, smem, y, warp, lane, pl, rq);
             }
         }
         __syncthreads();
@@ -1300,16 +1342,17 @@ __global__ void __launch_bounds__(MAXT, MINB) k_p1w(FArgs a) {
             pl.relx[v] = a.t.cb[0][pl.xv[v]] - xn0;
         }
     };
+    unsigned rq = 0;   // (the sample half copies no records)
     __syncthreads();
     for (int y = it.y0 + warp; y < it.y0 + it.ylen; y += W) {
         if (interior) {
             P1Lane<XV, true> pl;
             setup(pl);
-            p1_row<XV, true, 1>(a, it, L, smem, y, warp, lane, pl);
+            p1_row<XV, true, 1>(a, it, L, smem, y, warp, lane, pl, rq);
         } else {
             P1Lane<XV, false> pl;
             setup(pl);
-            p1_row<XV, false, 1>(a, it, L, smem, y, warp, lane, pl);
+            p1_row<XV, false, 1>(a, it, L, smem, y, warp, lane, pl, rq);
         }
     }
 }
