@@ -323,11 +323,17 @@ def test_pipelined_host_evaluation_bitwise(phi, monkeypatch):
     g, pb, Fn, Mn, params = _case("C5", 1, phi)
     st = g.stats()
     assert st["fast_path"] == 1
-    D1, g1 = g.eval(params)                      # host buffers: pipelined
+    D1, g1 = g.eval(params)                      # pageable host buffers: pipelined
     pt = torch.from_numpy(params).cuda()
     gt = torch.empty_like(pt)
     D2, _ = g.eval(pt, grad=gt)                  # device buffers: one launch per kernel (graph)
     D3, g3 = g.eval(params)
+    hp = torch.from_numpy(params.copy()).pin_memory()
+    hg = torch.empty_like(hp).pin_memory()
+    D4, _ = g.eval(hp, grad=hg)                  # pinned host buffers: the pipelined parts as a graph
+    g4 = hg.numpy().copy()
+    D5, _ = g.eval(hp, grad=hg)                  # replayed
     g.close()
-    assert D1 == D2 == D3
+    assert D1 == D2 == D3 == D4 == D5
     assert np.array_equal(g1, gt.cpu().numpy()) and np.array_equal(g1, g3)
+    assert np.array_equal(g1, g4) and np.array_equal(g1, hg.numpy())
