@@ -615,12 +615,14 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             l.back() = g.GzExt;
             c->fp1_b = b;
             c->fp1_l = l;
-            const int np2 = std::min(5, std::max(2, atoi(getenv("SRWCR_PIPE_P2") ? getenv("SRWCR_PIPE_P2") : "2")));
+            const int np2 = std::min(5, std::max(2, atoi(getenv("SRWCR_PIPE_P2") ? getenv("SRWCR_PIPE_P2") : "3")));
             // (C5 e2e, pass-1 / pass-2 parts: 3/4 372.6, 2/4 375.0, 3/3 375.6, 3/2 377.6, 2/2
-            // 380.1 evals/s; 351.5 without the parts: each part boundary drains a wave)
+            // 380.1 evals/s; 351.5 without the parts: each part boundary drains a wave; with 2
+            // pass-1 parts, pass-2 parts / first boundary in waves from the end: 2/1 378.9,
+            // 2/2 381.6, 3/2 383.9, 3/3 381.3)
             // the first pass-2 boundary sits k2 waves before the end (its final layers go back while
             // the last k2 waves run), later ones one wave apart
-            const int k2 = std::max(np2 - 1, atoi(getenv("SRWCR_PIPE_P2K") ? getenv("SRWCR_PIPE_P2K") : "1"));
+            const int k2 = std::max(np2 - 1, atoi(getenv("SRWCR_PIPE_P2K") ? getenv("SRWCR_PIPE_P2K") : "2"));
             std::vector<int> b2 = {0, nn - k2 * wave}, l2;
             for (int k = np2 - 2; k >= 1; --k) b2.push_back(nn - k * wave);
             b2.push_back(nn);
