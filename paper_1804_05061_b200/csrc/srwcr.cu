@@ -643,7 +643,9 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     if (const char *e = getenv("SRWCR_SPLIT")) c->fsplit = atoi(e) != 0;
     if (const char *e = getenv("SRWCR_P1W_MINB")) c->fMinbW = atoi(e) == 2 ? 2 : 3;
     if (const char *e = getenv("SRWCR_P1W_W")) c->fWw = std::min(16, std::max(1, atoi(e)));
-    CK(cudaMalloc(&c->fMv, sizeof(float) * slab));   // (also when fused: SRWCR_SPLIT is re-read per launch)
+    // the split variant's m array (4 B/voxel) only when SRWCR_SPLIT is set at create (then it
+    // is re-read per launch: the fused-vs-split test toggles it on one context)
+    if (c->fsplit || getenv("SRWCR_SPLIT")) CK(cudaMalloc(&c->fMv, sizeof(float) * slab));
     CK(cudaMalloc(&c->fphi4, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
     CK(cudaMemset(c->fphi4, 0, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
     c->fsmemw = p1w_smem(c->fWw).total;
@@ -724,6 +726,7 @@ static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bo
     const int n = cnt >= 0 ? cnt : c->nfitems - i0;
     bool split = c->fsplit;
     if (const char *e = getenv("SRWCR_SPLIT")) split = atoi(e) != 0;   // experiments / the fused-vs-split test
+    split = split && c->fMv != nullptr;
     if (n > 0 && split) {
         // sample half, then the moment half (same items)
         FArgs aw = a;

@@ -167,7 +167,8 @@ def test_split_pass1_bitwise_equals_fused(name, monkeypatch):
     """Pass 1 split into its sample half (k_p1w: FFD, gathers, trilinear, exact flags -> MG
     and m) and its moment half (k_p1f MODE 2: m -> line tables) runs the same per-voxel
     arithmetic as the fused kernel: bitwise-equal statistics, D and gradient (one context;
-    SRWCR_SPLIT is read at each launch)."""
+    SRWCR_SPLIT, set at create to allocate the split's m array, is re-read at each launch)."""
+    monkeypatch.setenv("SRWCR_SPLIT", "0")
     g, pb, Fn, Mn, params = _case(name, 1, "small")
     res = []
     for split in ("0", "1", "0"):
