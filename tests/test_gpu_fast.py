@@ -338,3 +338,21 @@ def test_pipelined_host_evaluation_bitwise(phi, monkeypatch):
     assert D1 == D2 == D3 == D4 == D5
     assert np.array_equal(g1, gt.cpu().numpy()) and np.array_equal(g1, g3)
     assert np.array_equal(g1, g4) and np.array_equal(g1, hg.numpy())
+
+
+def test_value_only_evaluation():
+    """srwcr_eval with grad = NULL (the L-BFGS line-search trials) runs pass 1 and the combine
+    only: the same D, bitwise, as the value + gradient evaluation, on host and device buffers
+    (pipelined and graph paths)."""
+    torch = pytest.importorskip("torch")
+    g, pb, Fn, Mn, params = _case("C5", 1, "small")
+    D1, grad = g.eval(params)
+    D2, none = g.eval(params, want_grad=False)
+    pt = torch.from_numpy(params).cuda()
+    D3, _ = g.eval(pt, want_grad=False)
+    gt = torch.empty_like(pt)
+    D4, _ = g.eval(pt, grad=gt)
+    g.close()
+    assert none is None
+    assert D1 == D2 == D3 == D4
+    assert np.array_equal(grad, gt.cpu().numpy())
