@@ -156,10 +156,12 @@ def test_fast_path_nccl_single_rank_graph():
     D2, _ = g2.eval(pt, grad=gt2)      # captured
     g2c = gt2.clone()
     D3, _ = g2.eval(pt, grad=gt2)      # replayed
+    D4, g4 = g2.eval(params)           # host buffers with a communicator (not pipelined, not a graph)
     g1.close()
     g2.close()
     assert D3 == D2 and torch.equal(g2c, gt2)
     assert D2 == D1 and torch.equal(gt2, gt1)
+    assert D4 == D1 and np.array_equal(g4, gt1.cpu().numpy())
 
 
 @pytest.mark.parametrize("name", ["C3", "C5"])
