@@ -158,6 +158,7 @@ struct srwcr_ctx {
     std::vector<int> fp1_b, fp1_l, fp2_b, fp2_l;
     float4 *fphi4 = nullptr;                // fp32 phi, one float4 (x, y, z, 0) per node
     std::vector<NBox> h_nboxes;             // whole-volume boxes of the deterministic static counts
+    int fzmax = FZMAX;                      // the fast items' longest z-range (sizes the per-slice tables)
     cudaTextureObject_t ftexM = 0;
     int fWw = 8, fMinbW = 3;
     size_t fsmemw = 0;
@@ -421,6 +422,10 @@ static srwcr_status run_combine(srwcr_ctx *c) {
 // Items, static fixed-image records and per-line touched-slot lists of srwcr_fast.cuh.
 // Eligible: 3-D, orientation 0, coarse spatial lattice (no multi-cell items), every
 // x-chunk reading at most 32 control x-nodes.  SRWCR_NOFAST=1 keeps the round-1 passes.
+// pass 1 keeps its per-slice tables at FZMAX (its row-offset stride is a compile-time
+// constant: a runtime stride cost ~1 %); pass 2 sizes them by the items' z-range (room for its
+// row-buffer copies)
+static inline int P1ZM(int) { return FZMAX; }
 static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     const Geo &g = c->g;
     if (getenv("SRWCR_NOFAST")) return SRWCR_OK;
@@ -457,9 +462,11 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     std::vector<Item> its = make_items((int)c->z0, (int)c->z1);
     if (its.empty()) return SRWCR_OK;
     for (const Item &it : make_items(0, g.nz)) c->h_nboxes.push_back(NBox{it.x0, it.xlen, it.y0, it.ylen, it.z0, it.zlen});
+    int zm = 1;
     for (const Item &it : its) {
         const int nxn = c->h_cb[0][it.x0 + it.xlen - 1] + 4 - c->h_cb[0][it.x0];
         if (nxn > 32 || it.zlen > FZMAX) return SRWCR_OK;   // not eligible: round-1 passes
+        zm = std::max(zm, it.zlen);
     }
     if (P1_TEX) {   // the layered copy of M (2-D layered limits: 32768 x 32768 x 2048)
         if (g.nx > 32768 || g.ny > 32768 || g.nz > 2048) return SRWCR_OK;
@@ -538,10 +545,10 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->dev);
     int W = 0;
     for (int Wc : {16, 12, 8, 4})
-        if (!W && p1_smem(Wc, S).total <= maxsm) W = Wc;
+        if (!W && p1_smem(Wc, S, P1ZM(zm)).total <= maxsm) W = Wc;
     if (const char *e = getenv("SRWCR_FW")) {   // experiments: up to 24 warps (XV 1: <= 85 registers)
         const int w = std::max(1, atoi(e));
-        if (w <= 16 || (XV == 1 && w <= 24 && p1_smem(w, S).total <= maxsm)) W = w;
+        if (w <= 16 || (XV == 1 && w <= 24 && p1_smem(w, S, P1ZM(zm)).total <= maxsm)) W = w;
     }
     if (W == 0) return SRWCR_OK;
     // device copies
@@ -592,7 +599,8 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     c->fW = W;
     c->fS = S;
     c->nfitems = (int)n;
-    c->fsmem1 = p1_smem(W, S).total;
+    c->fsmem1 = p1_smem(W, S, P1ZM(zm)).total;
+    c->fzmax = zm;
     c->h_fitems = fi;
     // pipelined host-buffer evaluation (one rank): pass 1 in parts of one wave, one wave, the
     // rest (the first params upload part is as small as one wave's layers); pass 2 as all but
@@ -648,7 +656,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     if (c->fsplit || getenv("SRWCR_SPLIT")) CK(cudaMalloc(&c->fMv, sizeof(float) * slab));
     CK(cudaMalloc(&c->fphi4, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
     CK(cudaMemset(c->fphi4, 0, sizeof(float4) * (size_t)g.Gx * g.Gy * g.Gz));
-    c->fsmemw = p1w_smem(c->fWw).total;
+    c->fsmemw = p1w_smem(c->fWw, zm).total;
     // pass 2: node window and warps per CTA
     int npmax = 0;
     for (const FItem &f : fi) {
@@ -659,12 +667,12 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     }
     int W2 = 0;
     for (int Wc : {16, 12, 8, 4})
-        if (!W2 && p2_smem(Wc, S, npmax).total <= maxsm) W2 = Wc;
+        if (!W2 && p2_smem(Wc, S, npmax, zm).total <= maxsm) W2 = Wc;
     if (const char *e = getenv("SRWCR_FW2")) W2 = std::min(W2, std::max(1, atoi(e)));
     if (W2 == 0) return SRWCR_OK;
     c->fW2 = W2;
     c->fnpmax = npmax;
-    c->fsmem2 = p2_smem(W2, S, npmax).total;
+    c->fsmem2 = p2_smem(W2, S, npmax, zm).total;
     c->fdxz = (float)((std::ceil(c->delta[0]) + 1.0) * (std::ceil(c->delta[2]) + 1.0));
     CK(cudaMalloc(&c->gradi, sizeof(unsigned long long) * c->nparams));
     CK(cudaMemset(c->gradi, 0, sizeof(unsigned long long) * c->nparams));
@@ -713,7 +721,7 @@ static FArgs fast_args(srwcr_ctx *c) {
     a.MG = c->MG; a.Mv = c->fMv; a.mgz0 = (int)c->z0;
     a.texM = (unsigned long long)c->ftexM;
     a.S = c->fS; a.W = c->fW; a.i0 = 0;
-    a.L1 = p1_smem(c->fW, c->fS);
+    a.L1 = p1_smem(c->fW, c->fS, P1ZM(c->fzmax));
     a.ablate = 0;
     if (const char *e = getenv("SRWCR_ABLATE")) a.ablate = atoi(e);
     return a;
@@ -731,7 +739,7 @@ static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bo
         // sample half, then the moment half (same items)
         FArgs aw = a;
         aw.W = c->fWw;
-        aw.L1 = p1w_smem(c->fWw);
+        aw.L1 = p1w_smem(c->fWw, c->fzmax);
         const int Tw = 32 * c->fWw, T = 32 * c->fW;
         const size_t smw = c->fsmemw;
         if (c->fXV == 2) {
@@ -796,7 +804,7 @@ static F2Args fast_pass2_args(srwcr_ctx *c) {
     A.xlist = c->xlist; A.xcount = c->xcount; A.xcap = c->xcap;
     A.npmax = c->fnpmax;
     A.f.W = c->fW2;
-    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax);
+    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax, c->fzmax);
     return A;
 }
 static srwcr_status launch_fast_p2f(srwcr_ctx *c, const F2Args &A0, int i0, int n) {
@@ -827,7 +835,7 @@ static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad, bool reduce_in
     A.xlist = c->xlist; A.xcount = c->xcount; A.xcap = c->xcap;
     A.npmax = c->fnpmax;
     A.f.W = c->fW2;
-    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax);
+    A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax, c->fzmax);
     CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
     const int n = c->nfitems, T = 32 * c->fW2;
     if (c->fXV == 2) {

@@ -56,6 +56,11 @@ constexpr int LTW = SRWCR_LTW;
 // 1.222 -> 1.166 ms (copies by octet parity instead: 1.167)
 constexpr int LTC = SRWCR_LTC;
 constexpr int LTSW = LTW * LTC;            // words per slot
+#ifndef SRWCR_RBC
+#define SRWCR_RBC 2
+#endif
+// pass 2: copies of the retire row buffer (lanes 0-15 / 16-31), summed when it is read out
+constexpr int RBC = SRWCR_RBC;
 
 struct FItem {
     int x0, xlen, y0, ylen, z0, zlen;
@@ -183,9 +188,12 @@ __device__ __forceinline__ float mfloor(float u, int &iu) {
 // shared-memory layout of k_p1f (bytes); the host sizes the launch with the same function
 struct P1Smem {
     int lt, k, ct, pl, lm, lo, wx, wxr, wcx, wy, rm, zs, zc, zb, sh, ts, rr, rbar, total;
+    int lostride;                        // LO entries per warp: the items' longest z-range + 1
 };
-__host__ __device__ inline P1Smem p1_smem(int W, int S) {
+// ZM: the longest z-range of the items (<= FZMAX): sizes the per-slice tables
+__host__ __device__ inline P1Smem p1_smem(int W, int S, int ZM = FZMAX) {
     P1Smem o;
+    o.lostride = ZM + 1;
     int off = 0;
     auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
     o.lt = take(W * S * LTSW * 4);        // int   LT[W][S][LTW][LTC]
@@ -193,15 +201,15 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S) {
     o.ct = take(S * 128 * 4);            // float CT[S][4 m][8 e][4 n]
     o.pl = take(W * 32 * 16);            // float4 PL[W][32]   layer node buffer
     o.lm = take(W * 4 * 4 * 4);          // float LM[W][4 layers][4]
-    o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]  the row's line-list offsets
+    o.lo = take(W * (ZM + 1) * 4);       // unsigned LO[W][ZM + 1]  the row's line-list offsets
     o.wx = take(64 * 16);                // float4 WX[XV * 32]  the lane voxels' spatial x weights (0: padding)
     o.wxr = take(64 * 16);               // float4 WXR[XV * 32] the same, rotated: component k = tap (k + lane) & 3
     o.wcx = take(64 * 16);               // float4 WCX[XV * 32] the lane voxels' control x weights
     o.wy = take(W * 16);                 // float4 WY[W]
     o.rm = take(W * 16);                 // uint4 RM[W]
-    o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
-    o.zc = take(FZMAX * 16);             // float4 ZC[z]  control z weights
-    o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
+    o.zs = take(ZM * 16);                // float4 ZS[z]  spatial z weights
+    o.zc = take(ZM * 16);                // float4 ZC[z]  control z weights
+    o.zb = take(ZM * 4);                 // int    ZB[z]  control z base
     o.sh = take(S * 4);                  // float  SH[S]  per-slot shift
     o.ts = take(160 * 4);                // int    TS[]   touched-slot list of a round
     o.rr = take(W * RRING * 64 * 4);     // unsigned RR[W][RRING][XV * 32] record ring (TMA bulk / cp.async)
@@ -605,7 +613,7 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     float *Kw = reinterpret_cast<float *>(smem + L.k) + warp * S * 32;
     float4 *PLw = reinterpret_cast<float4 *>(smem + L.pl) + warp * 32;
     float *LMw = reinterpret_cast<float *>(smem + L.lm) + warp * 16;
-    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);
+    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);   // (pass 1: L.lostride == FZMAX + 1)
     const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
     const float4 *ZC = reinterpret_cast<const float4 *>(smem + L.zc);
     const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
@@ -1320,15 +1328,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
 // The sample half of a split pass 1 (MODE 1): same items, rows dealt to the warps with no
 // CTA barrier in the loop and only the FFD / z-weight shared state, so the kernel runs at
 // MINB CTAs per SM (more resident warps to cover the gathers' latency than the fused pass).
-__host__ __device__ inline P1Smem p1w_smem(int W) {
+__host__ __device__ inline P1Smem p1w_smem(int W, int ZM = FZMAX) {
     P1Smem o{};
+    o.lostride = ZM + 1;
     int off = 0;
     auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
     o.pl = take(W * 32 * 16);
     o.lm = take(W * 4 * 4 * 4);
     o.wcx = take(64 * 16);
-    o.zc = take(FZMAX * 16);
-    o.zb = take(FZMAX * 4);
+    o.zc = take(ZM * 16);
+    o.zb = take(ZM * 4);
     o.total = off;
     return o;
 }
@@ -1394,22 +1403,24 @@ namespace srwcr {
 // combine's bound), flushed once per item into the int64 global gradient: deterministic.
 struct P2Smem {
     int gam, ab, gy, gz, rb, nph, npl, lo, zc, zb, zs, cx, ws, cr, total;
+    int lostride;
 };
-__host__ __device__ inline P2Smem p2_smem(int W, int S, int npn) {
+__host__ __device__ inline P2Smem p2_smem(int W, int S, int npn, int ZM = FZMAX) {
     P2Smem o;
+    o.lostride = ZM + 1;
     int off = 0;
     auto take = [&](int bytes) { const int r = off; off += (bytes + 15) & ~15; return r; };
     o.gam = take(S * 2 * 64 * 4);        // float  GAM[S][2][64]    gamma of the item's regions, bins a0, a0+1
     o.ab = take(2 * 64 * 4);             // float  AB[2][64]        alpha, beta of the item's regions
     o.gy = take(W * S * 8 * 16);         // float4 GY[W][S][2][4 l] (over n), y-contracted per row
     o.gz = take(W * 2 * S * 2 * 16);     // float4 GZ[W][2][S][2]   (over l), z-contracted per line (2 buffers)
-    o.rb = take(W * 3 * 32 * 4);         // int    RB[W][3][32]     x-contraction of a retiring layer
+    o.rb = take(W * 3 * 32 * RBC * 4);   // int    RB[W][3][32][RBC] x-contraction of a retiring layer
     o.nph = take(npn * 4);               // int    NPH[npn], NPL[npn] node window (hi, lo)
     o.npl = take(npn * 4);
-    o.lo = take(W * (FZMAX + 1) * 4);    // unsigned LO[W][FZMAX + 1]
-    o.zc = take(FZMAX * 16);             // float4 ZC[z]  control z weights
-    o.zb = take(FZMAX * 4);              // int    ZB[z]  control z base
-    o.zs = take(FZMAX * 16);             // float4 ZS[z]  spatial z weights
+    o.lo = take(W * (ZM + 1) * 4);       // unsigned LO[W][ZM + 1]
+    o.zc = take(ZM * 16);                // float4 ZC[z]  control z weights
+    o.zb = take(ZM * 4);                 // int    ZB[z]  control z base
+    o.zs = take(ZM * 16);                // float4 ZS[z]  spatial z weights
     o.cx = take(32 * 4);                 // int    CX[32] adds per x-node of a retire (magic offsets)
     o.ws = take(64 * 16);                // float4 WS[XV * 32] the lane voxels' spatial x weights (0: padding)
     o.cr = take(64 * 16);                // float4 CR[XV * 32] rotated control x weights: component k = tap (k + lane) & 3
@@ -1447,10 +1458,11 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
     const float *AB = reinterpret_cast<const float *>(smem + L.ab);
     float4 *GYw = reinterpret_cast<float4 *>(smem + L.gy) + warp * S * 8;
     float4 *GZw = reinterpret_cast<float4 *>(smem + L.gz) + warp * 2 * S * 2;
-    int *RBw = reinterpret_cast<int *>(smem + L.rb) + warp * 96;
+    int *RBw = reinterpret_cast<int *>(smem + L.rb) + warp * 96 * RBC;
+    const int rbc = RBC == 2 ? (lane >> 4) & 1 : 0;   // this lane's copy of the row buffer
     int *NPH = reinterpret_cast<int *>(smem + L.nph);
     int *NPL = reinterpret_cast<int *>(smem + L.npl);
-    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);
+    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * L.lostride;
     const float4 *ZC = reinterpret_cast<const float4 *>(smem + L.zc);
     const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
     const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
@@ -1522,17 +1534,24 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
                 const int nd = pl.relx[v] + ((k + q4) & 3);
                 const float w = f4(crv[v], k);
                 FCHECK(nd >= 0 && nd < 32);
-                red_shared(RBw + nd, __float_as_int(fmaf(w, R0, MAGIC)));
-                red_shared(RBw + 32 + nd, __float_as_int(fmaf(w, R1, MAGIC)));
-                red_shared(RBw + 64 + nd, __float_as_int(fmaf(w, R2, MAGIC)));
+                red_shared(RBw + nd * RBC + rbc, __float_as_int(fmaf(w, R0, MAGIC)));
+                red_shared(RBw + (32 + nd) * RBC + rbc, __float_as_int(fmaf(w, R1, MAGIC)));
+                red_shared(RBw + (64 + nd) * RBC + rbc, __float_as_int(fmaf(w, R2, MAGIC)));
             }
         }
         __syncwarp();
         const int lz = gzr - zn0;
         for (int i = lane; i < 3 * nxn; i += 32) {
             const int c = i >= 2 * nxn ? 2 : (i >= nxn ? 1 : 0), j = i - c * nxn;
-            const int raw = RBw[c * 32 + j];
-            RBw[c * 32 + j] = 0;
+            int raw;
+            if constexpr (RBC == 2) {
+                const int2 r2 = reinterpret_cast<const int2 *>(RBw)[c * 32 + j];
+                reinterpret_cast<int2 *>(RBw)[c * 32 + j] = make_int2(0, 0);
+                raw = r2.x + r2.y;
+            } else {
+                raw = RBw[c * 32 + j];
+                RBw[c * 32 + j] = 0;
+            }
             const float rv = (float)(raw - CX[j] * MAGIC_I) * isc * gunit;
             if (rv != 0.f) {
                 FCHECK(lz >= 0 && (((lz * 3 + c) * nyn + (cby - yn0 + 3)) * nxn + j) < A2.npmax);
@@ -1726,7 +1745,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p2f(F2Args A2) {
         AB[i] = __ldg((ab ? A2.beta : A2.alpha) + reg);
     }
     for (int i = threadIdx.x; i < npn; i += blockDim.x) { NPH[i] = 0; NPL[i] = 0; }
-    for (int i = threadIdx.x; i < W * 96; i += blockDim.x) RB[i] = 0;
+    for (int i = threadIdx.x; i < W * 96 * RBC; i += blockDim.x) RB[i] = 0;
     for (int i = threadIdx.x; i < it.zlen; i += blockDim.x) {
         ZC[i] = a.t.cw[2][it.z0 + i];
         ZB[i] = a.t.cb[2][it.z0 + i];
