@@ -61,6 +61,10 @@ constexpr int LTSW = LTW * LTC;            // words per slot
 #endif
 // pass 2: copies of the retire row buffer (lanes 0-15 / 16-31), summed when it is read out
 constexpr int RBC = SRWCR_RBC;
+#ifndef SRWCR_P2_GZ_PLANAR
+#define SRWCR_P2_GZ_PLANAR 1
+#endif
+constexpr bool P2_GZ_PLANAR = SRWCR_P2_GZ_PLANAR != 0;
 
 struct FItem {
     int x0, xlen, y0, ylen, z0, zlen;
@@ -1458,6 +1462,9 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
     const float *AB = reinterpret_cast<const float *>(smem + L.ab);
     float4 *GYw = reinterpret_cast<float4 *>(smem + L.gy) + warp * S * 8;
     float4 *GZw = reinterpret_cast<float4 *>(smem + L.gz) + warp * 2 * S * 2;
+    // GZ entry of (slot, half b2): [b2][S] planes (P2_GZ_PLANAR: consecutive slots in
+    // consecutive 16-byte groups, fewer LDS.128 conflicts) or [S][2]
+    auto gzi = [S](int sl, int b2) { return P2_GZ_PLANAR ? b2 * S + sl : sl * 2 + b2; };
     int *RBw = reinterpret_cast<int *>(smem + L.rb) + warp * 96 * RBC;
     const int rbc = RBC == 2 ? (lane >> 4) & 1 : 0;   // this lane's copy of the row buffer
     int *NPH = reinterpret_cast<int *>(smem + L.nph);
@@ -1605,7 +1612,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             const int s = j < cnt ? (int)(ent & 0xFFu) : ns + 1;
             const float4 *gy = GYw + (s * 2 + b2) * 4;
             const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
-            GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
+            GZb[gzi(s, b2)] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
         }
         for (int p = 1; 16 * p < cnt; ++p) {
             const int j = 16 * p + (lane >> 1);
@@ -1615,14 +1622,14 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
                 const int s = (int)(ent & 0xFFu);
                 const float4 *gy = GYw + (s * 2 + b2) * 4;
                 const float4 q0 = gy[0], q1 = gy[1], q2 = gy[2], q3 = gy[3];
-                GZb[s * 2 + b2] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
+                GZb[gzi(s, b2)] = make_float4(dot4(wz, q0), dot4(wz, q1), dot4(wz, q2), dot4(wz, q3));
             }
         }
         float t = reinterpret_cast<const float *>(ZS + jz)[lane & 3] * abY;
         t += __shfl_xor_sync(FULL, t, 1);
         t += __shfl_xor_sync(FULL, t, 2);
         // (the 4 lanes of a group hold the same sum: all store it, no branch)
-        reinterpret_cast<float *>(GZb + ns * 2 + (lane >> 4))[(lane >> 2) & 3] = t;
+        reinterpret_cast<float *>(GZb + gzi(ns, lane >> 4))[(lane >> 2) & 3] = t;
     };
     gz_line(0, GZw);
     for (int iz = 0; iz < zlen; ++iz) {
@@ -1672,7 +1679,7 @@ __device__ __forceinline__ void p2_row(const F2Args &A2, const FItem &it, const 
             // g1' = 3.6 f + 0.1 below the fold, 3.7 - 3.6 f above; 0.1 at an integer m (c4)
             const float g1p = selp(integral, 0.1f, fm < 0.5f ? fmaf(3.6f, fm, 0.1f) : fmaf(-3.6f, fm, 3.7f));
             const float c2 = selp(integral, 2.0f * m, fmaf(2.0f, nf, 1.0f));
-            const float4 G0 = GZc[slot * 2], G1 = GZc[slot * 2 + 1], AY = GZc[ns * 2], BY = GZc[ns * 2 + 1];
+            const float4 G0 = GZc[gzi(slot, 0)], G1 = GZc[gzi(slot, 1)], AY = GZc[gzi(ns, 0)], BY = GZc[gzi(ns, 1)];
             const float4 wsv = WS[v * 32 + lane];
             const float w0 = wsv.x, w1 = wsv.y, w2 = wsv.z, w3 = wsv.w;
             const float At = fmaf(w3, AY.w, fmaf(w2, AY.z, fmaf(w1, AY.y, w0 * AY.x)));
