@@ -41,6 +41,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-slices", type=int, default=0, help="z-slices of the oracle sample (0 = auto)")
+    ap.add_argument("--grad-exchange", default="allreduce", choices=["allreduce", "halo"],
+                    help="N > 1: int64 all-reduce of the gradient (every rank gets it all) or the halo "
+                         "exchange (each rank gets its owned node layers; srwcr_options.grad_exchange)")
     ap.add_argument("--no-paper-workloads", action="store_true",
                     help="skip the context timings of the paper's Table VIII workloads")
     return ap.parse_args()
@@ -247,7 +250,8 @@ def main():
     Ft = torch.from_numpy(F).cuda()
     Mt = torch.from_numpy(M).cuda()
     g = S.Srwcr(Ft, Mt, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], device=local,
-                nranks=ws, rank=rank, nccl_id=nccl_id)
+                nranks=ws, rank=rank, nccl_id=nccl_id,
+                grad_exchange=1 if (ws > 1 and args.grad_exchange == "halo") else 0)
     del Ft, Mt
     params_np = synth.make_params(g.params_shape, args.phi, args.seed)
     params = torch.from_numpy(params_np).cuda()
@@ -373,7 +377,7 @@ def main():
             "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(args.config, cfg), "phi": args.phi, "seed": args.seed,
-                       "parallelism": f"z-slab x{ws}", "l2": "inputs 671 MB > 126 MB L2 (no flush needed)"
+                       "parallelism": f"z-slab x{ws}" + (f" ({args.grad_exchange} gradient exchange)" if ws > 1 else ""), "l2": "inputs 671 MB > 126 MB L2 (no flush needed)"
                        if args.config in ("C4", "C5") else "inputs may be L2-resident (no flush)"},
             "gvoxel_per_s": evals * nvox / 1e9,
             "pass_ms": {"prep": statistics.mean(pp), "pass1": t1, "combine": statistics.mean(cb), "pass2": t2},

@@ -79,10 +79,22 @@ typedef struct {
                                   grad) on one rank replays a CUDA graph of the
                                   evaluation captured on first use for that pointer pair
                                   (re-captured when a pointer changes); 0: ordinary launches */
+    int32_t grad_exchange;     /* z-slabs over NCCL (nccl_id set): 0 (default):
+                                  all-reduce of the int64 gradient, every rank gets the full
+                                  gradient; 1: halo exchange -- rank k sends its partial on the
+                                  node layers rank k+1 owns (ncclSend/Recv, 3 layers per
+                                  component when slabs follow control cells) and gets the
+                                  gradient on ITS OWNED layers only, zero elsewhere
+                                  (srwcr_grad_layers; the rank gradients sum / concatenate to
+                                  the full one, bitwise the all-reduce's on the owned layers):
+                                  for a caller-side optimizer sharded by layers.  3-D fast-path
+                                  configurations only (SRWCR_ENOTSUP otherwise), slabs at least
+                                  as thick as the 4 taps (SRWCR_EINVAL); srwcr_register
+                                  refuses it (its L-BFGS is replicated) */
 } srwcr_options;
 
 /* Fills *opt with defaults: orientation 0, inputs_normalized 0, device 0, nranks 1,
- * rank 0, nccl_id NULL, eps_mass 1e-12, eps_sigma 1e-6, moment_shift 1, use_graph 1. */
+ * rank 0, nccl_id NULL, eps_mass 1e-12, eps_sigma 1e-6, moment_shift 1, use_graph 1, grad_exchange 0. */
 srwcr_status srwcr_default_options(srwcr_options *opt);
 
 /* Create a context: copies F and M (host or device; the caller may free them on
@@ -111,7 +123,8 @@ srwcr_status srwcr_num_params(const srwcr_ctx *ctx, int64_t *n, int64_t grid_dim
  *   *value = D (Eq 9) on return (host pointer);
  *   grad   = dD/dPhi (host or device, fp64, same layout as params), or NULL for the
  *            value only.  With nranks > 1 every rank passes the same params and gets
- *            the same D and the full gradient.
+ *            the same D and the full gradient (grad_exchange = 1: the gradient on its
+ *            owned node layers, zero elsewhere).
  * Returns SRWCR_EDEGENERATE (value = 0, grad = 0) if no region is retained. */
 srwcr_status srwcr_eval(srwcr_ctx *ctx, const double *params, double *value, double *grad);
 
@@ -130,6 +143,24 @@ srwcr_status srwcr_eval_end(srwcr_ctx *ctx, double *value, double *grad);
 /* z-slab of rank `rank` out of `nranks` for a volume of nz slices: [*z0, *z1).
  * Host-only (no GPU needed).  Slabs split the slices as evenly as possible. */
 srwcr_status srwcr_plan_slab(int64_t nz, int32_t nranks, int32_t rank, int64_t *z0, int64_t *z1);
+
+/* Node-layer plan of the z-slab gradient (the halo exchange; Eq 17: voxel
+ * slice z feeds control layers cbz[z] .. cbz[z] + 3).  Host-only (no GPU needed).
+ *   nz, nranks, rank  as srwcr_plan_slab (nz >= nranks)
+ *   cbz[nz]           tap base of every slice on the control lattice, non-decreasing,
+ *                     in [0, gz) (srwcr_debug_dump SRWCR_DUMP_CTRL_TAPS, z part)
+ *   gz                control layers Gz
+ *   out[5]            t0, t1: layers [t0, t1) the rank's slab touches (its gradient
+ *                     partial is zero outside them); o0, o1: layers [o0, o1) the rank owns
+ *                     (o0 = t0, 0 for rank 0; o1 = t0 of rank + 1, gz for the last rank);
+ *                     r1: rank - 1's partial is non-zero on the owned layers [o0, r1)
+ *                     (r1 = o0 for rank 0).  The rank sends [o1, t1) to rank + 1.
+ * SRWCR_EINVAL on bad arguments or when some rank's touched layers reach past its upper
+ * neighbour's owned range (slabs thinner than the taps: use fewer ranks). */
+srwcr_status srwcr_plan_layers(int64_t nz, int32_t nranks, int32_t rank, const int32_t *cbz, int64_t gz,
+                               int64_t out[5]);
+/* srwcr_plan_layers of the context's own rank (3-D; SRWCR_ENOTSUP for 2-D or an invalid plan). */
+srwcr_status srwcr_grad_layers(const srwcr_ctx *ctx, int64_t out[5]);
 
 /* Bending energy C_p of the FFD (the constraint of Eq 1; Rueckert et
  * al. [26]; reading c19 of DESIGN.md):

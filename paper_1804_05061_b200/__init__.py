@@ -54,7 +54,7 @@ class _Options(ctypes.Structure):
                 ("inputs_normalized", ctypes.c_int32), ("device", ctypes.c_int32),
                 ("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
                 ("eps_mass", ctypes.c_double), ("eps_sigma", ctypes.c_double),
-                ("moment_shift", ctypes.c_int32), ("use_graph", ctypes.c_int32)]
+                ("moment_shift", ctypes.c_int32), ("use_graph", ctypes.c_int32), ("grad_exchange", ctypes.c_int32)]
 
 
 class _Stats(ctypes.Structure):
@@ -89,7 +89,8 @@ REGISTER_STATUS = {0: "converged", 1: "stable", 2: "max_iter", 3: "line_search_f
 _lib = None
 
 EXPORTS = ["srwcr_default_options", "srwcr_create", "srwcr_num_params", "srwcr_eval", "srwcr_eval_begin",
-           "srwcr_stats_buffer", "srwcr_eval_end", "srwcr_plan_slab", "srwcr_default_lbfgs_config",
+           "srwcr_stats_buffer", "srwcr_eval_end", "srwcr_plan_slab", "srwcr_plan_layers", "srwcr_grad_layers",
+           "srwcr_default_lbfgs_config",
            "srwcr_register", "srwcr_bending", "srwcr_field", "srwcr_resample", "srwcr_compose",
            "srwcr_downsample2", "srwcr_upsample2_field", "srwcr_debug_size", "srwcr_debug_dump", "srwcr_set_timing", "srwcr_get_stats",
            "srwcr_stream", "srwcr_last_error", "srwcr_destroy"]
@@ -112,6 +113,8 @@ def lib():
         L.srwcr_stats_buffer.argtypes = [vp, P(vp), P(ctypes.c_size_t)]
         L.srwcr_eval_end.argtypes = [vp, P(dbl), vp]
         L.srwcr_plan_slab.argtypes = [i64, i32, i32, P(i64), P(i64)]
+        L.srwcr_plan_layers.argtypes = [i64, i32, i32, P(i32), i64, P(i64)]
+        L.srwcr_grad_layers.argtypes = [vp, P(i64)]
         L.srwcr_debug_size.argtypes = [vp, i32, P(ctypes.c_size_t)]
         L.srwcr_debug_dump.argtypes = [vp, i32, vp, ctypes.c_size_t]
         L.srwcr_set_timing.argtypes = [vp, i32]
@@ -142,6 +145,21 @@ def plan_slab(nz: int, nranks: int, rank: int):
     if st != OK:
         raise SrwcrError(st, "plan_slab")
     return z0.value, z1.value
+
+
+def plan_layers(nz: int, nranks: int, rank: int, cbz, gz: int):
+    """Node-layer plan of `rank`'s gradient (host-only C function): (t0, t1, o0, o1, r1) --
+    touched layers [t0, t1), owned layers [o0, o1), rank - 1's partial on [o0, r1); the rank
+    sends [o1, t1) to rank + 1.  cbz: tap base of every slice (int32, length nz)."""
+    cb = np.ascontiguousarray(cbz, dtype=np.int32)
+    if cb.size != int(nz):
+        raise ValueError("cbz must have nz entries")
+    out = (ctypes.c_int64 * 5)()
+    st = lib().srwcr_plan_layers(int(nz), int(nranks), int(rank), cb.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)),
+                                 int(gz), out)
+    if st != OK:
+        raise SrwcrError(st, "plan_layers")
+    return tuple(out)
 
 
 def _ptr(a, n=None, what="array", out=False):
@@ -180,7 +198,7 @@ class Srwcr:
 
     def __init__(self, fixed, moving, spacing_mm, bins, spatial_bins, control_spacing_mm, *,
                  inputs_normalized=False, device=0, nranks=1, rank=0, nccl_id=None, eps_mass=1e-12,
-                 eps_sigma=1e-6, moment_shift=True, use_graph=True, orientation=0):
+                 eps_sigma=1e-6, moment_shift=True, use_graph=True, orientation=0, grad_exchange=0):
         L = lib()
         shape = tuple(int(s) for s in fixed.shape)
         if tuple(moving.shape) != shape or len(shape) != 3:
@@ -198,6 +216,7 @@ class Srwcr:
             opt.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p)
         opt.eps_mass, opt.eps_sigma = float(eps_mass), float(eps_sigma)
         opt.moment_shift, opt.use_graph = int(bool(moment_shift)), int(bool(use_graph))
+        opt.grad_exchange = int(grad_exchange)
         fp, fk = _ptr(fixed if hasattr(fixed, "data_ptr") else np.asarray(fixed, dtype=np.float32))
         mp, mk = _ptr(moving if hasattr(moving, "data_ptr") else np.asarray(moving, dtype=np.float32))
         dims = (ctypes.c_int64 * 3)(*self.dims)
@@ -339,6 +358,12 @@ class Srwcr:
         s = _Stats()
         self._check(lib().srwcr_get_stats(self._ctx, ctypes.byref(s)))
         return {f: getattr(s, f) for f, _ in _Stats._fields_}
+
+    def grad_layers(self):
+        """plan_layers of this context's rank: (t0, t1, o0, o1, r1)."""
+        out = (ctypes.c_int64 * 5)()
+        self._check(lib().srwcr_grad_layers(self._ctx, out))
+        return tuple(out)
 
     def stream_handle(self) -> int:
         p = ctypes.c_void_p()

@@ -33,6 +33,12 @@ struct NcclApi {
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*Broadcast)(const void *, void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
     const char *(*GetErrorString)(ncclResult_t) = nullptr;
+    // point-to-point (the halo gradient exchange)
+    bool p2p = false;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
 };
 NcclApi &nccl() {
     static NcclApi api;
@@ -48,6 +54,11 @@ NcclApi &nccl() {
             api.Broadcast = (decltype(api.Broadcast))dlsym(h, "ncclBroadcast");
             api.GetErrorString = (decltype(api.GetErrorString))dlsym(h, "ncclGetErrorString");
             api.ok = api.CommInitRank && api.AllReduce && api.CommDestroy && api.GetErrorString && api.Broadcast;
+            api.GroupStart = (decltype(api.GroupStart))dlsym(h, "ncclGroupStart");
+            api.GroupEnd = (decltype(api.GroupEnd))dlsym(h, "ncclGroupEnd");
+            api.Send = (decltype(api.Send))dlsym(h, "ncclSend");
+            api.Recv = (decltype(api.Recv))dlsym(h, "ncclRecv");
+            api.p2p = api.ok && api.GroupStart && api.GroupEnd && api.Send && api.Recv;
         }
     }
     return api;
@@ -92,6 +103,9 @@ struct srwcr_ctx {
     double *NQ = nullptr;                            // orientation 1: dynamic counts [R][B][2]
     int gstride = 0;                                 // row stride of the gamma table
     int pz0 = 0, pzb1 = 0, pz1 = 0;                  // node layers the slab reads: [pz0, pz1), bases < pzb1
+    int64_t lay[5] = {0, 0, 0, 0, 0};                // srwcr_plan_layers of this rank (3-D)
+    bool halo = false;                               // grad_exchange = 1: halo sum instead of the all-reduce
+    long long *halo_recv = nullptr;                  //   rank - 1's partial on layers [lay[2], lay[4])
     double *Nlo = nullptr, *Nup = nullptr, *dterm = nullptr, *reg = nullptr, *Dout = nullptr;
     unsigned *ticket = nullptr;   // k_combine's last-CTA ticket
     double *dpart = nullptr;      // k_combine's per-CTA partial sums
@@ -256,6 +270,47 @@ extern "C" srwcr_status srwcr_plan_slab(int64_t nz, int32_t nranks, int32_t rank
     if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !z0 || !z1) return SRWCR_EINVAL;
     *z0 = nz * rank / nranks;
     *z1 = nz * (rank + 1) / nranks;
+    return SRWCR_OK;
+}
+
+// touched node layers [t0, t1) of the slab [z0, z1): the bases of its first and last slice
+// and the 3 further taps (Eq 17), clipped to the lattice
+static void slab_layers(const int32_t *cbz, int64_t z0, int64_t z1, int64_t gz, int64_t &t0, int64_t &t1) {
+    t0 = cbz[z0];
+    t1 = std::min<int64_t>((int64_t)cbz[z1 - 1] + 4, gz);
+}
+
+extern "C" srwcr_status srwcr_plan_layers(int64_t nz, int32_t nranks, int32_t rank, const int32_t *cbz, int64_t gz,
+                                          int64_t out[5]) {
+    if (nz < 1 || nranks < 1 || rank < 0 || rank >= nranks || !cbz || gz < 1 || !out || nz < nranks)
+        return SRWCR_EINVAL;
+    for (int64_t z = 0; z < nz; ++z)
+        if (cbz[z] < 0 || cbz[z] >= gz || (z > 0 && cbz[z] < cbz[z - 1])) return SRWCR_EINVAL;
+    // owned layers of rank k: [t0_k, t0_{k+1}) (rank 0 from 0, the last rank to gz); valid
+    // iff no rank's touched layers reach past its upper neighbour's owned range, so the only
+    // exchange is rank k -> k + 1 (checked for every k: every rank reaches the same verdict)
+    std::vector<int64_t> t0(nranks), t1(nranks);
+    for (int k = 0; k < nranks; ++k) {
+        int64_t z0, z1;
+        srwcr_plan_slab(nz, nranks, k, &z0, &z1);
+        slab_layers(cbz, z0, z1, gz, t0[k], t1[k]);
+    }
+    auto own0 = [&](int k) { return k == 0 ? (int64_t)0 : t0[k]; };
+    auto own1 = [&](int k) { return k + 1 == nranks ? gz : t0[k + 1]; };
+    for (int k = 0; k + 1 < nranks; ++k)
+        if (t1[k] > own1(k + 1)) return SRWCR_EINVAL;
+    out[0] = t0[rank];
+    out[1] = t1[rank];
+    out[2] = own0(rank);
+    out[3] = own1(rank);
+    out[4] = rank == 0 ? out[2] : std::max(out[2], t1[rank - 1]);
+    return SRWCR_OK;
+}
+
+extern "C" srwcr_status srwcr_grad_layers(const srwcr_ctx *c, int64_t out[5]) {
+    if (!c || !out) return SRWCR_EINVAL;
+    if (c->g.ndim != 3 || c->lay[1] <= c->lay[0]) return SRWCR_ENOTSUP;
+    for (int i = 0; i < 5; ++i) out[i] = c->lay[i];
     return SRWCR_OK;
 }
 
@@ -824,6 +879,35 @@ static srwcr_status launch_fast_p2f(srwcr_ctx *c, const F2Args &A0, int i0, int 
     CKL();
     return SRWCR_OK;
 }
+// Halo gradient exchange: instead of the all-reduce of the whole int64
+// gradient, rank k sends its partial on the layers [o1, t1) that rank k + 1 owns and receives
+// rank k - 1's partial on its own layers [o0, r1) (srwcr_plan_layers: no other rank touches
+// them), adds it and zeroes every layer it does not own.  Integer adds of the same two
+// partials: the owned layers hold the all-reduce's bits; the rank gradients partition the
+// full gradient.  One ncclSend / ncclRecv per component (the layers of one component are
+// contiguous), grouped; captured in the evaluation graph like the all-reduce.
+static srwcr_status halo_exchange(srwcr_ctx *c) {
+    const Geo &g = c->g;
+    const long long plane = (long long)g.Gx * g.Gy;
+    const long long t1 = c->lay[1], o0 = c->lay[2], o1 = c->lay[3], r1 = c->lay[4];
+    const long long nsend = std::max(0LL, t1 - o1), nrecv = r1 - o0;
+    NCK(nccl().GroupStart());
+    for (int d = 0; d < g.ndim; ++d) {
+        if (nsend > 0 && c->rank + 1 < c->nranks)
+            NCK(nccl().Send(c->gradi + ((long long)d * g.Gz + o1) * plane, (size_t)(nsend * plane), ncclInt64,
+                            c->rank + 1, c->comm, c->stream));
+        if (nrecv > 0 && c->rank > 0)
+            NCK(nccl().Recv(c->halo_recv + (long long)d * nrecv * plane, (size_t)(nrecv * plane), ncclInt64,
+                            c->rank - 1, c->comm, c->stream));
+    }
+    NCK(nccl().GroupEnd());
+    const long long t0 = std::min<long long>(c->lay[0], o0), hi = std::max<long long>(t1, o1);
+    k_halo_finish<<<592, 256, 0, c->stream>>>(reinterpret_cast<long long *>(c->gradi), c->halo_recv, g.ndim, g.Gz,
+                                               plane, t0, hi, o0, o1, c->rank > 0 ? r1 : o0);
+    CKL();
+    return SRWCR_OK;
+}
+
 static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad, bool reduce_int64 = false) {
     F2Args A{};
     A.f = fast_args(c);
@@ -857,7 +941,8 @@ static srwcr_status launch_fast_pass2(srwcr_ctx *c, double *grad, bool reduce_in
     CKL();
     // z-slabs: the int64 gradient partials are summed across ranks before the conversion
     // (exact: the same gradient bits for every rank count)
-    if (reduce_int64) NCK(nccl().AllReduce(c->gradi, c->gradi, (size_t)c->nparams, ncclInt64, ncclSum, c->comm, c->stream));
+    if (reduce_int64 && c->halo) TRY(halo_exchange(c));
+    else if (reduce_int64) NCK(nccl().AllReduce(c->gradi, c->gradi, (size_t)c->nparams, ncclInt64, ncclSum, c->comm, c->stream));
     k_grad_convert<<<592, 256, 0, c->stream>>>(c->gradi, grad, (long long)c->nparams, c->Dout + 2, c->fdxz, 1.0 / c->Z);
     CKL();
     return SRWCR_OK;
@@ -1406,6 +1491,23 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         cudaFree(zb);
     }
     if (c->fast) c->launches_per_eval = c->fsplit ? 8 : 7;   // prep, pass 1 (split: 2 kernels), stats conversion, combine, pass 2, exact fix, gradient conversion
+    // node-layer plan of the slab (srwcr_grad_layers) and the halo gradient exchange
+    if (o.grad_exchange != 0 && o.grad_exchange != 1) return fail(c, SRWCR_EINVAL, "grad_exchange must be 0 or 1");
+    bool plan_ok = false;
+    if (!is2d) {
+        std::vector<int32_t> cbz(c->h_cb[2].begin(), c->h_cb[2].end());
+        plan_ok = srwcr_plan_layers(g.nz, c->nranks, c->rank, cbz.data(), g.Gz, c->lay) == SRWCR_OK;
+    }
+    if (o.grad_exchange == 1) {
+        if (!c->comm) return fail(c, SRWCR_EINVAL, "grad_exchange = 1 needs nccl_id (with the caller-driven exchange the caller sums the partials)");
+        if (is2d || !c->fast) return fail(c, SRWCR_ENOTSUP, "grad_exchange = 1: 3-D configurations of the fast passes only");
+        if (!nccl().p2p) return fail(c, SRWCR_ENCCL, "libnccl has no ncclSend/ncclRecv");
+        if (!plan_ok) return fail(c, SRWCR_EINVAL, "grad_exchange = 1: slabs too thin (a rank's node layers reach past its neighbour's)");
+        c->halo = true;
+        const size_t nrecv = (size_t)g.ndim * (size_t)(c->lay[4] - c->lay[2]) * g.Gx * g.Gy;
+        CK(cudaMalloc(&c->halo_recv, sizeof(long long) * std::max<size_t>(nrecv, 1)));
+        c->launches_per_eval += 1;   // k_halo_finish
+    }
     CK(cudaStreamSynchronize(c->stream));
     return SRWCR_OK;
 }
@@ -1977,7 +2079,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma, c->ticket, c->dpart, c->xbeg, c->fitems, c->fitemw, c->fslotbins,
-                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv, c->fphi4};
+                    c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv, c->fphi4, c->halo_recv};
     for (void *p : bufs)
         if (p) cudaFree(p);
     for (int i = 0; i < 3; ++i) {

@@ -1830,4 +1830,18 @@ __global__ void k_grad_convert_layers(unsigned long long *__restrict__ gi, doubl
     }
 }
 
+// halo gradient exchange (srwcr.cu halo_exchange): over the layers [lo, hi) of every
+// component, zero the layers this rank does not own ([o0, o1)) and add rank - 1's partial
+// (recv: [ndim][r1 - o0][plane]) on the owned layers [o0, r1) -- exact int64 adds
+__global__ void k_halo_finish(long long *__restrict__ gi, const long long *__restrict__ recv, int ndim, int Gz,
+                              long long plane, long long lo, long long hi, long long o0, long long o1, long long r1) {
+    const long long per = (hi - lo) * plane, n = per * ndim, nr = (r1 - o0) * plane;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        const long long c = k / per, r = k - c * per, l = lo + r / plane, p = r - (l - lo) * plane;
+        const long long i = (c * Gz + l) * plane + p;
+        if (l < o0 || l >= o1) gi[i] = 0;
+        else if (l < r1) gi[i] += recv[c * nr + (l - o0) * plane + p];
+    }
+}
+
 }  // namespace srwcr

@@ -135,11 +135,13 @@ def test_dynamic_bin_mismatch_report():
     assert mism <= 1e-4 * m_o.size
 
 
-def test_fast_path_nccl_single_rank_graph():
+@pytest.mark.parametrize("grad_exchange", [0, 1])
+def test_fast_path_nccl_single_rank_graph(grad_exchange):
     """The library-driven z-slab exchange (int64 ncclAllReduce of the statistics and of the
-    gradient, captured into the per-rank CUDA graph with the kernels) on one rank: bitwise
-    the result of the context without a communicator (both compute the same deterministic
-    static counts), and bitwise reproducible across graph replays."""
+    gradient -- or, grad_exchange = 1, the grouped ncclSend/Recv halo exchange and
+    k_halo_finish -- captured into the per-rank CUDA graph with the kernels) on one rank:
+    bitwise the result of the context without a communicator (both compute the same
+    deterministic static counts), and bitwise reproducible across graph replays."""
     torch = pytest.importorskip("torch")
     import paper_1804_05061_b200 as S
     import synth
@@ -150,8 +152,13 @@ def test_fast_path_nccl_single_rank_graph():
     cfg = synth.config("C5", FAST_DIMS["C5"])
     F, M = synth.make_pair("C5", 1, cfg["dims"])
     g2 = S.Srwcr(F, M, cfg["spacing"], cfg["bins"], cfg["cells"], cfg["control_mm"], nranks=1, rank=0,
-                 nccl_id=torch.cuda.nccl.unique_id())
+                 nccl_id=torch.cuda.nccl.unique_id(), grad_exchange=grad_exchange)
     assert g2.stats()["fast_path"] == 1
+    gz = g2.params_shape[1]
+    assert g2.grad_layers() == (0, gz, 0, gz, 0)
+    if grad_exchange:
+        with pytest.raises(S.SrwcrError):   # the in-library L-BFGS is replicated: it needs the all-reduce
+            g2.register(None, max_iter=1)
     gt2 = torch.empty_like(pt)
     D2, _ = g2.eval(pt, grad=gt2)      # captured
     g2c = gt2.clone()

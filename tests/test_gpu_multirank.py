@@ -33,7 +33,7 @@ def _free_port():
     return p
 
 
-def _rank_main(rank, world, port, out_dir):
+def _rank_main(rank, world, port, out_dir, halo=False):
     import torch
     import torch.distributed as dist
 
@@ -52,7 +52,24 @@ def _rank_main(rank, world, port, out_dir):
     dist.all_reduce(h, op=dist.ReduceOp.SUM)
     _h2d(p, h.numpy())
     D, grad = g.eval_end()
-    gt = torch.from_numpy(np.ascontiguousarray(grad))
+    gt = torch.from_numpy(np.ascontiguousarray(grad)).reshape(g.params_shape)
+    if halo:
+        # the halo exchange by the library's layer plan: the partial is
+        # zero outside the touched layers; rank k sends [o1, t1) to k + 1 and adds rank
+        # k - 1's [o0, r1); each rank then holds the gradient on its owned layers only
+        t0, t1, o0, o1, r1 = g.grad_layers()
+        cbz = g.debug_dump("ctrl_taps")[DIMS[0] + DIMS[1]:]   # the z part (Nx + Ny + Nz values)
+        assert (t0, t1, o0, o1, r1) == S.plan_layers(DIMS[2], world, rank, cbz, g.params_shape[1])
+        assert not gt[:, :t0].any() and not gt[:, t1:].any()
+        if rank + 1 < world and t1 > o1:
+            dist.send(gt[:, o1:t1].contiguous(), rank + 1)
+        if rank > 0 and r1 > o0:
+            buf = torch.empty_like(gt[:, o0:r1])
+            dist.recv(buf, rank - 1)
+            gt[:, o0:r1] += buf
+        gt[:, :o0] = 0
+        gt[:, o1:] = 0
+        np.save(os.path.join(out_dir, f"own{rank}.npy"), np.array([o0, o1]))
     dist.all_reduce(gt, op=dist.ReduceOp.SUM)
     if rank == 0:
         np.save(os.path.join(out_dir, "grad.npy"), gt.numpy())
@@ -85,7 +102,8 @@ def _h2d(p, h):
     assert _cudart().cudaMemcpy(ctypes.c_void_p(p), h.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(h.nbytes), 1) == 0
 
 
-def test_two_rank_library_gloo_exchange():
+@pytest.mark.parametrize("halo", [False, True])
+def test_two_rank_library_gloo_exchange(halo):
     import torch.multiprocessing as mp
 
     import oracle as O
@@ -99,9 +117,12 @@ def test_two_rank_library_gloo_exchange():
     D1, grad1 = g1.eval(params)
     g1.close()
     with tempfile.TemporaryDirectory() as td:
-        mp.start_processes(_rank_main, args=(2, _free_port(), td), nprocs=2, join=True, start_method="spawn")
+        mp.start_processes(_rank_main, args=(2, _free_port(), td, halo), nprocs=2, join=True, start_method="spawn")
         D2 = float(np.load(os.path.join(td, "D.npy"))[0])
         grad2 = np.load(os.path.join(td, "grad.npy")).reshape(grad1.shape)
+        if halo:   # the owned ranges partition the node layers
+            own = [np.load(os.path.join(td, f"own{r}.npy")) for r in range(2)]
+            assert own[0][0] == 0 and own[0][1] == own[1][0] and own[1][1] == grad1.shape[1]
     assert D2 == D1, (D2, D1)
     assert np.linalg.norm(grad2 - grad1) / np.linalg.norm(grad1) <= 1e-14
     L = cfg["bins"] - 1

@@ -162,6 +162,103 @@ def test_oracle_zslab_algebra_gloo_two_ranks():
     assert gerr <= 1e-12
 
 
+def _halo_rank_main(rank, world, port, q):
+    """The halo gradient exchange on the oracle's slab partials: the
+    library's host-only layer plan decides what rank k sends to k + 1; after the exchange
+    each rank keeps its owned layers, and the rank gradients must partition the full one."""
+    import torch
+    import torch.distributed as dist
+
+    import oracle as O
+    import synth
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.config("C3", (40, 36, 30))
+        F, M = synth.make_pair("C3", 1, cfg["dims"])
+        L = cfg["bins"] - 1
+        delta = tuple(c / s for c, s in zip(cfg["control_mm"], cfg["spacing"]))
+        pb = O.Problem(dims=cfg["dims"], L=L, delta=delta, kcells=cfg["cells"], nthreads=1)
+        Fn, Mn = O.normalize(F, L), O.normalize(M, L)
+        params = synth.make_params(pb.params_shape, "small", 1)
+        nz, gz = cfg["dims"][2], pb.params_shape[1]
+        cbz = [O.taps(z, delta[2])[0] for z in range(nz)]
+        t0, t1, o0, o1, r1 = S.plan_layers(nz, world, rank, cbz, gz)
+        z0, z1 = S.plan_slab(nz, world, rank)
+        N, Sm, Q = (torch.from_numpy(t) for t in O.moments(pb, Fn, Mn, params, z0, z1))
+        for t in (N, Sm, Q):
+            dist.all_reduce(t)
+        D, al, be, ga, reg, Z = O.combine(pb, N.numpy(), Sm.numpy(), Q.numpy())
+        g = torch.from_numpy(O.grad_moments(pb, Fn, Mn, params, al, be, ga, Z, z0, z1))   # [ndim, Gz, Gy, Gx]
+        # the partial is zero outside the touched layers (Eq 17 taps of slices z0 .. z1-1)
+        assert not g[:, :t0].any() and not g[:, t1:].any()
+        reqs = []
+        if rank + 1 < world and t1 > o1:
+            reqs.append(dist.isend(g[:, o1:t1].contiguous(), rank + 1))
+        if rank > 0 and r1 > o0:
+            buf = torch.empty_like(g[:, o0:r1])
+            dist.recv(buf, rank - 1)
+            g[:, o0:r1] += buf
+        for r in reqs:
+            r.wait()
+        g[:, :o0] = 0
+        g[:, o1:] = 0
+        owned = torch.zeros(gz, dtype=torch.int64)
+        owned[o0:o1] = 1
+        dist.all_reduce(owned)
+        gsum = g.clone()
+        dist.all_reduce(gsum)
+        if rank == 0:
+            D1, g1 = O.eval_moments(pb, Fn, Mn, params)
+            q.put((owned.tolist(), float(np.linalg.norm(gsum.numpy() - g1) / np.linalg.norm(g1))))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_halo_gradient_exchange_plan_gloo(world):
+    import torch.multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_halo_rank_main, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    owned, gerr = q.get(timeout=10)
+    assert all(o == 1 for o in owned)   # the owned ranges partition the node layers
+    assert gerr <= 1e-12
+
+
+def test_plan_layers_properties():
+    """Host-only layer plan: touched ranges follow the Eq 17 taps of the slab's slices, the
+    owned ranges partition [0, Gz), and slabs thinner than the taps are refused."""
+    import oracle as O
+    nz, d = 96, 6.0
+    cbz = [O.taps(z, d)[0] for z in range(nz)]
+    gz = max(cbz) + 4
+    for P in (1, 2, 3, 4):
+        plans = [S.plan_layers(nz, P, k, cbz, gz) for k in range(P)]
+        assert plans[0][2] == 0 and plans[-1][3] == gz
+        for k, (t0, t1, o0, o1, r1) in enumerate(plans):
+            z0, z1 = S.plan_slab(nz, P, k)
+            assert (t0, t1) == (cbz[z0], min(cbz[z1 - 1] + 4, gz))
+            assert o0 <= o1 and o0 <= r1 <= o1
+            if k > 0:
+                assert o0 == plans[k - 1][3] and r1 == max(o0, plans[k - 1][1])
+    assert S.plan_layers(nz, 1, 0, cbz, gz) == (0, gz, 0, gz, 0)
+    with pytest.raises(S.SrwcrError):
+        S.plan_layers(nz, 5, 0, cbz, gz)    # 19-slice slabs: rank 0 reaches rank 2's layers
+    with pytest.raises(S.SrwcrError):
+        S.plan_layers(nz, 2, 0, cbz[::-1], gz)   # bases must not decrease
+    with pytest.raises(S.SrwcrError):
+        S.plan_layers(nz, 2, 2, cbz, gz)
+
+
 def test_buffer_marshalling_rejects_wrong_params_and_outputs():
     """The binding hands raw pointers to the C ABI, which reads / writes nparams doubles:
     wrong dtypes or sizes, and non-contiguous outputs, must be refused before the call."""
