@@ -65,6 +65,8 @@ NcclApi &nccl() {
 }
 }  // namespace
 
+constexpr int NPART = 8;   // pipelined host evaluation: at most this many concurrent parts per pass
+
 struct srwcr_ctx {
     std::string err;
     bool poisoned = false;
@@ -134,6 +136,11 @@ struct srwcr_ctx {
     // gradient D2H with pass 2, on a second stream
     cudaStream_t cstream = nullptr;
     cudaEvent_t pev[4]{};
+    cudaStream_t kst[NPART]{};             // pipelined host evaluation: part j of a pass runs on kst[j],
+    cudaEvent_t pex[12]{};                 //   priority decreasing with j (upload / prep / part-done events)
+    bool fconc = false;                    //   (concurrent parts, no drain at the boundaries)
+    bool fconc2 = false;                   //   (pass 2 too)
+    int xparts = 1;                        // exact-path lists of the last evaluation (pinned + 2)
     int *xbeg = nullptr;
     // pass 1 in parts: items [p1_b[j], p1_b[j+1]) need params layers [0, p1_l[j]); pass 2 in
     // parts: after items [0, p2_b[j+1]) the gradient layers [0, p2_l[j]) are final
@@ -668,7 +675,20 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
         if (nn >= 6 * wave) {
             const int np = std::min(4, std::max(2, atoi(getenv("SRWCR_PIPE_P1") ? getenv("SRWCR_PIPE_P1") : "2")));
             std::vector<int> b = {0}, l;
-            for (int k = 1; k < np; ++k) b.push_back(k * wave);
+            c->fconc = !getenv("SRWCR_PIPE_CONC") || atoi(getenv("SRWCR_PIPE_CONC")) != 0;
+            c->fconc2 = c->fconc && (!getenv("SRWCR_PIPE_CONC2") || atoi(getenv("SRWCR_PIPE_CONC2")) != 0);
+            if (c->fconc) {
+                // concurrent parts (each on its own stream: a part's items fill the SMs the
+                // previous part's last wave leaves, so a boundary costs no drain): q, q, 2q items
+                // and the rest, q = the items of the first z-run (its layers go up first)
+                int q = 0;
+                while (q < nn && fi[q].z0 == fi[0].z0) ++q;
+                if (const char *e = getenv("SRWCR_PIPE_Q")) q = std::max(1, atoi(e));
+                for (int k : {q, 2 * q, 4 * q})
+                    if (k < nn) b.push_back(k);
+            } else {
+                for (int k = 1; k < np; ++k) b.push_back(k * wave);
+            }
             b.push_back(nn);
             for (size_t j = 0; j + 1 < b.size(); ++j) {
                 int hi = 0;
@@ -686,8 +706,24 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
             // the first pass-2 boundary sits k2 waves before the end (its final layers go back while
             // the last k2 waves run), later ones one wave apart
             const int k2 = std::max(np2 - 1, atoi(getenv("SRWCR_PIPE_P2K") ? getenv("SRWCR_PIPE_P2K") : "2"));
-            std::vector<int> b2 = {0, nn - k2 * wave}, l2;
-            for (int k = np2 - 2; k >= 1; --k) b2.push_back(nn - k * wave);
+            std::vector<int> b2 = {0}, l2;
+            if (c->fconc2) {
+                // concurrent parts: the last five z-runs of items one by one (the fewest
+                // layers go back after the last kernel, the first ones early), the rest.
+                // (C5 e2e, evals/s: serial parts 397; concurrent pass-1 parts 410; + concurrent
+                // pass-2 parts, trailing z-runs 1 / 2 / 3 / 5 / 7: 398 / 409 / 421 / 437 / 421 --
+                // 7 exceeds the device's 6 stream priorities; without
+                // cudaGraphInstantiateFlagUseNodePriority the graph ignores them: 402)
+                int q = 0;
+                while (q < nn && fi[nn - 1 - q].z0 == fi[nn - 1].z0) ++q;
+                if (const char *e = getenv("SRWCR_PIPE_Q2")) q = std::max(1, atoi(e));
+                const int nt = std::min(NPART - 1, std::max(1, atoi(getenv("SRWCR_PIPE_P2N") ? getenv("SRWCR_PIPE_P2N") : "5")));
+                for (int k = nt; k >= 1; --k)
+                    if (nn - k * q > b2.back()) b2.push_back(nn - k * q);
+            } else {
+                b2.push_back(nn - k2 * wave);
+                for (int k = np2 - 2; k >= 1; --k) b2.push_back(nn - k * wave);
+            }
             b2.push_back(nn);
             for (size_t j = 0; j + 1 < b2.size(); ++j) {
                 int lo = g.GzExt;
@@ -783,7 +819,8 @@ static FArgs fast_args(srwcr_ctx *c) {
 }
 
 // fast pass 1 over items [i0, i0 + cnt) and the int64 -> fp64 statistics conversion
-static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bool convert = true) {
+static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bool convert = true, cudaStream_t st = nullptr) {
+    cudaStream_t ks = st ? st : c->stream;
     FArgs a = fast_args(c);
     a.i0 = i0;
     const int n = cnt >= 0 ? cnt : c->nfitems - i0;
@@ -798,34 +835,34 @@ static srwcr_status launch_fast_pass1(srwcr_ctx *c, int i0 = 0, int cnt = -1, bo
         const int Tw = 32 * c->fWw, T = 32 * c->fW;
         const size_t smw = c->fsmemw;
         if (c->fXV == 2) {
-            if (Tw <= 256 && c->fMinbW == 3) k_p1w<2, 256, 3><<<n, Tw, smw, c->stream>>>(aw);
-            else if (Tw <= 256) k_p1w<2, 256, 2><<<n, Tw, smw, c->stream>>>(aw);
-            else k_p1w<2, 512, 1><<<n, Tw, smw, c->stream>>>(aw);
+            if (Tw <= 256 && c->fMinbW == 3) k_p1w<2, 256, 3><<<n, Tw, smw, ks>>>(aw);
+            else if (Tw <= 256) k_p1w<2, 256, 2><<<n, Tw, smw, ks>>>(aw);
+            else k_p1w<2, 512, 1><<<n, Tw, smw, ks>>>(aw);
             CKL();
-            if (T > 384) k_p1f<2, 512, 2><<<n, T, c->fsmem1, c->stream>>>(a);
-            else if (T > 256) k_p1f<2, 384, 2><<<n, T, c->fsmem1, c->stream>>>(a);
-            else k_p1f<2, 256, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            if (T > 384) k_p1f<2, 512, 2><<<n, T, c->fsmem1, ks>>>(a);
+            else if (T > 256) k_p1f<2, 384, 2><<<n, T, c->fsmem1, ks>>>(a);
+            else k_p1f<2, 256, 2><<<n, T, c->fsmem1, ks>>>(a);
         } else {
-            if (Tw <= 256 && c->fMinbW == 3) k_p1w<1, 256, 3><<<n, Tw, smw, c->stream>>>(aw);
-            else if (Tw <= 256) k_p1w<1, 256, 2><<<n, Tw, smw, c->stream>>>(aw);
-            else k_p1w<1, 512, 1><<<n, Tw, smw, c->stream>>>(aw);
+            if (Tw <= 256 && c->fMinbW == 3) k_p1w<1, 256, 3><<<n, Tw, smw, ks>>>(aw);
+            else if (Tw <= 256) k_p1w<1, 256, 2><<<n, Tw, smw, ks>>>(aw);
+            else k_p1w<1, 512, 1><<<n, Tw, smw, ks>>>(aw);
             CKL();
-            if (T > 384) k_p1f<1, 512, 2><<<n, T, c->fsmem1, c->stream>>>(a);
-            else if (T > 256) k_p1f<1, 384, 2><<<n, T, c->fsmem1, c->stream>>>(a);
-            else k_p1f<1, 256, 2><<<n, T, c->fsmem1, c->stream>>>(a);
+            if (T > 384) k_p1f<1, 512, 2><<<n, T, c->fsmem1, ks>>>(a);
+            else if (T > 256) k_p1f<1, 384, 2><<<n, T, c->fsmem1, ks>>>(a);
+            else k_p1f<1, 256, 2><<<n, T, c->fsmem1, ks>>>(a);
         }
         CKL();
     } else if (n > 0) {
         const int T = 32 * c->fW;
         if (c->fXV == 2) {
-            if (T > 384) k_p1f<2, 512><<<n, T, c->fsmem1, c->stream>>>(a);
-            else if (T > 256) k_p1f<2, 384><<<n, T, c->fsmem1, c->stream>>>(a);
-            else k_p1f<2, 256><<<n, T, c->fsmem1, c->stream>>>(a);
+            if (T > 384) k_p1f<2, 512><<<n, T, c->fsmem1, ks>>>(a);
+            else if (T > 256) k_p1f<2, 384><<<n, T, c->fsmem1, ks>>>(a);
+            else k_p1f<2, 256><<<n, T, c->fsmem1, ks>>>(a);
         } else {
-            if (T > 512) k_p1f<1, 768><<<n, T, c->fsmem1, c->stream>>>(a);
-            else if (T > 384) k_p1f<1, 512><<<n, T, c->fsmem1, c->stream>>>(a);
-            else if (T > 256) k_p1f<1, 384><<<n, T, c->fsmem1, c->stream>>>(a);
-            else k_p1f<1, 256><<<n, T, c->fsmem1, c->stream>>>(a);
+            if (T > 512) k_p1f<1, 768><<<n, T, c->fsmem1, ks>>>(a);
+            else if (T > 384) k_p1f<1, 512><<<n, T, c->fsmem1, ks>>>(a);
+            else if (T > 256) k_p1f<1, 384><<<n, T, c->fsmem1, ks>>>(a);
+            else k_p1f<1, 256><<<n, T, c->fsmem1, ks>>>(a);
         }
         CKL();
     }
@@ -862,19 +899,20 @@ static F2Args fast_pass2_args(srwcr_ctx *c) {
     A.L2 = p2_smem(c->fW2, c->fS, c->fnpmax, c->fzmax);
     return A;
 }
-static srwcr_status launch_fast_p2f(srwcr_ctx *c, const F2Args &A0, int i0, int n) {
+static srwcr_status launch_fast_p2f(srwcr_ctx *c, const F2Args &A0, int i0, int n, cudaStream_t st = nullptr) {
     if (n <= 0) return SRWCR_OK;
     F2Args A = A0;
     A.f.i0 = i0;
     const int T = 32 * c->fW2;
+    cudaStream_t ks = st ? st : c->stream;
     if (c->fXV == 2) {
-        if (T > 384) k_p2f<2, 512><<<n, T, c->fsmem2, c->stream>>>(A);
-        else if (T > 256) k_p2f<2, 384><<<n, T, c->fsmem2, c->stream>>>(A);
-        else k_p2f<2, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+        if (T > 384) k_p2f<2, 512><<<n, T, c->fsmem2, ks>>>(A);
+        else if (T > 256) k_p2f<2, 384><<<n, T, c->fsmem2, ks>>>(A);
+        else k_p2f<2, 256><<<n, T, c->fsmem2, ks>>>(A);
     } else {
-        if (T > 384) k_p2f<1, 512><<<n, T, c->fsmem2, c->stream>>>(A);
-        else if (T > 256) k_p2f<1, 384><<<n, T, c->fsmem2, c->stream>>>(A);
-        else k_p2f<1, 256><<<n, T, c->fsmem2, c->stream>>>(A);
+        if (T > 384) k_p2f<1, 512><<<n, T, c->fsmem2, ks>>>(A);
+        else if (T > 256) k_p2f<1, 384><<<n, T, c->fsmem2, ks>>>(A);
+        else k_p2f<1, 256><<<n, T, c->fsmem2, ks>>>(A);
     }
     CKL();
     return SRWCR_OK;
@@ -998,11 +1036,19 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaSetDevice(c->dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&c->ev[i]));
-    CK(cudaMallocHost(&c->pinned, 4 * sizeof(double)));
+    CK(cudaMallocHost(&c->pinned, (2 + NPART / 2) * sizeof(double)));   // D, #retained, then NPART int counts
     CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->pev[i], cudaEventDisableTiming));
+    {   // part streams: the earlier part's CTAs are dispatched first, a later part fills the SMs
+        // its last wave leaves
+        int least = 0, greatest = 0;
+        CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        for (int i = 0; i < NPART; ++i)
+            CK(cudaStreamCreateWithPriority(&c->kst[i], cudaStreamNonBlocking, std::min(least, greatest + i)));
+    }
+    for (int i = 0; i < 12; ++i) CK(cudaEventCreateWithFlags(&c->pex[i], cudaEventDisableTiming));
     CK(cudaMalloc(&c->xbeg, sizeof(int)));
-    memset(c->pinned, 0, 4 * sizeof(double));
+    memset(c->pinned, 0, (2 + NPART / 2) * sizeof(double));
 
     // per-axis tables (fp64 on host -> device), control and spatial lattices
     for (int ax = 0; ax < 3; ++ax) {
@@ -1320,8 +1366,8 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         c->xcap = (int)std::min<int64_t>(std::max<int64_t>(4096, sv / 16), 1 << 30);
         if (const char *e = getenv("SRWCR_XCAP")) c->xcap = std::max(1, atoi(e));  // tests: force the scan fallback
         CK(cudaMalloc(&c->xlist, sizeof(int) * (size_t)c->xcap));
-        CK(cudaMalloc(&c->xcount, sizeof(int)));
-        CK(cudaMemset(c->xcount, 0, sizeof(int)));
+        CK(cudaMalloc(&c->xcount, NPART * sizeof(int)));   // [0]: the list's count ([1..]: pipelined parts)
+        CK(cudaMemset(c->xcount, 0, NPART * sizeof(int)));
     }
     CK(cudaMalloc(&c->MG, sizeof(float4) * (size_t)std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy)));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
@@ -1790,21 +1836,34 @@ static srwcr_status enqueue_host_pipelined_fast(srwcr_ctx *c, const double *para
     CK(cudaStreamWaitEvent(c->cstream, c->pev[3], 0));
     c->cur_params = c->params64;
     const int np1 = (int)c->fp1_l.size();
+    // concurrent parts: part j > 0 on its own stream, after its upload and the previous part's
+    // prep (its items read the fp32 layers the earlier preps converted); the int64 statistics
+    // adds of the parts commute, so the result is the same bits in any interleaving
+    const bool conc = c->fconc && np1 <= 4;   // (pex: 4 uploads, 4 preps, 4 part ends)
+    if (conc)
+        for (int j = 0; j < np1; ++j) CK(cudaStreamWaitEvent(c->kst[j], c->pev[3], 0));
     int lo = 0;
     for (int j = 0; j < np1; ++j) {
         const int hi = c->fp1_l[j];
+        cudaStream_t ks = conc ? c->kst[j] : c->stream;
         TRY(copy_layers(c->params64, params, lo, hi, cudaMemcpyHostToDevice, c->cstream));
-        CK(cudaEventRecord(c->pev[0], c->cstream));
-        CK(cudaStreamWaitEvent(c->stream, c->pev[0], 0));
+        cudaEvent_t up = conc ? c->pex[j] : c->pev[0];
+        CK(cudaEventRecord(up, c->cstream));
+        CK(cudaStreamWaitEvent(ks, up, 0));
+        if (conc && j > 0) CK(cudaStreamWaitEvent(ks, c->pex[4 + j - 1], 0));
         const int b0 = c->fp1_b[j], nb = c->fp1_b[j + 1] - b0;
         const int zl = std::max(lo, c->pz0), zh = j + 1 == np1 ? c->pz1 : std::min(hi, c->pz1);
         const int nconv = zh > zl ? 296 : 0;
-        k_fprep<<<(unsigned)(nconv + nb), 256, 0, c->stream>>>(c->params64, c->fphi4, g, zl, std::max(zl, zh), nconv,
-                                                             c->fitems + b0, nb, t, c->fiflag + b0);
+        k_fprep<<<(unsigned)(nconv + nb), 256, 0, ks>>>(c->params64, c->fphi4, g, zl, std::max(zl, zh), nconv,
+                                                      c->fitems + b0, nb, t, c->fiflag + b0);
         CKL();
-        TRY(launch_fast_pass1(c, b0, nb, false));
+        if (conc) CK(cudaEventRecord(c->pex[4 + j], ks));
+        TRY(launch_fast_pass1(c, b0, nb, false, ks));
+        if (conc) CK(cudaEventRecord(c->pex[8 + j], ks));
         lo = hi;
     }
+    if (conc)
+        for (int j = 0; j < np1; ++j) CK(cudaStreamWaitEvent(c->stream, c->pex[8 + j], 0));
     k_stats_convert<<<592, 256, 0, c->stream>>>(c->SQi, c->SQ, (long long)stats_count(c), (long long)c->R * c->g.B * 2);
     CKL();
     TRY(run_combine(c));
@@ -1817,9 +1876,50 @@ static srwcr_status enqueue_host_pipelined_fast(srwcr_ctx *c, const double *para
         pa.gbound = c->Dout + 2;
         pa.dxz = c->fdxz;
         pa.xbeg = c->xbeg;
+        const int np2 = (int)c->fp2_l.size();
+        if (c->fconc2 && np2 <= NPART) {
+            // concurrent parts: part j on its own stream with its own exact-path list (a quarter
+            // of the capacity: no kernel reads a list another part is still appending to); after
+            // part j and the fix / conversion of part j - 1, part j's deferred voxels are fixed,
+            // the layers final after part j converted and sent back.  An overflow of any part's
+            // list is detected on the host and the evaluation redone without parts.
+            const int cap = c->xcap / NPART;
+            CK(cudaMemsetAsync(c->xcount, 0, NPART * sizeof(int), c->stream));
+            CK(cudaEventRecord(c->pev[2], c->stream));
+            int done = 0;
+            for (int j = 0; j < np2; ++j) {
+                cudaStream_t ks = c->kst[j];
+                CK(cudaStreamWaitEvent(ks, c->pev[2], 0));
+                F2Args Aj = A;
+                Aj.xlist = c->xlist + (size_t)j * cap;
+                Aj.xcount = c->xcount + j;
+                Aj.xcap = cap;
+                TRY(launch_fast_p2f(c, Aj, c->fp2_b[j], c->fp2_b[j + 1] - c->fp2_b[j], ks));
+                if (j > 0) CK(cudaStreamWaitEvent(ks, c->pex[j - 1], 0));   // part j - 1 fixed and converted
+                PassArgs pj = pa;
+                pj.xlist = Aj.xlist;
+                pj.xcount = Aj.xcount;
+                pj.xcap = cap;
+                pj.xbeg = nullptr;
+                pj.xmode = 1;
+                k_exact_fix<0><<<1184, 128, 0, ks>>>(pj);
+                CKL();
+                const int hi = c->fp2_l[j];
+                if (hi > done) {
+                    k_grad_convert_layers<<<592, 256, 0, ks>>>(c->gradi, c->grad64, (long long)plane, (long long)cs, g.ndim,
+                                                               done, hi, c->Dout + 2, c->fdxz, 1.0 / c->Z);
+                    CKL();
+                }
+                CK(cudaEventRecord(c->pex[j], ks));
+                CK(cudaStreamWaitEvent(c->cstream, c->pex[j], 0));
+                TRY(copy_layers(grad, c->grad64, done, hi, cudaMemcpyDeviceToHost, c->cstream));
+                done = std::max(done, hi);
+            }
+            for (int j = 0; j < np2; ++j) CK(cudaStreamWaitEvent(c->stream, c->pex[j], 0));
+            CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, NPART * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        } else {
         CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
         CK(cudaMemsetAsync(c->xbeg, 0, sizeof(int), c->stream));
-        const int np2 = (int)c->fp2_l.size();
         int done = 0;
         for (int j = 0; j < np2; ++j) {
             const bool last = j + 1 == np2;
@@ -1844,6 +1944,7 @@ static srwcr_status enqueue_host_pipelined_fast(srwcr_ctx *c, const double *para
             done = std::max(done, hi);
         }
         CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        }
     }
     // join the copy stream back (a graph capture must end on its origin stream)
     CK(cudaEventRecord(c->pev[1], c->cstream));
@@ -1878,7 +1979,7 @@ static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params,
                 if (gr) cudaGraphDestroy(gr);
                 return st != SRWCR_OK ? st : fail(c, SRWCR_ECUDA, "graph capture failed: %s", cudaGetErrorString(e));
             }
-            const cudaError_t e2 = cudaGraphInstantiate(&c->hexec, gr, 0);
+            const cudaError_t e2 = cudaGraphInstantiate(&c->hexec, gr, cudaGraphInstantiateFlagUseNodePriority);
             cudaGraphDestroy(gr);
             if (e2 != cudaSuccess) {
                 c->hexec = nullptr;
@@ -1895,9 +1996,17 @@ static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params,
     CK(cudaStreamSynchronize(c->cstream));
     CK(cudaStreamSynchronize(c->stream));
     if (grad) {
-        int xc = 0;
-        memcpy(&xc, c->pinned + 2, sizeof(int));
-        if (xc > c->xcap) {
+        int xc[NPART] = {};
+        memcpy(xc, c->pinned + 2, sizeof xc);
+        const int np2 = (int)c->fp2_l.size();
+        bool over = xc[0] > c->xcap;
+        if (c->fconc2 && np2 <= NPART) {
+            over = false;
+            for (int j = 0; j < np2; ++j) over = over || xc[j] > c->xcap / NPART;
+        }
+        c->xparts = c->fconc2 && np2 <= NPART ? np2 : 1;
+        if (over) {
+            c->xparts = 1;
             // list overflow: voxels of layers already converted were fixed by the last part's
             // scan after their conversion (their int64 adds are still in gradi) -- rare;
             // clear the int64 gradient and evaluate again without the parts
@@ -1911,6 +2020,7 @@ static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params,
 
 extern "C" srwcr_status srwcr_eval(srwcr_ctx *c, const double *params, double *value, double *grad) {
     if (!c) return SRWCR_EINVAL;
+    c->xparts = 1;
     if (c->external_exchange) return fail(c, SRWCR_ESTATE, "caller-driven exchange: use srwcr_eval_begin/end");
     if (c->opt.use_graph && !c->poisoned && params && is_device_ptr(params) &&
         (!grad || is_device_ptr(grad)))
@@ -1943,6 +2053,7 @@ extern "C" srwcr_status srwcr_eval_end(srwcr_ctx *c, double *value, double *grad
     if (!c) return SRWCR_EINVAL;
     if (!c->begun) return fail(c, SRWCR_ESTATE, "srwcr_eval_end without srwcr_eval_begin");
     c->begun = false;
+    c->xparts = 1;
     return eval_end_impl(c, value, grad, false);
 }
 
@@ -2049,7 +2160,8 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->exact_capacity = c->xcap;
     out->pipe_items1 = c->p1_split;
     out->pipe_items2 = c->p2_split;
-    out->exact_voxels = c->pinned ? reinterpret_cast<const int *>(c->pinned + 2)[0] : 0;
+    out->exact_voxels = 0;
+    for (int j = 0; c->pinned && j < c->xparts; ++j) out->exact_voxels += reinterpret_cast<const int *>(c->pinned + 2)[j];
     out->fast_path = c->fast ? 1 : 0;
     out->fast_items = c->nfitems;
     out->fast_warps = c->fW;
@@ -2075,6 +2187,10 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     if (c->fMarr) cudaFreeArray(c->fMarr);
     for (int i = 0; i < 4; ++i)
         if (c->pev[i]) cudaEventDestroy(c->pev[i]);
+    for (int i = 0; i < 12; ++i)
+        if (c->pex[i]) cudaEventDestroy(c->pex[i]);
+    for (int i = 0; i < NPART; ++i)
+        if (c->kst[i]) cudaStreamDestroy(c->kst[i]);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,

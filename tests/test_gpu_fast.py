@@ -322,14 +322,18 @@ def test_fast_path_slabs_on_one_gpu(P):
     _check(D, gsum, Do, go)
 
 
-@pytest.mark.parametrize("phi", ["small", "large"])
-def test_pipelined_host_evaluation_bitwise(phi, monkeypatch):
+@pytest.mark.parametrize("phi,conc", [("small", "1"), ("large", "1"), ("small", "0")])
+def test_pipelined_host_evaluation_bitwise(phi, conc, monkeypatch):
     """Host params / gradient buffers: the parts-pipelined evaluation (params uploaded in parts
-    overlapped with pass 1, gradient layers converted and copied back while later pass-2 parts
-    run; parts forced small with SRWCR_PIPE_WAVE) runs the same kernels on item ranges, with
-    integer sums: bitwise the device-buffer evaluation."""
+    overlapped with pass 1 -- the parts concurrent on their own streams, or in one stream with
+    SRWCR_PIPE_CONC=0 -- gradient layers converted and copied back while later pass-2 parts
+    run; parts forced small with SRWCR_PIPE_WAVE / SRWCR_PIPE_Q) runs the same kernels on item
+    ranges, with integer sums: bitwise the device-buffer evaluation."""
     torch = pytest.importorskip("torch")
     monkeypatch.setenv("SRWCR_PIPE_WAVE", "16")
+    monkeypatch.setenv("SRWCR_PIPE_CONC", conc)
+    monkeypatch.setenv("SRWCR_PIPE_Q", "8")
+    monkeypatch.setenv("SRWCR_PIPE_Q2", "8")
     g, pb, Fn, Mn, params = _case("C5", 1, phi)
     st = g.stats()
     assert st["fast_path"] == 1
