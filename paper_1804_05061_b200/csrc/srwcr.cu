@@ -664,19 +664,21 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     c->fsmem1 = p1_smem(W, S, P1ZM(zm)).total;
     c->fzmax = zm;
     c->h_fitems = fi;
-    // pipelined host-buffer evaluation (one rank): pass 1 in parts of one wave, one wave, the
-    // rest (the first params upload part is as small as one wave's layers); pass 2 as all but
-    // three waves, then one wave at a time (the gradient layers final after each part go back
-    // while the next runs).  Items are ordered by z, so both boundaries are layer prefixes.
+    // pipelined host-buffer evaluation (one rank).  Items are ordered by z, so every part
+    // boundary is a layer prefix.  Concurrent parts (default): see below.  Serial parts
+    // (SRWCR_PIPE_CONC=0): pass 1 in parts of one wave, one wave, the rest; pass 2 as all but
+    // two waves, then one wave at a time (each boundary drains a wave, so only for >= 6 waves).
     if (c->nranks == 1 && !getenv("SRWCR_NOPIPE")) {
         int wave = nsm;
         if (const char *e = getenv("SRWCR_PIPE_WAVE")) wave = std::max(1, atoi(e));   // tests: small volumes
         const int nn = (int)n;
-        if (nn >= 6 * wave) {
+        c->fconc = !getenv("SRWCR_PIPE_CONC") || atoi(getenv("SRWCR_PIPE_CONC")) != 0;
+        c->fconc2 = c->fconc && (!getenv("SRWCR_PIPE_CONC2") || atoi(getenv("SRWCR_PIPE_CONC2")) != 0);
+        int q0 = 0;   // items of the first z-run
+        while (q0 < nn && fi[q0].z0 == fi[0].z0) ++q0;
+        if (c->fconc ? (nn >= wave && nn >= 3 * q0) : nn >= 6 * wave) {
             const int np = std::min(4, std::max(2, atoi(getenv("SRWCR_PIPE_P1") ? getenv("SRWCR_PIPE_P1") : "2")));
             std::vector<int> b = {0}, l;
-            c->fconc = !getenv("SRWCR_PIPE_CONC") || atoi(getenv("SRWCR_PIPE_CONC")) != 0;
-            c->fconc2 = c->fconc && (!getenv("SRWCR_PIPE_CONC2") || atoi(getenv("SRWCR_PIPE_CONC2")) != 0);
             if (c->fconc) {
                 // concurrent parts (each on its own stream: a part's items fill the SMs the
                 // previous part's last wave leaves, so a boundary costs no drain): q, q, 2q items
