@@ -353,6 +353,30 @@ def test_pipelined_host_evaluation_bitwise(phi, conc, monkeypatch):
     assert np.array_equal(g1, g4) and np.array_equal(g1, hg.numpy())
 
 
+def test_pipelined_concurrent_parts_list_overflow(monkeypatch):
+    """The concurrent pass-2 parts give each part its own exact-path list; with the capacity
+    forced to 1 (0 per part) every part with a deferred voxel overflows, the host sees it
+    and redoes the evaluation without parts (the slab scan fixes the voxels): bitwise the
+    device-buffer evaluation, which overflows and scans too."""
+    torch = pytest.importorskip("torch")
+    monkeypatch.setenv("SRWCR_PIPE_WAVE", "16")
+    monkeypatch.setenv("SRWCR_PIPE_Q", "8")
+    monkeypatch.setenv("SRWCR_PIPE_Q2", "8")
+    monkeypatch.setenv("SRWCR_XCAP", "1")
+    g, pb, Fn, Mn, params = _case("C5", 1, "large")
+    assert g.stats()["exact_capacity"] == 1
+    hp = torch.from_numpy(params.copy()).pin_memory()
+    hg = torch.empty_like(hp).pin_memory()
+    D1, _ = g.eval(hp, grad=hg)
+    assert g.stats()["exact_voxels"] > 1
+    pt = hp.cuda()
+    gt = torch.empty_like(pt)
+    D2, _ = g.eval(pt, grad=gt)
+    g.close()
+    assert D1 == D2 and np.array_equal(hg.numpy(), gt.cpu().numpy())
+    _check(D1, hg.numpy(), *__import__("oracle").eval_moments(pb, Fn, Mn, params))
+
+
 def test_value_only_evaluation():
     """srwcr_eval with grad = NULL (the L-BFGS line-search trials) runs pass 1 and the combine
     only: the same D, bitwise, as the value + gradient evaluation, on host and device buffers
