@@ -487,7 +487,7 @@ static srwcr_status run_combine(srwcr_ctx *c) {
 // pass 1 keeps its per-slice tables at FZMAX (its row-offset stride is a compile-time
 // constant: a runtime stride cost ~1 %); pass 2 sizes them by the items' z-range (room for its
 // row-buffer copies)
-static inline int P1ZM(int) { return FZMAX; }
+static inline int P1ZM(int zm) { return LTC == 4 ? zm : FZMAX; }   // (4 line-table copies: room from the z-range)
 static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     const Geo &g = c->g;
     if (getenv("SRWCR_NOFAST")) return SRWCR_OK;

@@ -217,7 +217,7 @@ __host__ __device__ inline P1Smem p1_smem(int W, int S, int ZM = FZMAX) {
     o.sh = take(S * 4);                  // float  SH[S]  per-slot shift
     o.ts = take(160 * 4);                // int    TS[]   touched-slot list of a round
     o.rr = take(W * RRING * 64 * 4);     // unsigned RR[W][RRING][XV * 32] record ring (TMA bulk / cp.async)
-    o.rbar = take(W * RRING * 8);        // mbarrier RB[W][RRING] of the ring's bulk copies
+    o.rbar = take(SRWCR_P1_TMA_REC || LTC != 4 ? W * RRING * 8 : 0);   // mbarrier RB[W][RRING] of the ring's bulk copies
     o.total = off;
     return o;
 }
@@ -617,7 +617,8 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
     float *Kw = reinterpret_cast<float *>(smem + L.k) + warp * S * 32;
     float4 *PLw = reinterpret_cast<float4 *>(smem + L.pl) + warp * 32;
     float *LMw = reinterpret_cast<float *>(smem + L.lm) + warp * 16;
-    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (FZMAX + 1);   // (pass 1: L.lostride == FZMAX + 1)
+    // (pass 1: L.lostride == FZMAX + 1, a compile-time stride, except with 4 line-table copies)
+    unsigned *LOw = reinterpret_cast<unsigned *>(smem + L.lo) + warp * (LTC == 4 ? L.lostride : FZMAX + 1);
     const float4 *ZS = reinterpret_cast<const float4 *>(smem + L.zs);
     const float4 *ZC = reinterpret_cast<const float4 *>(smem + L.zc);
     const int *ZB = reinterpret_cast<const int *>(smem + L.zb);
@@ -1093,7 +1094,12 @@ __device__ __forceinline__ void p1_row(const FArgs &a, const FItem &it, const P1
                 FCHECK((s < ns || s == dummy) && nadd <= 32 * XV);
                 const unsigned la = lt_s + (unsigned)(s * (4 * LTSW) + e * 4 * LTC);
                 int raw;
-                if constexpr (LTC == 2) {
+                if constexpr (LTC == 4) {
+                    int r0, r1, r2, r3;
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3) : "r"(la));
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(la), "r"(0) : "memory");
+                    raw = (r0 + r1) + (r2 + r3);
+                } else if constexpr (LTC == 2) {
                     int r0, r1;
                     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(r0), "=r"(r1) : "r"(la));
                     asm volatile("st.shared.v2.u32 [%0], {%1, %1};" ::"r"(la), "r"(0) : "memory");
@@ -1221,7 +1227,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_p1f(FArgs a) {
         for (int k = 0; k < 4; ++k) {
             const int l = (k + q4) & 3;
             pl.lts[k] = (unsigned)__cvta_generic_to_shared(LT + warp * S * LTSW) + 4u * LTC * (2u * (unsigned)l + ((lane >> 2) & 1)) +
-                        (LTC == 2 ? 4u * (unsigned)((lane >> 4) & 1) : 0u);
+                        (LTC == 2 ? 4u * (unsigned)((lane >> 4) & 1) : LTC == 4 ? 4u * (unsigned)((lane >> 3) & 3) : 0u);
         }
     };
     // the warp's record-ring mbarriers (one arrival: lane 0's expect_tx; the bulk copy's bytes)
