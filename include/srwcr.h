@@ -135,7 +135,11 @@ srwcr_status srwcr_eval(srwcr_ctx *ctx, const double *params, double *value, dou
  *                     srwcr_stats_buffer (device, fp64, `count` values) which the
  *                     caller must sum over ranks in place (e.g. an all-reduce);
  *   srwcr_eval_end    combines and runs pass 2 on this rank's slab; grad receives
- *                     this rank's PARTIAL gradient, which the caller sums over ranks. */
+ *                     this rank's PARTIAL gradient, which the caller sums over ranks.
+ *                     It first waits for all work on the device (cudaDeviceSynchronize), so
+ *                     the caller's writes of the summed statistics on any stream -- or a
+ *                     pageable cudaMemcpy, whose DMA may still be in flight when it returns --
+ *                     have landed. */
 srwcr_status srwcr_eval_begin(srwcr_ctx *ctx, const double *params);
 srwcr_status srwcr_stats_buffer(srwcr_ctx *ctx, double **dev_ptr, size_t *count);
 srwcr_status srwcr_eval_end(srwcr_ctx *ctx, double *value, double *grad);

@@ -24,6 +24,15 @@
 
 using namespace srwcr;
 
+// Host -> device copy of create-time (and other host-built) tables: a pageable cudaMemcpy may
+// return before its DMA has landed, and the kernels that read these tables run on the
+// context's non-blocking stream, which does not wait for the legacy stream -- so wait for the
+// device (under contention from another process the race was real: wrong line lists)
+static cudaError_t h2d_sync(void *dst, const void *src, size_t bytes) {
+    const cudaError_t e = cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice);
+    return e != cudaSuccess ? e : cudaDeviceSynchronize();
+}
+
 // ------------------------------------------------------------------ NCCL (dlopen)
 namespace {
 struct NcclApi {
@@ -140,7 +149,7 @@ struct srwcr_ctx {
     cudaEvent_t pex[12]{};                 //   priority decreasing with j (upload / prep / part-done events)
     bool fconc = false;                    //   (concurrent parts, no drain at the boundaries)
     bool fconc2 = false;                   //   (pass 2 too)
-    int xparts = 1;                        // exact-path lists of the last evaluation (pinned + 2)
+    int xparts = 1;                        // exact-path lists of the last evaluation (pinned + 4)
     int *xbeg = nullptr;
     // pass 1 in parts: items [p1_b[j], p1_b[j+1]) need params layers [0, p1_l[j]); pass 2 in
     // parts: after items [0, p2_b[j+1]) the gradient layers [0, p2_l[j]) are final
@@ -558,7 +567,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     CK(cudaMalloc(&d_it, sizeof(Item) * n));
     CK(cudaMalloc(&d_mask, sizeof(unsigned) * 4 * n));
     CK(cudaMalloc(&d_sum, sizeof(double) * n));
-    CK(cudaMemcpy(d_it, its.data(), sizeof(Item) * n, cudaMemcpyHostToDevice));
+    CK(h2d_sync(d_it, its.data(), sizeof(Item) * n));
     k_item_scan<<<(unsigned)n, 256, 0, c->stream>>>(c->F, c->M, d_it, g, d_mask, d_sum);
     CKL();
     std::vector<unsigned> mask(4 * n);
@@ -615,11 +624,11 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     if (W == 0) return SRWCR_OK;
     // device copies
     CK(cudaMalloc(&c->fitems, sizeof(FItem) * n));
-    CK(cudaMemcpy(c->fitems, fi.data(), sizeof(FItem) * n, cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->fitems, fi.data(), sizeof(FItem) * n));
     CK(cudaMalloc(&c->fitemw, sizeof(ItemW) * n));
-    CK(cudaMemcpy(c->fitemw, w.data(), sizeof(ItemW) * n, cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->fitemw, w.data(), sizeof(ItemW) * n));
     CK(cudaMalloc(&c->fslotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
-    CK(cudaMemcpy(c->fslotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->fslotbins, slotbins.data(), sizeof(int) * slotbins.size()));
     CK(cudaMalloc(&c->fiflag, sizeof(int) * n));
     CK(cudaMemset(c->fiflag, 0, sizeof(int) * n));
     const long long slab = (c->z1 - c->z0) * (long long)g.nxy;
@@ -634,7 +643,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     unsigned *d_cnt = nullptr;
     CK(cudaMalloc(&d_iol, sizeof(int) * lines));
     CK(cudaMalloc(&d_cnt, sizeof(unsigned) * lines));
-    CK(cudaMemcpy(d_iol, iol.data(), sizeof(int) * lines, cudaMemcpyHostToDevice));
+    CK(h2d_sync(d_iol, iol.data(), sizeof(int) * lines));
     CK(cudaMalloc(&c->frmask, sizeof(uint4) * rows));
     CK(cudaMemset(c->frmask, 0, sizeof(uint4) * rows));
     const unsigned lb = (unsigned)((lines * 32 + 255) / 256);
@@ -647,7 +656,7 @@ static srwcr_status build_fast(srwcr_ctx *c, int nsm) {
     off[0] = 0;
     for (long long i = 0; i < lines; ++i) off[i + 1] = off[i] + cnt[i];
     CK(cudaMalloc(&c->floff, sizeof(unsigned) * (lines + 1)));
-    CK(cudaMemcpy(c->floff, off.data(), sizeof(unsigned) * (lines + 1), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->floff, off.data(), sizeof(unsigned) * (lines + 1)));
     CK(cudaMalloc(&c->flent, sizeof(unsigned) * std::max<unsigned>(1, off[lines])));
     if (XV == 2) k_lists<2><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, nullptr, c->floff, c->flent, reinterpret_cast<unsigned *>(c->frmask), lines, 1);
     else k_lists<1><<<lb, 256, 0, c->stream>>>(c->frec, c->fitems, (int)n, g, (int)c->z0, d_iol, nullptr, c->floff, c->flent, reinterpret_cast<unsigned *>(c->frmask), lines, 1);
@@ -1038,7 +1047,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaSetDevice(c->dev));
     CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&c->ev[i]));
-    CK(cudaMallocHost(&c->pinned, (2 + NPART / 2) * sizeof(double)));   // D, #retained, then NPART int counts
+    CK(cudaMallocHost(&c->pinned, (4 + NPART / 2) * sizeof(double)));   // a copy of Dout (D, #retained, ..., counts)
     CK(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
     for (int i = 0; i < 4; ++i) CK(cudaEventCreateWithFlags(&c->pev[i], cudaEventDisableTiming));
     {   // part streams: the earlier part's CTAs are dispatched first, a later part fills the SMs
@@ -1050,7 +1059,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     }
     for (int i = 0; i < 12; ++i) CK(cudaEventCreateWithFlags(&c->pex[i], cudaEventDisableTiming));
     CK(cudaMalloc(&c->xbeg, sizeof(int)));
-    memset(c->pinned, 0, (2 + NPART / 2) * sizeof(double));
+    memset(c->pinned, 0, (4 + NPART / 2) * sizeof(double));
 
     // per-axis tables (fp64 on host -> device), control and spatial lattices
     for (int ax = 0; ax < 3; ++ax) {
@@ -1060,17 +1069,17 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         CK(cudaMalloc(&c->cb[ax], sizeof(int) * dims[ax]));
         CK(cudaMalloc(&c->cw[ax], sizeof(float4) * dims[ax]));
         CK(cudaMalloc(&c->cw64[ax], sizeof(double4) * dims[ax]));
-        CK(cudaMemcpy(c->cw64[ax], w64.data(), sizeof(double4) * dims[ax], cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->cb[ax], c->h_cb[ax].data(), sizeof(int) * dims[ax], cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->cw[ax], w.data(), sizeof(float4) * dims[ax], cudaMemcpyHostToDevice));
+        CK(h2d_sync(c->cw64[ax], w64.data(), sizeof(double4) * dims[ax]));
+        CK(h2d_sync(c->cb[ax], c->h_cb[ax].data(), sizeof(int) * dims[ax]));
+        CK(h2d_sync(c->cw[ax], w.data(), sizeof(float4) * dims[ax]));
         const bool deg = c->kcells[ax] == 0;
         c->Delta[ax] = deg ? 0.0 : (double)dims[ax] / (double)c->kcells[ax];
         build_axis(dims[ax], c->Delta[ax], deg, c->h_sb[ax], w);
         c->h_sw[ax] = w;
         CK(cudaMalloc(&c->sb[ax], sizeof(int) * dims[ax]));
         CK(cudaMalloc(&c->sw[ax], sizeof(float4) * dims[ax]));
-        CK(cudaMemcpy(c->sb[ax], c->h_sb[ax].data(), sizeof(int) * dims[ax], cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(c->sw[ax], w.data(), sizeof(float4) * dims[ax], cudaMemcpyHostToDevice));
+        CK(h2d_sync(c->sb[ax], c->h_sb[ax].data(), sizeof(int) * dims[ax]));
+        CK(h2d_sync(c->sw[ax], w.data(), sizeof(float4) * dims[ax]));
     }
     // max lanes sharing a control x-base inside a 32-lane chunk -> segmented-reduction steps
     // volumes: upload (host or device source) and normalise
@@ -1086,7 +1095,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         float *dst = v == 0 ? c->F : c->M;
         CK(cudaMemcpy(raw, src, sizeof(float) * nvox, cudaMemcpyDefault));
         int init[2] = {0x7f800000, (int)(0xff800000u ^ 0x7fffffffu)};
-        CK(cudaMemcpy(mm, init, sizeof init, cudaMemcpyHostToDevice));
+        CK(h2d_sync(mm, init, sizeof init));
         k_minmax<<<296, 256>>>(raw, nvox, reinterpret_cast<float *>(mm));
         CKL();
         int key[2];
@@ -1280,7 +1289,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         CK(cudaMalloc(&d_it, sizeof(Item) * n));
         CK(cudaMalloc(&d_mask, sizeof(unsigned) * 4 * n));
         CK(cudaMalloc(&d_sum, sizeof(double) * n));
-        CK(cudaMemcpy(d_it, its.data(), sizeof(Item) * n, cudaMemcpyHostToDevice));
+        CK(h2d_sync(d_it, its.data(), sizeof(Item) * n));
         k_item_scan<<<(unsigned)n, 256>>>(c->F, c->M, d_it, g, d_mask, d_sum);
         CKL();
         std::vector<unsigned> mask(4 * n);
@@ -1332,7 +1341,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
                 }
         }
         CK(cudaMalloc(dw, sizeof(ItemW) * n));
-        CK(cudaMemcpy(*dw, w.data(), sizeof(ItemW) * n, cudaMemcpyHostToDevice));
+        CK(h2d_sync(*dw, w.data(), sizeof(ItemW) * n));
         return SRWCR_OK;
     };
     TRY(scan_items(items, &c->itemw, false));
@@ -1345,17 +1354,17 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     c->S = smax + (c->MC ? 1 : 0);   // MC: + the binless slot
     c->S2 = s2max;
     CK(cudaMalloc(&c->slotbins, sizeof(int) * std::max<size_t>(1, slotbins.size())));
-    CK(cudaMemcpy(c->slotbins, slotbins.data(), sizeof(int) * slotbins.size(), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->slotbins, slotbins.data(), sizeof(int) * slotbins.size()));
     if (c->nitems) {
         CK(cudaMalloc(&c->items, sizeof(Item) * items.size()));
-        CK(cudaMemcpy(c->items, items.data(), sizeof(Item) * items.size(), cudaMemcpyHostToDevice));
+        CK(h2d_sync(c->items, items.data(), sizeof(Item) * items.size()));
     }
     if (c->nitems2) {
         CK(cudaMalloc(&c->items2, sizeof(Item) * items2.size()));
-        CK(cudaMemcpy(c->items2, items2.data(), sizeof(Item) * items2.size(), cudaMemcpyHostToDevice));
+        CK(h2d_sync(c->items2, items2.data(), sizeof(Item) * items2.size()));
     }
     CK(cudaMalloc(&c->items_full, sizeof(Item) * items_full.size()));
-    CK(cudaMemcpy(c->items_full, items_full.data(), sizeof(Item) * items_full.size(), cudaMemcpyHostToDevice));
+    CK(h2d_sync(c->items_full, items_full.data(), sizeof(Item) * items_full.size()));
 
     // buffers
     const long long RB = c->R * g.B;
@@ -1368,8 +1377,6 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         c->xcap = (int)std::min<int64_t>(std::max<int64_t>(4096, sv / 16), 1 << 30);
         if (const char *e = getenv("SRWCR_XCAP")) c->xcap = std::max(1, atoi(e));  // tests: force the scan fallback
         CK(cudaMalloc(&c->xlist, sizeof(int) * (size_t)c->xcap));
-        CK(cudaMalloc(&c->xcount, NPART * sizeof(int)));   // [0]: the list's count ([1..]: pipelined parts)
-        CK(cudaMemset(c->xcount, 0, NPART * sizeof(int)));
     }
     CK(cudaMalloc(&c->MG, sizeof(float4) * (size_t)std::max<int64_t>(1, (c->z1 - c->z0) * (int64_t)g.nxy)));
     CK(cudaMalloc(&c->params64, sizeof(double) * c->nparams));
@@ -1384,8 +1391,11 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     CK(cudaMalloc(&c->S_out, sizeof(double) * RB));
     CK(cudaMalloc(&c->dterm, sizeof(double) * c->R));
     CK(cudaMalloc(&c->reg, sizeof(double) * c->R * 6));
-    CK(cudaMalloc(&c->Dout, sizeof(double) * 4));   // D, #retained, gradient bound (fast pass 2)
-    CK(cudaMemset(c->Dout, 0, sizeof(double) * 4));
+    // D, #retained, gradient bound (fast pass 2), spare, then the exact-path list counts
+    // (xcount: [0] the list, [1..] the pipelined parts): one 64-byte copy returns them all
+    CK(cudaMalloc(&c->Dout, sizeof(double) * (4 + NPART / 2)));
+    CK(cudaMemset(c->Dout, 0, sizeof(double) * (4 + NPART / 2)));
+    c->xcount = reinterpret_cast<int *>(c->Dout + 4);
     CK(cudaMalloc(&c->ticket, sizeof(unsigned)));
     CK(cudaMalloc(&c->dpart, sizeof(double) * 3 * (size_t)std::min<int64_t>((c->R + 7) / 8, 148 * 8)));
     CK(cudaMemset(c->ticket, 0, sizeof(unsigned)));
@@ -1470,7 +1480,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
     {
         std::vector<float> sh(g.B);
         for (int b = 0; b < g.B; ++b) sh[b] = (float)b;
-        CK(cudaMemcpy(c->shiftc, sh.data(), sizeof(float) * g.B, cudaMemcpyHostToDevice));
+        CK(h2d_sync(c->shiftc, sh.data(), sizeof(float) * g.B));
         if (o.moment_shift) {
             CK(cudaMemsetAsync(c->SQ, 0, sizeof(double) * stats_count(c), c->stream));
             TRY(launch_pass1(c, false, true));
@@ -1495,7 +1505,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         NBox *d_nb = nullptr;
         unsigned long long *Ni = nullptr, *Ci = nullptr;
         CK(cudaMalloc(&d_nb, sizeof(NBox) * nb));
-        CK(cudaMemcpy(d_nb, c->h_nboxes.data(), sizeof(NBox) * nb, cudaMemcpyHostToDevice));
+        CK(h2d_sync(d_nb, c->h_nboxes.data(), sizeof(NBox) * nb));
         CK(cudaMalloc(&Ni, sizeof(unsigned long long) * 2 * RB));
         CK(cudaMalloc(&Ci, sizeof(unsigned long long) * 4 * g.B));
         CK(cudaMemsetAsync(Ni, 0, sizeof(unsigned long long) * 2 * RB, c->stream));
@@ -1532,7 +1542,7 @@ static srwcr_status create_impl(srwcr_ctx *c, const float *fixed, const float *m
         NCK(nccl().Broadcast(c->shiftc, c->shiftc, (size_t)g.B, ncclFloat32, 0, c->comm, c->stream));
         double *zb = nullptr;
         CK(cudaMalloc(&zb, sizeof(double)));
-        CK(cudaMemcpy(zb, &c->Z, sizeof(double), cudaMemcpyHostToDevice));
+        CK(h2d_sync(zb, &c->Z, sizeof(double)));
         NCK(nccl().Broadcast(zb, zb, 1, ncclFloat64, 0, c->comm, c->stream));
         CK(cudaStreamSynchronize(c->stream));
         CK(cudaMemcpy(&c->Z, zb, sizeof(double), cudaMemcpyDeviceToHost));
@@ -1658,8 +1668,7 @@ static srwcr_status eval_end_enqueue(srwcr_ctx *c, double *grad, bool reduce_gra
         }
     }
     if (c->timing) CK(record_ev(c, 3));
-    CK(cudaMemcpyAsync(c->pinned, c->Dout, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
-    if (grad) CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(c->pinned, c->Dout, (grad ? 4 + NPART / 2 : 2) * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     if (grad && !grad_dev) CK(cudaMemcpyAsync(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost, c->stream));
     return SRWCR_OK;
 }
@@ -1804,13 +1813,13 @@ static srwcr_status eval_host_pipelined(srwcr_ctx *c, const double *params, doub
             TRY(launch_pass2(c, c->grad64));
             TRY(copy_layers(grad, c->grad64, 0, g.GzExt, cudaMemcpyDeviceToHost, c->stream));
         }
-        CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->pinned + 4, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     }
     CK(cudaStreamSynchronize(c->cstream));
     CK(cudaStreamSynchronize(c->stream));
     if (parts2) {   // list overflow: the last launch scanned the whole slab, after the early
         int xc = 0;   // gradient layers had gone back -- copy the whole gradient again
-        memcpy(&xc, c->pinned + 2, sizeof(int));
+        memcpy(&xc, c->pinned + 4, sizeof(int));
         if (xc > c->xcap) CK(cudaMemcpy(grad, c->grad64, sizeof(double) * c->nparams, cudaMemcpyDeviceToHost));
     }
     return eval_finish(c, value);
@@ -1918,7 +1927,7 @@ static srwcr_status enqueue_host_pipelined_fast(srwcr_ctx *c, const double *para
                 done = std::max(done, hi);
             }
             for (int j = 0; j < np2; ++j) CK(cudaStreamWaitEvent(c->stream, c->pex[j], 0));
-            CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, NPART * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(c->pinned + 4, c->xcount, NPART * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         } else {
         CK(cudaMemsetAsync(c->xcount, 0, sizeof(int), c->stream));
         CK(cudaMemsetAsync(c->xbeg, 0, sizeof(int), c->stream));
@@ -1945,7 +1954,7 @@ static srwcr_status enqueue_host_pipelined_fast(srwcr_ctx *c, const double *para
             }
             done = std::max(done, hi);
         }
-        CK(cudaMemcpyAsync(c->pinned + 2, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(c->pinned + 4, c->xcount, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
         }
     }
     // join the copy stream back (a graph capture must end on its origin stream)
@@ -1999,7 +2008,7 @@ static srwcr_status eval_host_pipelined_fast(srwcr_ctx *c, const double *params,
     CK(cudaStreamSynchronize(c->stream));
     if (grad) {
         int xc[NPART] = {};
-        memcpy(xc, c->pinned + 2, sizeof xc);
+        memcpy(xc, c->pinned + 4, sizeof xc);
         const int np2 = (int)c->fp2_l.size();
         bool over = xc[0] > c->xcap;
         if (c->fconc2 && np2 <= NPART) {
@@ -2055,6 +2064,9 @@ extern "C" srwcr_status srwcr_eval_end(srwcr_ctx *c, double *value, double *grad
     if (!c) return SRWCR_EINVAL;
     if (!c->begun) return fail(c, SRWCR_ESTATE, "srwcr_eval_end without srwcr_eval_begin");
     c->begun = false;
+    // the caller summed the statistics in place, possibly with copies on another stream or a
+    // pageable cudaMemcpy whose DMA can still be in flight when it returns: wait for all of it
+    CK(cudaDeviceSynchronize());
     c->xparts = 1;
     return eval_end_impl(c, value, grad, false);
 }
@@ -2163,7 +2175,7 @@ extern "C" srwcr_status srwcr_get_stats(const srwcr_ctx *c, srwcr_stats *out) {
     out->pipe_items1 = c->p1_split;
     out->pipe_items2 = c->p2_split;
     out->exact_voxels = 0;
-    for (int j = 0; c->pinned && j < c->xparts; ++j) out->exact_voxels += reinterpret_cast<const int *>(c->pinned + 2)[j];
+    for (int j = 0; c->pinned && j < c->xparts; ++j) out->exact_voxels += reinterpret_cast<const int *>(c->pinned + 4)[j];
     out->fast_path = c->fast ? 1 : 0;
     out->fast_items = c->nfitems;
     out->fast_warps = c->fW;
@@ -2194,7 +2206,7 @@ extern "C" void srwcr_destroy(srwcr_ctx *c) {
     for (int i = 0; i < NPART; ++i)
         if (c->kst[i]) cudaStreamDestroy(c->kst[i]);
     if (c->cstream) cudaStreamDestroy(c->cstream);
-    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->xcount, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
+    void *bufs[] = {c->F, c->M, c->phi, c->phimax, c->MG, c->xlist, c->params64, c->grad64, c->items, c->items_full, c->items2, c->itemw, c->itemw_full,
                     c->slotbins, c->SQ, c->Nlo, c->Nup, c->dterm, c->reg, c->Dout, c->S_out, c->shiftc, c->alpha,
                     c->beta, c->gamma, c->ticket, c->dpart, c->xbeg, c->fitems, c->fitemw, c->fslotbins,
                     c->fiflag, c->frec, c->floff, c->flent, c->frmask, c->SQi, c->gradi, c->fMv, c->fphi4, c->halo_recv};

@@ -100,6 +100,9 @@ def _h2d(p, h):
     import ctypes
     h = np.ascontiguousarray(h)
     assert _cudart().cudaMemcpy(ctypes.c_void_p(p), h.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(h.nbytes), 1) == 0
+    # a pageable H2D cudaMemcpy may return before its DMA has landed: complete it (the library's
+    # srwcr_eval_end waits for the device too)
+    assert _cudart().cudaDeviceSynchronize() == 0
 
 
 @pytest.mark.parametrize("halo", [False, True])
